@@ -1,0 +1,167 @@
+"""Oracle invariants and brute-force argmax.
+
+Properties that must hold at any size: conservation, monotone lifecycle,
+TTFT independent of decode cap and of fabric bandwidth (static), TPOT
+strictly larger at lower bandwidth, met monotone in SLO slack,
+attainment recount, determinism, and argmax = brute force
+over every pool-uniform allocation of tiny nodes (north_star).
+"""
+import numpy as np
+import pytest
+
+import oracle
+from workloads import DEFAULT_POLICY, DEFAULT_SLO, make_trace, static_candidates
+
+
+def rep(model, n, xpd, tr, qps, slo=DEFAULT_SLO, budget=None, pol=DEFAULT_POLICY):
+    role, cap = static_candidates(n, [xpd])
+    return oracle.replay(model, role[0], cap[0], pol, budget or 750 * n, slo, tr, qps)
+
+
+@pytest.mark.parametrize("family", ["lb", "lb_bursty"])
+@pytest.mark.parametrize("qps", [0.5, 1.5, 3.0])
+def test_conservation_and_lifecycle(model, family, qps):
+    tr = make_trace(family, 2, 600)
+    r = rep(model, 8, (4, 675, 525), tr, qps)
+    a = tr["s_unit"] * (1.0 / (qps * 8.0))
+    assert np.all(np.isfinite(r["completion"]))
+    assert np.all(r["prefill_end"] > a)
+    assert np.all(r["transfer_end"] > r["prefill_end"])
+    assert np.all(r["completion"] >= r["transfer_end"])
+    assert np.all(r["tpot"] >= 0)
+    # attainment recount from raw records
+    ts = np.where(tr["phase"] == 1, DEFAULT_SLO["tpot"][1], DEFAULT_SLO["tpot"][0])
+    met = int(((r["ttft"] <= DEFAULT_SLO["ttft"]) & (r["tpot"] <= ts)).sum())
+    assert r["met"] == met
+    dur = r["completion"].max() - a[0]
+    assert r["duration"] == dur and r["goodput"] == met / dur
+
+
+def test_ttft_independent_of_decode_and_fabric(model):
+    # S:274 TTFT independent of fabric; static: decode state never feeds back into prefill
+    tr = make_trace("lb", 4, 800)
+    base = rep(model, 8, (5, 600, 400), tr, 2.0)
+    for d in (450, 500, 600):
+        other = rep(model, 8, (5, 600, d), tr, 2.0)
+        assert np.array_equal(base["prefill_end"], other["prefill_end"])
+        assert np.array_equal(base["transfer_end"], other["transfer_end"])
+    slow = rep(dict(model, bw=24e9), 8, (5, 600, 400), tr, 2.0)
+    assert np.array_equal(base["prefill_end"], slow["prefill_end"])
+    # TPOT strictly larger at lower bandwidth for every request with out >= 2
+    # (checked at low load where the decode stage has no queueing interaction)
+    tr2 = make_trace("lb", 4, 200)
+    b2 = rep(model, 8, (4, 600, 600), tr2, 0.05)
+    s2 = rep(dict(model, bw=24e9), 8, (4, 600, 600), tr2, 0.05)
+    mask = tr2["out_tok"] >= 2
+    assert np.all(s2["tpot"][mask] > b2["tpot"][mask])
+    assert np.array_equal(b2["ttft"], s2["ttft"])
+
+
+def test_met_monotone_in_slo_slack(model):
+    tr = make_trace("lb", 6, 500)
+    for qps in (1.0, 2.0):
+        r1 = rep(model, 8, (4, 700, 500), tr, qps, slo={"ttft": 0.5, "tpot": (0.02, 0.02)})
+        r2 = rep(model, 8, (4, 700, 500), tr, qps, slo={"ttft": 1.0, "tpot": (0.04, 0.04)})
+        r4 = rep(model, 8, (4, 700, 500), tr, qps, slo={"ttft": 2.0, "tpot": (0.08, 0.08)})
+        assert r1["met"] <= r2["met"] <= r4["met"]
+        assert np.array_equal(r1["completion"], r4["completion"])   # trajectory SLO-independent
+
+
+def test_determinism(model):
+    tr = make_trace("lb_bursty", 9, 700)
+    a = rep(model, 8, (3, 725, 425), tr, 1.75)
+    b = rep(model, 8, (3, 725, 425), tr, 1.75)
+    for k in ("ttft", "tpot", "prefill_end", "completion", "transfer_end"):
+        assert a[k].tobytes() == b[k].tobytes()
+    ev = oracle.evaluate(model, *static_candidates(8, [(3, 725, 425), (4, 600, 600)]),
+                         [DEFAULT_POLICY] * 2, 4800, DEFAULT_SLO, [tr, make_trace("lb", 1, 300)],
+                         [1.0, 2.0], n_threads=4)
+    ev2 = oracle.evaluate(model, *static_candidates(8, [(3, 725, 425), (4, 600, 600)]),
+                          [DEFAULT_POLICY] * 2, 4800, DEFAULT_SLO, [tr, make_trace("lb", 1, 300)],
+                          [1.0, 2.0], n_threads=1)
+    for k in ev:
+        assert ev[k].tobytes() == ev2[k].tobytes()
+
+
+def test_evaluate_matches_replays(model):
+    trs = [make_trace("lb", s, 150) for s in range(3)]
+    xpd = [(2, 700, 550), (4, 600, 600), (6, 500, 700)]
+    role, cap = static_candidates(8, xpd)
+    qps = [0.75, 2.5]
+    ev = oracle.evaluate(model, role, cap, [DEFAULT_POLICY] * 3, 4800, DEFAULT_SLO, trs, qps,
+                         n_threads=3, per_replay=True)
+    for c in range(3):
+        for q in range(2):
+            g = 0.0
+            m = 0
+            for s in range(3):
+                r = oracle.replay(model, role[c], cap[c], DEFAULT_POLICY, 4800, DEFAULT_SLO, trs[s], qps[q])
+                assert ev["rep_met"][c, q, s] == r["met"]
+                m += r["met"]
+                g += r["goodput"]
+            assert ev["met"][c, q] == m and ev["goodput"][c, q] == g
+
+
+@pytest.mark.parametrize("N,B", [(2, 1200), (2, 1400), (3, 1500), (3, 1800)])
+def test_argmax_brute_force_tiny_nodes(model, N, B):
+    # every pool-uniform allocation on a 25 W grid, enumerated independently here
+    cands = [(x, p, d) for x in range(1, N) for p in range(400, 751, 25) for d in range(400, 751, 25)
+             if x * p + (N - x) * d <= B]
+    role, cap = static_candidates(N, cands)
+    trs = [make_trace("lb", 20 + s, 40) for s in range(2)]
+    qps = [0.5, 1.5, 3.0]
+    ev = oracle.evaluate(model, role, cap, [DEFAULT_POLICY] * len(cands), B, DEFAULT_SLO, trs, qps,
+                         n_threads=4)
+    for q, qv in enumerate(qps):
+        best = None
+        for c, (x, p, d) in enumerate(cands):
+            m = sum(oracle.replay(model, role[c], cap[c], DEFAULT_POLICY, B, DEFAULT_SLO, t, qv)["met"]
+                    for t in trs)
+            key = (-m, x * p + (N - x) * d, c)
+            best = key if best is None or key < best else best
+        assert ev["argmax"][q] == best[2]
+        assert ev["met"][best[2], q] == -best[0]
+
+
+def test_validation_errors(model):
+    tr = make_trace("lb", 0, 10)
+    role, cap = static_candidates(8, [(4, 700, 600)])
+    with pytest.raises(oracle.OracleError) as e:          # Σcaps 5200 > 4800
+        oracle.replay(model, role[0], cap[0], DEFAULT_POLICY, 4800, DEFAULT_SLO, tr, 1.0)
+    assert e.value.rc == -3
+    role, cap = static_candidates(8, [(4, 350, 600)])
+    with pytest.raises(oracle.OracleError) as e:          # cap outside [400, 750]
+        oracle.replay(model, role[0], cap[0], DEFAULT_POLICY, 4800, DEFAULT_SLO, tr, 1.0)
+    assert e.value.rc == -2
+    role = np.zeros(8, np.uint8)
+    with pytest.raises(oracle.OracleError) as e:          # no decode GPU
+        oracle.replay(model, role, np.full(8, 600, np.int32), DEFAULT_POLICY, 4800, DEFAULT_SLO, tr, 1.0)
+    assert e.value.rc == -4
+    bad = dict(model, decode=[(400, 1.0), (500, 0.9), (750, 1.45)])
+    role, cap = static_candidates(8, [(4, 600, 600)])
+    with pytest.raises(oracle.OracleError) as e:          # non-monotone anchors
+        oracle.replay(bad, role[0], cap[0], DEFAULT_POLICY, 4800, DEFAULT_SLO, tr, 1.0)
+    assert e.value.rc == -5
+    tr0 = dict(tr, in_tok=np.zeros(10, np.int32))
+    with pytest.raises(oracle.OracleError) as e:          # zero tokens
+        oracle.replay(model, role[0], cap[0], DEFAULT_POLICY, 4800, DEFAULT_SLO, tr0, 1.0)
+    assert e.value.rc == -6
+
+
+def test_empty_trace(model):
+    tr = {"s_unit": np.zeros(0), "in_tok": np.zeros(0, np.int32), "out_tok": np.zeros(0, np.int32),
+          "phase": np.zeros(0, np.uint8)}
+    r = rep(model, 8, (4, 600, 600), tr, 1.0)
+    assert r["met"] == 0 and r["goodput"] == 0.0 and r["duration"] == 0.0   # S:417 D12
+
+
+def test_static_orderings_smoke(model):
+    # SPEC acceptance #5/#6 (calibration-dependent; smoke, not parity)
+    trs = [make_trace("lb", s, 2000) for s in range(3)]
+    def att(xpd, slo, qps, budget=4800):
+        return sum(rep(model, 8, xpd, t, qps, slo=slo, budget=budget)["met"] for t in trs)
+    slo40 = DEFAULT_SLO
+    a_nu = att((4, 750, 450), slo40, 1.5)
+    a_53 = att((5, 600, 600), slo40, 1.5)
+    a_44 = att((4, 600, 600), slo40, 1.5)
+    assert a_nu >= a_44 and a_53 >= a_44
