@@ -1,0 +1,243 @@
+/*
+ * padsim.h — C ABI of the B200-native what-if evaluator for power-aware
+ * prefill/decode disaggregation ("Power Aware Dynamic Reallocation For
+ * Inference", arXiv 2601.12241; /root/reference/PAPER.md cited "P:<line>",
+ * SPEC.md cited "S:<line>", readings "A<n>"/"c.N" = SURVEY.md §8(c) and
+ * DESIGN.md §3).
+ *
+ * What it computes (BASELINE.json north_star; SURVEY.md §8(a) rows a1–a8):
+ * for every candidate allocation — an xPyD split of the node's GPUs into
+ * prefill and decode roles with per-GPU power caps under a node budget
+ * (P:129), optionally with the paper's dynamic reallocation policy
+ * (Algorithm 1) — replay every trace at every QPS point through
+ * the prefill/decode latency-and-power model, score
+ * every request against the TTFT/TPOT SLOs, reduce to SLO
+ * attainment and goodput per (candidate, QPS), and take the argmax per QPS.
+ *
+ * Conventions
+ *  - Every function is extern "C", returns int status (PADSIM_OK = 0, <0 =
+ *    error), never throws, never aborts.  padsim_last_error() gives a static
+ *    message for the last failure on that context.
+ *  - Input pointers are caller-owned HOST memory unless the parameter name
+ *    starts with "d_" (device memory); they are read during the call only.
+ *  - Output buffers are caller-allocated with the documented sizes.
+ *  - A padsim_ctx owns its device buffers (cudaMalloc) and is bound to one
+ *    CUDA device; it is not thread-safe (one ctx per host thread/stream).
+ *  - "stream" parameters are cudaStream_t passed as void* (NULL = default).
+ *  - All times are FP64 seconds, all powers int32 watts.  Results are
+ *    deterministic: bit-identical for identical inputs.
+ *  - There is no CPU fallback: without a usable CUDA device every compute
+ *    call fails with PADSIM_ECUDA.
+ */
+#ifndef PADSIM_H
+#define PADSIM_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PADSIM_MAX_GPUS 64      /* simulated GPUs per node (cfg 5: 64)          */
+#define PADSIM_MAX_ANCHORS 8    /* anchors per power->speedup curve             */
+#define PADSIM_MAX_SLOTS 32     /* KV request buffer bound (32)          */
+#define PADSIM_MAX_DECODE_BATCH 256
+#define PADSIM_MAX_PREFILL_BATCH 256
+
+enum {
+    PADSIM_OK = 0,
+    PADSIM_EINVAL = -1,   /* null pointer, bad size, bad policy field              */
+    PADSIM_ERANGE = -2,   /* a cap outside [min_w, max_w]            */
+    PADSIM_EBUDGET = -3,  /* Σ caps > budget; bad_index = first offender   */
+    PADSIM_EROLE = -4,    /* prefill or decode role count outside [1, N−1] */
+    PADSIM_EMODEL = -5,   /* anchors unsorted / non-monotone / not spanning
+                             [min_w,max_w] / first speedup != 1 / params <= 0
+                                                           */
+    PADSIM_EDOMAIN = -6,  /* token count < 1 or unsorted arrivals    */
+    PADSIM_ECUDA = -7,    /* CUDA runtime/kernel error or no device                */
+    PADSIM_ENOMEM = -8    /* host or device allocation failure                     */
+};
+
+typedef struct padsim_ctx padsim_ctx;
+
+/* a2 — one synthetic trace, sorted by arrival.  s_unit[i] are cumulative
+ * arrival times of a unit-rate process (first gap > 0 or 0); the arrival at
+ * QPS-per-GPU q on N GPUs is s_unit[i] * (1.0/(q*(double)N)) (A16).
+ * phase[i] ∈ {0,1} selects the per-phase TPOT SLO.  in_tok ≥ 1,
+ * out_tok ≥ 1 (the first output token comes from prefill).          */
+typedef struct {
+    int32_t n_req;
+    const double* s_unit;
+    const int32_t* in_tok;
+    const int32_t* out_tok;
+    const uint8_t* phase;    /* nullable: all phase 0 */
+} padsim_trace;
+
+/* A1 — piecewise-linear power->speedup curve (D1 S:92, D3 S:94):
+ * anchors strictly increasing in w, w[0] = min_w, w[n-1] = max_w,
+ * s non-decreasing, s[0] = 1.0.                                             */
+typedef struct { int32_t n; int32_t w[PADSIM_MAX_ANCHORS]; double s[PADSIM_MAX_ANCHORS]; } padsim_curve;
+
+/* a3 — latency/power model (c.1, defaults D2 S:93):
+ *   prefill_lat(T,b,w) = ((double)T / (rate*(1+eff*(b-1)))) / s_pre(w)
+ *   decode_lat(n,C,w)  = (fixed + per_seq*n [+ per_ctx*C]) / s_dec(w)
+ *   kv_lat(T)          = overhead + (T*kv_bytes)/fabric_bw                  */
+typedef struct {
+    int32_t min_w, max_w;              /* cap range (400–750 W)          */
+    padsim_curve prefill, decode;
+    double prefill_base_rate;          /* tokens/s at min_w, batch 1  (> 0)     */
+    double prefill_batch_eff;          /* per extra batch member      (>= 0)    */
+    double decode_fixed_s;             /* per step at min_w           (> 0)     */
+    double decode_per_seq_s;           /* per active sequence         (>= 0)    */
+    double decode_per_ctx_tok_s;       /* per active context token (>= 0; 0 = SPEC form, A15) */
+    double kv_bytes_per_token;         /* (> 0) Llama-3.1-8B: 131072     */
+    double fabric_bw_Bps;              /* (> 0)                                  */
+    double transfer_overhead_s;        /* (> 0)                                  */
+    int32_t max_prefill_batch;         /* [1, 256]  (A9: 16)                     */
+    int32_t prefill_token_budget;      /* >= 1      (16384)               */
+    int32_t max_decode_batch;          /* [1, 256]  (64)                  */
+    int32_t transfer_slots;            /* [1, 32]   (32)                  */
+} padsim_model;
+
+/* Algorithm 1 constants for one candidate.  kind: 0 static,
+ * 1 dyn-power, 2 dyn-gpu, 3 dyn-both.  For kind != 0:
+ * tick_s > 0 (MIN_TIME), settle_s > 0, reassign_s > 0
+ * (P:294), cooldown_s >= settle_s, window_s >= 0, power_step_w > 0,
+ * decode_ceiling_w ∈ [min_w, max_w], queue_threshold >= 0.        */
+typedef struct {
+    int32_t kind;
+    int32_t queue_threshold, power_step_w, decode_ceiling_w;
+    double cooldown_s, tick_s, window_s, settle_s, reassign_s;
+} padsim_policy;
+
+/* D7 — candidate set: n_cand rows of n_gpus entries.  role 0 = prefill,
+ * 1 = decode; cap_w = initial per-GPU cap.  policy[n_cand].               */
+typedef struct {
+    int32_t n_gpus, n_cand;
+    const uint8_t* role;
+    const int32_t* cap_w;
+    const padsim_policy* policy;
+} padsim_candidates;
+
+/* SLOs: inclusive ≤ (A6). All > 0.           */
+typedef struct { double ttft_s; double tpot_s[2]; } padsim_slo;
+typedef struct { int32_t budget_w; } padsim_budget;   /* node GPU budget */
+
+/* a7/a8 results.  met[c*n_qps+q] = Σ over traces of requests meeting both
+ * SLOs (int, exact); goodput = Σ over traces (ascending) of met/duration;
+ * near_boundary = requests within 1e-9 relative of an SLO; argmax[q] =
+ * candidate maximising (Σmet ↓, Σcaps ↑, index ↑) (A25).  Any pointer may
+ * be NULL.  bad_index: first offending candidate on EBUDGET/ERANGE/EROLE,
+ * else -1.                                                                  */
+typedef struct {
+    int64_t* met;
+    double* goodput;
+    int64_t* near_boundary;
+    int32_t* argmax;
+    int32_t bad_index;
+} padsim_result;
+
+/* ---- context ------------------------------------------------------------ */
+int padsim_create(int32_t cuda_device, padsim_ctx** out);
+void padsim_destroy(padsim_ctx* ctx);
+const char* padsim_last_error(const padsim_ctx* ctx);
+const char* padsim_version(void);
+
+/* ---- evaluate_allocations (north_star) ------------------------------------
+ * One-shot host API: validate, upload, run every replay (n_cand × n_qps ×
+ * n_traces), reduce, argmax, download.  Synchronous.  qps_per_gpu[n_qps] > 0.
+ */
+int padsim_evaluate_allocations(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
+                                const double* qps_per_gpu, int32_t n_qps,
+                                const padsim_model* model, const padsim_candidates* cands,
+                                const padsim_slo* slo, const padsim_budget* budget,
+                                padsim_result* out);
+
+/* ---- split API (inputs resident in HBM between calls) ---------------------
+ * padsim_plan: validate + upload inputs + precompute model tables (a3) on the
+ * device; synchronous; replaces any previous plan.  flags: PADSIM_RECORDS
+ * keeps per-request records (memory n_cand*n_qps*Σn_req*40 B).
+ * padsim_run: launch the replay, seed-reduction and argmax kernels on
+ * `stream`; asynchronous; results stay in ctx-owned device buffers.
+ * padsim_fetch: copy the last run's results to host (synchronises stream).
+ */
+#define PADSIM_RECORDS 1u
+int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
+                const double* qps_per_gpu, int32_t n_qps, const padsim_model* model,
+                const padsim_candidates* cands, const padsim_slo* slo,
+                const padsim_budget* budget, uint32_t flags, int32_t* bad_index);
+int padsim_run(padsim_ctx* ctx, void* stream);
+int padsim_fetch(padsim_ctx* ctx, void* stream, padsim_result* out);
+
+/* Device views of the last run's outputs (valid until the next plan/destroy):
+ * d_met i64[C*Q], d_goodput f64[C*Q], d_near i64[C*Q], d_argmax i32[Q],
+ * per replay r = (c*Q + q)*S + s: d_rep_met i32, d_rep_near i32,
+ * d_rep_duration f64, d_rep_goodput f64, d_rep_events i64 [C*Q*S].          */
+typedef struct {
+    int64_t* d_met; double* d_goodput; int64_t* d_near; int32_t* d_argmax;
+    int32_t* d_rep_met; int32_t* d_rep_near; double* d_rep_duration; double* d_rep_goodput;
+    int64_t* d_rep_events;
+    int32_t n_cand, n_qps, n_traces;
+} padsim_device_results;
+int padsim_get_device_results(padsim_ctx* ctx, padsim_device_results* out);
+
+/* Per-replay host copies (synchronises): arrays of C*Q*S, any may be NULL. */
+int padsim_fetch_replays(padsim_ctx* ctx, void* stream, int32_t* met, int32_t* near_boundary,
+                         double* duration, double* goodput, int64_t* events);
+
+/* Per-request records of the last run (plan flag PADSIM_RECORDS): for replay
+ * r = (c*Q + q)*S + s, request i at [r*R_max + i] where R_max = max n_req;
+ * arrays of C*Q*S*R_max, any may be NULL.                                   */
+int padsim_fetch_records(padsim_ctx* ctx, void* stream, double* ttft, double* tpot,
+                         double* prefill_end, double* completion, double* transfer_end,
+                         int32_t* r_max);
+
+/* a8 across ranks: argmax over a device met array (e.g. after an NCCL
+ * all-reduce of d_met) using the planned candidates' Σcaps; asynchronous.   */
+int padsim_argmax_device(padsim_ctx* ctx, void* stream, const int64_t* d_met, int32_t n_cand,
+                         int32_t n_qps, int32_t* d_argmax);
+
+/* ---- step_controller (north_star; Algorithm 1 body) -----------
+ * One controller decision, run on the device by the same __device__ code the
+ * dynamic replay kernel uses.  Guards of Alg. 1 on the window statistics
+ * (strict > / <), cooldown strict (A20), PowerLimitsReached checked
+ * before moving (A18), MovePower, MoveGPU of the least-loaded donor
+ * then DistributeUniformPower.  Mutates *state, writes
+ * *action.  Synchronous.                                                      */
+typedef struct {
+    uint8_t role[PADSIM_MAX_GPUS];      /* 0 prefill, 1 decode                  */
+    uint8_t draining[PADSIM_MAX_GPUS];  /* in neither pool (A26)                */
+    int32_t cmd_cap_w[PADSIM_MAX_GPUS]; /* commanded caps (targets)             */
+    int32_t n_gpus;
+    int32_t drain_pending;              /* a role change is in progress         */
+    double last_move_s;                 /* Alg.1 last_move_time         */
+} padsim_ctrl_state;
+typedef struct {
+    double ttft_stat_s, tpot_stat_s;    /* window p90 statistics (A22)          */
+    double ttft_slo_s, tpot_slo_s;      /* SLOs in effect               */
+    int32_t q_prefill;                  /* |Q_P| queued prompts         */
+    int32_t load[PADSIM_MAX_GPUS];      /* P: outstanding tokens, D: active+pending */
+} padsim_window_stats;
+typedef struct {
+    int32_t kind;                       /* 0 none, 1 move-power, 2 move-gpu, 3 saturated */
+    int32_t direction;                  /* 0 D->P, 1 P->D, -1 none              */
+    int32_t gpu;                        /* drained GPU (move-gpu) else -1       */
+    int32_t new_cap_w[PADSIM_MAX_GPUS]; /* caps once the move settles           */
+} padsim_action;
+int padsim_step_controller(padsim_ctx* ctx, const padsim_policy* policy,
+                           const padsim_budget* budget, const padsim_model* model,
+                           padsim_ctrl_state* inout, const padsim_window_stats* stats,
+                           double now_s, padsim_action* out);
+
+/* ---- a1 candidate enumeration (host) ----------------------------------------
+ * All pool-uniform (x, p, d): x ∈ [1, N−1] prefill GPUs at p W, N−x decode
+ * GPUs at d W, p,d ∈ {min_w + k·step_w} ∩ [min_w, max_w], x·p + (N−x)·d ≤ B
+ * (== B if exact).  Lexicographic (x, p, d) order.
+ * out_xpd may be NULL to count; *n_out = total count (may exceed cap).       */
+int padsim_enumerate_pool_uniform(int32_t n_gpus, int32_t budget_w, int32_t min_w, int32_t max_w,
+                                  int32_t step_w, int32_t exact, int32_t* out_xpd, int32_t cap,
+                                  int32_t* n_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,70 @@
+// common.cuh — device-side plan layout shared by the padsim kernels.
+//
+// Product code (never includes or links anything under oracle/).  Every
+// kernel is compiled with --fmad=false so each FP64 expression keeps the
+// operation order pinned in DESIGN.md §3 (c.1): no contraction into FMA,
+// IEEE round-to-nearest division and conversion.
+#pragma once
+#include <cstdint>
+
+#include "../../include/padsim.h"
+
+namespace padsim {
+
+constexpr int kThreads = 128;          // replays per CTA (4 warps)
+constexpr int kWarps = kThreads / 32;
+constexpr int kNoIdx = -1;
+
+// Device model: scalar parameters + precomputed tables (a3).
+struct DevModel {
+    int min_w, max_w, ncap;            // ncap = max_w - min_w + 1
+    double rate, eff, dec_fixed, dec_per_seq, dec_per_ctx, kvb, bw, ovh;
+    int max_pb, pb_tokens, max_db, slots;
+    const double* spre;                // [ncap]  s_pre(w)
+    const double* sdec;                // [ncap]  s_dec(w)
+    const double* den;                 // [max_pb+1] rate*(1+eff*(b-1))
+    const double* ltab;                // [ncap][max_db] decode step latency, n = 1..max_db
+};
+
+// Everything a replay kernel launch needs (passed by value as a kernel param).
+struct Plan {
+    DevModel m;
+    int N, C, Q, S, Rmax, B;
+    // traces: SoA, trace s occupies [toff[s], toff[s]+nreq[s]); toff multiple of 16
+    const long long* toff;
+    const int* nreq;
+    const double* s_unit;
+    const double* kv;                  // kv_lat(in_tok) per request (a3)
+    const int* in_tok;
+    const int* out_tok;
+    const unsigned char* phase;
+    // candidates
+    const unsigned char* role;         // [C][N]
+    const int* cap;                    // [C][N]
+    const padsim_policy* pol;          // [C]
+    const double* qps;                 // [Q]
+    double ttft_slo, tpot_slo0, tpot_slo1;
+    // replay subset for this launch: candidate list
+    const int* clist;                  // [n_clist]
+    int n_clist;
+    int items_per_trace;               // ceil(Q*n_clist / kThreads)
+    int n_items;
+    unsigned* work;                    // work counter (zeroed before launch)
+    // outputs per replay r = (c*Q + q)*S + s
+    int* rep_met;
+    int* rep_near;
+    double* rep_dur;
+    double* rep_good;
+    long long* rep_events;
+    // optional per-request records [r*Rmax + i]
+    double *rec_ttft, *rec_tpot, *rec_pe, *rec_comp, *rec_te;
+    // scratch: per CTA slot, lane-interleaved
+    char* scratch;
+    size_t scratch_per_cta;
+    size_t off_link, off_pe, off_mem, off_ordt, off_tst, off_tfl;   // per-warp offsets
+    size_t warp_bytes;
+    int smem_trace;                    // stage the trace in shared memory (TMA bulk)
+    size_t smem_trace_bytes;
+};
+
+}  // namespace padsim

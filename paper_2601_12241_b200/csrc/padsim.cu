@@ -1,0 +1,725 @@
+// padsim.cu — C ABI (include/padsim.h) of the B200-native what-if evaluator:
+// host validation + upload (plan), the model-table kernel (row a3), the
+// replay kernels (rows a4–a7, replay.cuh), the seed reduction and the
+// per-QPS argmax (row a8), the device controller step (row a6 ABI).
+//
+// Build: nvcc -O3 -gencode arch=compute_100a,code=sm_100a -lineinfo
+//        --fmad=false -Xcompiler -fPIC -shared
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "controller.cuh"
+#include "replay.cuh"
+
+using namespace padsim;
+
+struct padsim_ctx {
+    int device = 0;
+    int n_sm = 0;
+    std::string err;
+    // plan
+    bool planned = false;
+    uint32_t flags = 0;
+    int N = 0, C = 0, Q = 0, S = 0, Rmax = 0, B = 0;
+    padsim_model model{};
+    padsim_slo slo{};
+    std::vector<int> static_list, dyn_list;
+    std::vector<long long> toff;
+    std::vector<int> capsum_h;
+    // device buffers
+    std::vector<void*> bufs;
+    long long* d_toff = nullptr;
+    int* d_nreq = nullptr;
+    double* d_s_unit = nullptr;
+    double* d_kv = nullptr;
+    int* d_in = nullptr;
+    int* d_out = nullptr;
+    unsigned char* d_phase = nullptr;
+    unsigned char* d_role = nullptr;
+    int* d_cap = nullptr;
+    int* d_capsum = nullptr;
+    padsim_policy* d_pol = nullptr;
+    double* d_qps = nullptr;
+    int* d_clist_static = nullptr;
+    int* d_clist_dyn = nullptr;
+    double *d_spre = nullptr, *d_sdec = nullptr, *d_den = nullptr, *d_ltab = nullptr;
+    int* d_rep_met = nullptr;
+    int* d_rep_near = nullptr;
+    double* d_rep_dur = nullptr;
+    double* d_rep_good = nullptr;
+    long long* d_rep_events = nullptr;
+    long long* d_met = nullptr;
+    double* d_good = nullptr;
+    long long* d_near = nullptr;
+    int* d_argmax = nullptr;
+    double *d_rec[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    unsigned* d_work = nullptr;
+    char* d_scratch_static = nullptr;
+    char* d_scratch_dyn = nullptr;
+    Plan plan_static{}, plan_dyn{};
+    int grid_static = 0, grid_dyn = 0;
+    size_t smem_static = 0, smem_dyn = 0;
+    // host staging for the one-shot API
+    padsim_ctrl_state* d_ctl_state = nullptr;
+    padsim_action* d_ctl_act = nullptr;
+};
+
+static const char* kVersion = "padsim 0.1 (sm_100a)";
+
+static int fail(padsim_ctx* ctx, int code, const char* msg) {
+    if (ctx) ctx->err = msg;
+    return code;
+}
+static int cuda_fail(padsim_ctx* ctx, cudaError_t e, const char* where) {
+    if (ctx) ctx->err = std::string(where) + ": " + cudaGetErrorString(e);
+    return PADSIM_ECUDA;
+}
+#define CK(call)                                               \
+    do {                                                       \
+        cudaError_t e_ = (call);                               \
+        if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #call); \
+    } while (0)
+
+template <class T>
+static int dalloc(padsim_ctx* ctx, T** p, size_t n) {
+    *p = nullptr;
+    if (n == 0) n = 1;
+    void* q = nullptr;
+    cudaError_t e = cudaMalloc(&q, n * sizeof(T));
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        ctx->err = std::string("cudaMalloc: ") + cudaGetErrorString(e);
+        return PADSIM_ENOMEM;
+    }
+    ctx->bufs.push_back(q);
+    *p = (T*)q;
+    return PADSIM_OK;
+}
+
+static void free_plan(padsim_ctx* ctx) {
+    for (void* p : ctx->bufs) cudaFree(p);
+    ctx->bufs.clear();
+    ctx->planned = false;
+    ctx->static_list.clear();
+    ctx->dyn_list.clear();
+    for (auto& r : ctx->d_rec) r = nullptr;
+}
+
+// ---------------------------------------------------------------------------
+// row a3: model tables (device).  Same FP64 expressions as DESIGN.md §3 c.1.
+// ---------------------------------------------------------------------------
+__device__ double dev_speedup(const padsim_curve& c, int w) {
+    const int n = c.n;
+    if (w == c.w[n - 1]) return c.s[n - 1];
+    int j = 0;
+    for (int k = 1; k < n - 1; k++)
+        if (c.w[k] <= w) j = k;
+    const double diff = c.s[j + 1] - c.s[j];
+    const double frac = (double)(w - c.w[j]) / (double)(c.w[j + 1] - c.w[j]);
+    return c.s[j] + diff * frac;
+}
+
+__global__ void tables_kernel(const padsim_model m, double* spre, double* sdec, double* den,
+                              double* ltab, const int* in_tok, double* kv, long long n_tok) {
+    const int ncap = m.max_w - m.min_w + 1;
+    const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long k = tid; k < ncap; k += stride) {
+        spre[k] = dev_speedup(m.prefill, m.min_w + (int)k);
+        sdec[k] = dev_speedup(m.decode, m.min_w + (int)k);
+    }
+    for (long long b = tid; b <= m.max_prefill_batch; b += stride) {
+        const double be = 1.0 + m.prefill_batch_eff * (double)((int)b - 1);
+        den[b] = m.prefill_base_rate * be;
+    }
+    const long long nl = (long long)ncap * m.max_decode_batch;
+    for (long long k = tid; k < nl; k += stride) {
+        const int ci = (int)(k / m.max_decode_batch);
+        const int n = (int)(k % m.max_decode_batch) + 1;
+        const double x = m.decode_fixed_s + m.decode_per_seq_s * (double)n;
+        ltab[k] = x / dev_speedup(m.decode, m.min_w + ci);
+    }
+    for (long long i = tid; i < n_tok; i += stride) {
+        kv[i] = m.transfer_overhead_s + ((double)in_tok[i] * m.kv_bytes_per_token) / m.fabric_bw_Bps;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// row a8: seed reduction (ascending trace order) and per-QPS argmax
+// ---------------------------------------------------------------------------
+__global__ void reduce_kernel(const int* rep_met, const int* rep_near, const double* rep_good,
+                              int CQ, int S, long long* met, double* good, long long* near) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= CQ) return;
+    long long m = 0, nn = 0;
+    double g = 0.0;
+    const long long base = (long long)k * S;
+    for (int s = 0; s < S; s++) {
+        m += rep_met[base + s];
+        nn += rep_near[base + s];
+        g += rep_good[base + s];
+    }
+    met[k] = m;
+    near[k] = nn;
+    good[k] = g;
+}
+
+struct Key { long long met; int capsum; int idx; };
+__device__ __forceinline__ bool key_better(const Key& a, const Key& b) {
+    if (a.met != b.met) return a.met > b.met;            // Σmet ↓
+    if (a.capsum != b.capsum) return a.capsum < b.capsum;  // Σcaps ↑ (A25)
+    return a.idx < b.idx;                              // index ↑
+}
+
+__global__ void argmax_kernel(const long long* met, const int* capsum, int C, int Q, int* argmax) {
+    const int q = blockIdx.x;
+    Key best{-1, 0x7fffffff, 0x7fffffff};
+    for (int c = threadIdx.x; c < C; c += blockDim.x) {
+        Key k{met[(long long)c * Q + q], capsum[c], c};
+        if (key_better(k, best)) best = k;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        Key other;
+        other.met = __shfl_xor_sync(0xffffffffu, best.met, o);
+        other.capsum = __shfl_xor_sync(0xffffffffu, best.capsum, o);
+        other.idx = __shfl_xor_sync(0xffffffffu, best.idx, o);
+        if (key_better(other, best)) best = other;
+    }
+    __shared__ Key sk[32];
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) sk[w] = best;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        Key b = sk[0];
+        for (int i = 1; i < (int)(blockDim.x >> 5); i++)
+            if (key_better(sk[i], b)) b = sk[i];
+        argmax[q] = b.idx;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// row a6 ABI: one controller step on the device (same ctl_step as the replay)
+// ---------------------------------------------------------------------------
+struct AbiView {
+    const padsim_ctrl_state* st;
+    const padsim_window_stats* ws;
+    __device__ int role(int g) const { return st->role[g]; }
+    __device__ bool draining(int g) const { return st->draining[g] != 0; }
+    __device__ int target(int g) const { return st->cmd_cap_w[g]; }
+    __device__ long long load(int g) const { return ws->load[g]; }
+};
+
+__global__ void controller_kernel(const padsim_policy pol, const int min_w, const int max_w,
+                                  const int budget, padsim_ctrl_state* st,
+                                  const padsim_window_stats ws, const double now,
+                                  padsim_action* act) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    CtlSignals sg;
+    sg.ttft_gt = ws.ttft_stat_s > ws.ttft_slo_s;
+    sg.ttft_lt = ws.ttft_stat_s < ws.ttft_slo_s;
+    sg.tpot_gt = ws.tpot_stat_s > ws.tpot_slo_s;
+    sg.tpot_lt = ws.tpot_stat_s < ws.tpot_slo_s;
+    sg.q_prefill = ws.q_prefill;
+    AbiView v{st, &ws};
+    int newcap[PADSIM_MAX_GPUS];
+    int gsel, dir;
+    const int N = st->n_gpus;
+    const int kind = ctl_step(pol, min_w, max_w, budget, N, v, st->drain_pending != 0,
+                              st->last_move_s, now, sg, newcap, &gsel, &dir);
+    act->kind = kind;
+    act->direction = dir;
+    act->gpu = gsel;
+    for (int g = 0; g < PADSIM_MAX_GPUS; g++) act->new_cap_w[g] = g < N ? st->cmd_cap_w[g] : 0;
+    if (kind == ACT_MOVE_POWER || kind == ACT_MOVE_GPU) {
+        for (int g = 0; g < N; g++) {
+            act->new_cap_w[g] = newcap[g];
+            st->cmd_cap_w[g] = newcap[g];
+        }
+        st->last_move_s = now;
+        if (kind == ACT_MOVE_GPU) {
+            st->draining[gsel] = 1;
+            st->drain_pending = 1;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host validation
+// ---------------------------------------------------------------------------
+static int validate_model(padsim_ctx* ctx, const padsim_model* m) {
+    if (!m) return fail(ctx, PADSIM_EINVAL, "model is NULL");
+    if (!(m->min_w > 0 && m->min_w < m->max_w)) return fail(ctx, PADSIM_EMODEL, "min_w/max_w");
+    const padsim_curve* cs[2] = {&m->prefill, &m->decode};
+    for (const padsim_curve* c : cs) {
+        if (c->n < 2 || c->n > PADSIM_MAX_ANCHORS) return fail(ctx, PADSIM_EMODEL, "curve anchor count");
+        if (c->w[0] != m->min_w || c->w[c->n - 1] != m->max_w)
+            return fail(ctx, PADSIM_EMODEL, "curve must span [min_w, max_w]");
+        if (c->s[0] != 1.0) return fail(ctx, PADSIM_EMODEL, "speedup at lowest anchor must be 1.0");
+        for (int k = 1; k < c->n; k++) {
+            if (!(c->w[k] > c->w[k - 1])) return fail(ctx, PADSIM_EMODEL, "anchors not increasing");
+            if (!(c->s[k] >= c->s[k - 1]) || !std::isfinite(c->s[k]))
+                return fail(ctx, PADSIM_EMODEL, "speedup not monotone");
+        }
+    }
+    if (!(m->prefill_base_rate > 0 && m->prefill_batch_eff >= 0 && m->decode_fixed_s > 0 &&
+          m->decode_per_seq_s >= 0 && m->decode_per_ctx_tok_s >= 0 && m->kv_bytes_per_token > 0 &&
+          m->fabric_bw_Bps > 0 && m->transfer_overhead_s > 0))
+        return fail(ctx, PADSIM_EMODEL, "model parameters must be positive");
+    if (m->max_prefill_batch < 1 || m->max_prefill_batch > PADSIM_MAX_PREFILL_BATCH ||
+        m->prefill_token_budget < 1 || m->max_decode_batch < 1 ||
+        m->max_decode_batch > PADSIM_MAX_DECODE_BATCH || m->transfer_slots < 1 ||
+        m->transfer_slots > PADSIM_MAX_SLOTS)
+        return fail(ctx, PADSIM_EMODEL, "batch / slot limits");
+    return PADSIM_OK;
+}
+
+static int validate_policy(padsim_ctx* ctx, const padsim_policy* p, const padsim_model* m, int N,
+                           int B) {
+    if (p->kind < 0 || p->kind > 3) return fail(ctx, PADSIM_EINVAL, "policy kind");
+    if (p->kind == 0) return PADSIM_OK;
+    if (!(p->tick_s > 0 && p->settle_s > 0 && p->reassign_s > 0 && p->cooldown_s >= p->settle_s &&
+          p->window_s >= 0 && p->power_step_w > 0 && p->queue_threshold >= 0 &&
+          p->decode_ceiling_w >= m->min_w && p->decode_ceiling_w <= m->max_w &&
+          (long long)N * m->min_w <= B && std::isfinite(p->cooldown_s) && std::isfinite(p->window_s)))
+        return fail(ctx, PADSIM_EINVAL, "dynamic policy fields");
+    return PADSIM_OK;
+}
+
+extern "C" {
+
+const char* padsim_version(void) { return kVersion; }
+
+int padsim_create(int32_t dev, padsim_ctx** out) {
+    if (!out) return PADSIM_EINVAL;
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n <= 0 || dev < 0 || dev >= n) {
+        cudaGetLastError();
+        return PADSIM_ECUDA;
+    }
+    padsim_ctx* ctx = new (std::nothrow) padsim_ctx();
+    if (!ctx) return PADSIM_ENOMEM;
+    ctx->device = dev;
+    if (cudaSetDevice(dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&ctx->n_sm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+        cudaGetLastError();
+        delete ctx;
+        return PADSIM_ECUDA;
+    }
+    *out = ctx;
+    return PADSIM_OK;
+}
+
+void padsim_destroy(padsim_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    free_plan(ctx);
+    if (ctx->d_ctl_state) cudaFree(ctx->d_ctl_state);
+    if (ctx->d_ctl_act) cudaFree(ctx->d_ctl_act);
+    delete ctx;
+}
+
+const char* padsim_last_error(const padsim_ctx* ctx) { return ctx ? ctx->err.c_str() : "null ctx"; }
+
+int padsim_enumerate_pool_uniform(int32_t n_gpus, int32_t budget_w, int32_t min_w, int32_t max_w,
+                                  int32_t step_w, int32_t exact, int32_t* out_xpd, int32_t cap,
+                                  int32_t* n_out) {
+    if (!n_out || n_gpus < 2 || n_gpus > PADSIM_MAX_GPUS || step_w <= 0 || min_w <= 0 ||
+        min_w > max_w || cap < 0)
+        return PADSIM_EINVAL;
+    int32_t cnt = 0;
+    const int levels = (max_w - min_w) / step_w + 1;
+    for (int x = 1; x < n_gpus; x++) {
+        const long long y = n_gpus - x;
+        for (int a = 0; a < levels; a++) {
+            const long long p = min_w + (long long)a * step_w;
+            // largest d with x*p + y*d <= B (or == B): a closed-form bound per p
+            const long long rem = (long long)budget_w - x * p;
+            if (rem < y * min_w) break;            // p increasing: no larger p fits either
+            long long dmax = rem / y;
+            if (dmax > max_w) dmax = max_w;
+            const long long kmax = (dmax - min_w) / step_w;
+            for (long long k = 0; k <= kmax; k++) {
+                const long long d = min_w + k * step_w;
+                if (exact && x * p + y * d != budget_w) continue;
+                if (out_xpd && cnt < cap) {
+                    out_xpd[3 * cnt + 0] = x;
+                    out_xpd[3 * cnt + 1] = (int32_t)p;
+                    out_xpd[3 * cnt + 2] = (int32_t)d;
+                }
+                cnt++;
+            }
+        }
+    }
+    *n_out = cnt;
+    return PADSIM_OK;
+}
+
+int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
+                const double* qps, int32_t n_qps, const padsim_model* model,
+                const padsim_candidates* cands, const padsim_slo* slo,
+                const padsim_budget* budget, uint32_t flags, int32_t* bad_index) {
+    if (!ctx) return PADSIM_EINVAL;
+    if (bad_index) *bad_index = -1;
+    CK(cudaSetDevice(ctx->device));
+    free_plan(ctx);
+    if (!traces || n_traces < 1 || !qps || n_qps < 1 || !cands || !slo || !budget)
+        return fail(ctx, PADSIM_EINVAL, "null input or empty dimension");
+    int rc = validate_model(ctx, model);
+    if (rc) return rc;
+    const int N = cands->n_gpus, C = cands->n_cand, B = budget->budget_w;
+    if (N < 2 || N > PADSIM_MAX_GPUS || C < 1 || !cands->role || !cands->cap_w || !cands->policy)
+        return fail(ctx, PADSIM_EINVAL, "candidates");
+    if (!(slo->ttft_s > 0 && slo->tpot_s[0] > 0 && slo->tpot_s[1] > 0))
+        return fail(ctx, PADSIM_EINVAL, "SLOs must be > 0");
+    for (int q = 0; q < n_qps; q++)
+        if (!(qps[q] > 0) || !std::isfinite(qps[q])) return fail(ctx, PADSIM_EINVAL, "qps must be > 0");
+    std::vector<int> capsum(C);
+    for (int c = 0; c < C; c++) {
+        int np = 0;
+        long long cs = 0;
+        for (int g = 0; g < N; g++) {
+            const int r = cands->role[(size_t)c * N + g];
+            const int w = cands->cap_w[(size_t)c * N + g];
+            if (r > 1) { if (bad_index) *bad_index = c; return fail(ctx, PADSIM_EROLE, "role must be 0/1"); }
+            np += r == 0;
+            if (w < model->min_w || w > model->max_w) {
+                if (bad_index) *bad_index = c;
+                return fail(ctx, PADSIM_ERANGE, "cap outside [min_w, max_w]");
+            }
+            cs += w;
+        }
+        if (np < 1 || np > N - 1) {
+            if (bad_index) *bad_index = c;
+            return fail(ctx, PADSIM_EROLE, "need >= 1 prefill and >= 1 decode GPU");
+        }
+        if (cs > B) {
+            if (bad_index) *bad_index = c;
+            return fail(ctx, PADSIM_EBUDGET, "sum of caps exceeds the node budget");
+        }
+        rc = validate_policy(ctx, &cands->policy[c], model, N, B);
+        if (rc) { if (bad_index) *bad_index = c; return rc; }
+        capsum[c] = (int)cs;
+    }
+    // traces
+    std::vector<long long> toff(n_traces + 1);
+    int Rmax = 0;
+    long long tot = 0;
+    for (int s = 0; s < n_traces; s++) {
+        const padsim_trace& t = traces[s];
+        if (t.n_req < 0 || (t.n_req > 0 && (!t.s_unit || !t.in_tok || !t.out_tok)))
+            return fail(ctx, PADSIM_EINVAL, "trace arrays");
+        for (int i = 0; i < t.n_req; i++) {
+            if (t.in_tok[i] < 1 || t.out_tok[i] < 1) return fail(ctx, PADSIM_EDOMAIN, "token count < 1");
+            if (!(t.s_unit[i] >= 0) || !std::isfinite(t.s_unit[i]))
+                return fail(ctx, PADSIM_EDOMAIN, "arrival not finite / negative");
+            if (i > 0 && !(t.s_unit[i] >= t.s_unit[i - 1])) return fail(ctx, PADSIM_EDOMAIN, "arrivals unsorted");
+            if (t.phase && t.phase[i] > 1) return fail(ctx, PADSIM_EINVAL, "phase must be 0/1");
+        }
+        toff[s] = tot;
+        tot += (t.n_req + 15) & ~15;
+        Rmax = std::max(Rmax, t.n_req);
+    }
+    toff[n_traces] = tot;
+    ctx->N = N; ctx->C = C; ctx->Q = n_qps; ctx->S = n_traces; ctx->Rmax = Rmax; ctx->B = B;
+    ctx->model = *model;
+    ctx->slo = *slo;
+    ctx->flags = flags;
+    ctx->capsum_h = capsum;
+    ctx->toff = toff;
+    for (int c = 0; c < C; c++) (cands->policy[c].kind == 0 ? ctx->static_list : ctx->dyn_list).push_back(c);
+
+    // host staging of the padded SoA trace arrays
+    std::vector<double> hs(tot, 0.0);
+    std::vector<int> hin(tot, 1), hout(tot, 1);
+    std::vector<unsigned char> hph(tot, 0);
+    std::vector<int> nreq(n_traces);
+    for (int s = 0; s < n_traces; s++) {
+        const padsim_trace& t = traces[s];
+        nreq[s] = t.n_req;
+        if (t.n_req == 0) continue;
+        std::memcpy(&hs[toff[s]], t.s_unit, sizeof(double) * t.n_req);
+        std::memcpy(&hin[toff[s]], t.in_tok, sizeof(int) * t.n_req);
+        std::memcpy(&hout[toff[s]], t.out_tok, sizeof(int) * t.n_req);
+        if (t.phase) std::memcpy(&hph[toff[s]], t.phase, t.n_req);
+    }
+    const long long CQ = (long long)C * n_qps, R_all = CQ * n_traces;
+    const int ncap = model->max_w - model->min_w + 1;
+#define AL(p, n) do { int r_ = dalloc(ctx, &(p), (size_t)(n)); if (r_) return r_; } while (0)
+    AL(ctx->d_toff, n_traces + 1);
+    AL(ctx->d_nreq, n_traces);
+    AL(ctx->d_s_unit, tot);
+    AL(ctx->d_kv, tot);
+    AL(ctx->d_in, tot);
+    AL(ctx->d_out, tot);
+    AL(ctx->d_phase, tot);
+    AL(ctx->d_role, (size_t)C * N);
+    AL(ctx->d_cap, (size_t)C * N);
+    AL(ctx->d_capsum, C);
+    AL(ctx->d_pol, C);
+    AL(ctx->d_qps, n_qps);
+    AL(ctx->d_clist_static, std::max<size_t>(1, ctx->static_list.size()));
+    AL(ctx->d_clist_dyn, std::max<size_t>(1, ctx->dyn_list.size()));
+    AL(ctx->d_spre, ncap);
+    AL(ctx->d_sdec, ncap);
+    AL(ctx->d_den, model->max_prefill_batch + 1);
+    AL(ctx->d_ltab, (size_t)ncap * model->max_decode_batch);
+    AL(ctx->d_rep_met, R_all);
+    AL(ctx->d_rep_near, R_all);
+    AL(ctx->d_rep_dur, R_all);
+    AL(ctx->d_rep_good, R_all);
+    AL(ctx->d_rep_events, R_all);
+    AL(ctx->d_met, CQ);
+    AL(ctx->d_good, CQ);
+    AL(ctx->d_near, CQ);
+    AL(ctx->d_argmax, n_qps);
+    AL(ctx->d_work, 2);
+    if (flags & PADSIM_RECORDS) {
+        for (auto& r : ctx->d_rec) AL(r, (size_t)R_all * std::max(Rmax, 1));
+    }
+    CK(cudaMemcpy(ctx->d_toff, toff.data(), sizeof(long long) * (n_traces + 1), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->d_nreq, nreq.data(), sizeof(int) * n_traces, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->d_s_unit, hs.data(), sizeof(double) * tot, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->d_in, hin.data(), sizeof(int) * tot, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->d_out, hout.data(), sizeof(int) * tot, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->d_phase, hph.data(), tot, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->d_role, cands->role, (size_t)C * N, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->d_cap, cands->cap_w, sizeof(int) * (size_t)C * N, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->d_capsum, capsum.data(), sizeof(int) * C, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->d_pol, cands->policy, sizeof(padsim_policy) * C, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->d_qps, qps, sizeof(double) * n_qps, cudaMemcpyHostToDevice));
+    if (!ctx->static_list.empty())
+        CK(cudaMemcpy(ctx->d_clist_static, ctx->static_list.data(), sizeof(int) * ctx->static_list.size(),
+                      cudaMemcpyHostToDevice));
+    if (!ctx->dyn_list.empty())
+        CK(cudaMemcpy(ctx->d_clist_dyn, ctx->dyn_list.data(), sizeof(int) * ctx->dyn_list.size(),
+                      cudaMemcpyHostToDevice));
+    tables_kernel<<<std::max(1, ctx->n_sm), 256>>>(*model, ctx->d_spre, ctx->d_sdec, ctx->d_den,
+                                                    ctx->d_ltab, ctx->d_in, ctx->d_kv, tot);
+    CK(cudaGetLastError());
+
+    // replay launch plans (static and dynamic candidates run in separate kernels)
+    for (int dyn = 0; dyn < 2; dyn++) {
+        const std::vector<int>& lst = dyn ? ctx->dyn_list : ctx->static_list;
+        Plan& P = dyn ? ctx->plan_dyn : ctx->plan_static;
+        std::memset(&P, 0, sizeof(P));
+        if (lst.empty()) continue;
+        P.m.min_w = model->min_w; P.m.max_w = model->max_w; P.m.ncap = ncap;
+        P.m.rate = model->prefill_base_rate; P.m.eff = model->prefill_batch_eff;
+        P.m.dec_fixed = model->decode_fixed_s; P.m.dec_per_seq = model->decode_per_seq_s;
+        P.m.dec_per_ctx = model->decode_per_ctx_tok_s; P.m.kvb = model->kv_bytes_per_token;
+        P.m.bw = model->fabric_bw_Bps; P.m.ovh = model->transfer_overhead_s;
+        P.m.max_pb = model->max_prefill_batch; P.m.pb_tokens = model->prefill_token_budget;
+        P.m.max_db = model->max_decode_batch; P.m.slots = model->transfer_slots;
+        P.m.spre = ctx->d_spre; P.m.sdec = ctx->d_sdec; P.m.den = ctx->d_den; P.m.ltab = ctx->d_ltab;
+        P.N = N; P.C = C; P.Q = n_qps; P.S = n_traces; P.Rmax = Rmax; P.B = B;
+        P.toff = ctx->d_toff; P.nreq = ctx->d_nreq; P.s_unit = ctx->d_s_unit; P.kv = ctx->d_kv;
+        P.in_tok = ctx->d_in; P.out_tok = ctx->d_out; P.phase = ctx->d_phase;
+        P.role = ctx->d_role; P.cap = ctx->d_cap; P.pol = ctx->d_pol; P.qps = ctx->d_qps;
+        P.ttft_slo = slo->ttft_s; P.tpot_slo0 = slo->tpot_s[0]; P.tpot_slo1 = slo->tpot_s[1];
+        P.clist = dyn ? ctx->d_clist_dyn : ctx->d_clist_static;
+        P.n_clist = (int)lst.size();
+        P.items_per_trace = (int)(((long long)n_qps * P.n_clist + kThreads - 1) / kThreads);
+        P.n_items = P.items_per_trace * n_traces;
+        P.work = ctx->d_work + dyn;
+        P.rep_met = ctx->d_rep_met; P.rep_near = ctx->d_rep_near; P.rep_dur = ctx->d_rep_dur;
+        P.rep_good = ctx->d_rep_good; P.rep_events = ctx->d_rep_events;
+        if (flags & PADSIM_RECORDS) {
+            P.rec_ttft = ctx->d_rec[0]; P.rec_tpot = ctx->d_rec[1]; P.rec_pe = ctx->d_rec[2];
+            P.rec_comp = ctx->d_rec[3]; P.rec_te = ctx->d_rec[4];
+        }
+        // scratch layout per warp (lane-interleaved, 32 lanes)
+        const size_t R = (size_t)std::max(Rmax, 1);
+        size_t off = 0;
+        auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~(size_t)255; return o; };
+        P.off_link = take(R * 32 * sizeof(int));
+        P.off_pe = take(R * 32 * sizeof(double));
+        P.off_mem = take((size_t)N * model->max_decode_batch * 32 * sizeof(int2));
+        if (dyn) {
+            P.off_ordt = take(R * 32 * sizeof(int));
+            P.off_tst = take(R * 32 * sizeof(double));
+            P.off_tfl = take(R * 32);
+        }
+        P.warp_bytes = off;
+        P.scratch_per_cta = off * kWarps;
+        // trace staging in shared memory via TMA bulk copies when it fits
+        const size_t Rp = ((size_t)Rmax + 15) & ~(size_t)15;
+        const size_t tbytes = Rp * (8 + 8 + 4 + 4 + 1);
+        P.smem_trace = tbytes <= 96 * 1024 ? 1 : 0;
+        P.smem_trace_bytes = P.smem_trace ? tbytes : 0;
+        const void* fn;
+        if (N <= 8) fn = dyn ? (const void*)replay_kernel<8, true> : (const void*)replay_kernel<8, false>;
+        else fn = dyn ? (const void*)replay_kernel<64, true> : (const void*)replay_kernel<64, false>;
+        CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem_trace_bytes));
+        int occ = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, P.smem_trace_bytes));
+        occ = std::max(occ, 1);
+        long long grid = (long long)ctx->n_sm * occ;
+        grid = std::min<long long>(grid, P.n_items);
+        // bound the scratch to ~40% of free device memory
+        size_t fr = 0, totm = 0;
+        CK(cudaMemGetInfo(&fr, &totm));
+        const long long max_ctas = (long long)((fr * 2 / 5) / std::max<size_t>(P.scratch_per_cta, 1));
+        if (max_ctas < 1) return fail(ctx, PADSIM_ENOMEM, "scratch does not fit in device memory");
+        grid = std::max<long long>(1, std::min(grid, max_ctas));
+        char* scr = nullptr;
+        AL(scr, (size_t)grid * P.scratch_per_cta);
+        P.scratch = scr;
+        (dyn ? ctx->grid_dyn : ctx->grid_static) = (int)grid;
+        (dyn ? ctx->smem_dyn : ctx->smem_static) = P.smem_trace_bytes;
+    }
+#undef AL
+    CK(cudaDeviceSynchronize());
+    ctx->planned = true;
+    return PADSIM_OK;
+}
+
+int padsim_run(padsim_ctx* ctx, void* stream) {
+    if (!ctx) return PADSIM_EINVAL;
+    if (!ctx->planned) return fail(ctx, PADSIM_EINVAL, "padsim_run before padsim_plan");
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    CK(cudaMemsetAsync(ctx->d_work, 0, 2 * sizeof(unsigned), st));
+    for (int dyn = 0; dyn < 2; dyn++) {
+        const Plan& P = dyn ? ctx->plan_dyn : ctx->plan_static;
+        if (P.n_clist == 0) continue;
+        const int grid = dyn ? ctx->grid_dyn : ctx->grid_static;
+        const size_t smem = dyn ? ctx->smem_dyn : ctx->smem_static;
+        if (ctx->N <= 8) {
+            if (dyn) replay_kernel<8, true><<<grid, kThreads, smem, st>>>(P);
+            else replay_kernel<8, false><<<grid, kThreads, smem, st>>>(P);
+        } else {
+            if (dyn) replay_kernel<64, true><<<grid, kThreads, smem, st>>>(P);
+            else replay_kernel<64, false><<<grid, kThreads, smem, st>>>(P);
+        }
+        CK(cudaGetLastError());
+    }
+    const int CQ = ctx->C * ctx->Q;
+    reduce_kernel<<<(CQ + 255) / 256, 256, 0, st>>>(ctx->d_rep_met, ctx->d_rep_near, ctx->d_rep_good,
+                                                    CQ, ctx->S, ctx->d_met, ctx->d_good, ctx->d_near);
+    CK(cudaGetLastError());
+    argmax_kernel<<<ctx->Q, 256, 0, st>>>(ctx->d_met, ctx->d_capsum, ctx->C, ctx->Q, ctx->d_argmax);
+    CK(cudaGetLastError());
+    return PADSIM_OK;
+}
+
+int padsim_fetch(padsim_ctx* ctx, void* stream, padsim_result* out) {
+    if (!ctx || !out) return PADSIM_EINVAL;
+    if (!ctx->planned) return fail(ctx, PADSIM_EINVAL, "fetch before plan");
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t CQ = (size_t)ctx->C * ctx->Q;
+    if (out->met) CK(cudaMemcpyAsync(out->met, ctx->d_met, CQ * 8, cudaMemcpyDeviceToHost, st));
+    if (out->goodput) CK(cudaMemcpyAsync(out->goodput, ctx->d_good, CQ * 8, cudaMemcpyDeviceToHost, st));
+    if (out->near_boundary)
+        CK(cudaMemcpyAsync(out->near_boundary, ctx->d_near, CQ * 8, cudaMemcpyDeviceToHost, st));
+    if (out->argmax)
+        CK(cudaMemcpyAsync(out->argmax, ctx->d_argmax, (size_t)ctx->Q * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    out->bad_index = -1;
+    return PADSIM_OK;
+}
+
+int padsim_get_device_results(padsim_ctx* ctx, padsim_device_results* o) {
+    if (!ctx || !o) return PADSIM_EINVAL;
+    if (!ctx->planned) return fail(ctx, PADSIM_EINVAL, "no plan");
+    o->d_met = (int64_t*)ctx->d_met; o->d_goodput = ctx->d_good; o->d_near = (int64_t*)ctx->d_near;
+    o->d_argmax = ctx->d_argmax; o->d_rep_met = ctx->d_rep_met; o->d_rep_near = ctx->d_rep_near;
+    o->d_rep_duration = ctx->d_rep_dur; o->d_rep_goodput = ctx->d_rep_good;
+    o->d_rep_events = (int64_t*)ctx->d_rep_events;
+    o->n_cand = ctx->C; o->n_qps = ctx->Q; o->n_traces = ctx->S;
+    return PADSIM_OK;
+}
+
+int padsim_fetch_replays(padsim_ctx* ctx, void* stream, int32_t* met, int32_t* near,
+                         double* dur, double* good, int64_t* events) {
+    if (!ctx) return PADSIM_EINVAL;
+    if (!ctx->planned) return fail(ctx, PADSIM_EINVAL, "no plan");
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t n = (size_t)ctx->C * ctx->Q * ctx->S;
+    if (met) CK(cudaMemcpyAsync(met, ctx->d_rep_met, n * 4, cudaMemcpyDeviceToHost, st));
+    if (near) CK(cudaMemcpyAsync(near, ctx->d_rep_near, n * 4, cudaMemcpyDeviceToHost, st));
+    if (dur) CK(cudaMemcpyAsync(dur, ctx->d_rep_dur, n * 8, cudaMemcpyDeviceToHost, st));
+    if (good) CK(cudaMemcpyAsync(good, ctx->d_rep_good, n * 8, cudaMemcpyDeviceToHost, st));
+    if (events) CK(cudaMemcpyAsync(events, ctx->d_rep_events, n * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return PADSIM_OK;
+}
+
+int padsim_fetch_records(padsim_ctx* ctx, void* stream, double* ttft, double* tpot, double* pe,
+                         double* comp, double* te, int32_t* r_max) {
+    if (!ctx) return PADSIM_EINVAL;
+    if (!ctx->planned || !(ctx->flags & PADSIM_RECORDS))
+        return fail(ctx, PADSIM_EINVAL, "plan without PADSIM_RECORDS");
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t n = (size_t)ctx->C * ctx->Q * ctx->S * std::max(ctx->Rmax, 1) * 8;
+    double* dst[5] = {ttft, tpot, pe, comp, te};
+    for (int k = 0; k < 5; k++)
+        if (dst[k]) CK(cudaMemcpyAsync(dst[k], ctx->d_rec[k], n, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (r_max) *r_max = ctx->Rmax;
+    return PADSIM_OK;
+}
+
+int padsim_argmax_device(padsim_ctx* ctx, void* stream, const int64_t* d_met, int32_t n_cand,
+                         int32_t n_qps, int32_t* d_argmax) {
+    if (!ctx || !d_met || !d_argmax) return PADSIM_EINVAL;
+    if (!ctx->planned || n_cand != ctx->C || n_qps < 1)
+        return fail(ctx, PADSIM_EINVAL, "argmax shape does not match the plan");
+    CK(cudaSetDevice(ctx->device));
+    argmax_kernel<<<n_qps, 256, 0, (cudaStream_t)stream>>>((const long long*)d_met, ctx->d_capsum,
+                                                           n_cand, n_qps, d_argmax);
+    CK(cudaGetLastError());
+    return PADSIM_OK;
+}
+
+int padsim_evaluate_allocations(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
+                                const double* qps, int32_t n_qps, const padsim_model* model,
+                                const padsim_candidates* cands, const padsim_slo* slo,
+                                const padsim_budget* budget, padsim_result* out) {
+    if (!ctx || !out) return PADSIM_EINVAL;
+    int32_t bad = -1;
+    int rc = padsim_plan(ctx, traces, n_traces, qps, n_qps, model, cands, slo, budget, 0, &bad);
+    out->bad_index = bad;
+    if (rc) return rc;
+    rc = padsim_run(ctx, nullptr);
+    if (rc) return rc;
+    rc = padsim_fetch(ctx, nullptr, out);
+    out->bad_index = -1;
+    return rc;
+}
+
+int padsim_step_controller(padsim_ctx* ctx, const padsim_policy* policy, const padsim_budget* budget,
+                           const padsim_model* model, padsim_ctrl_state* st,
+                           const padsim_window_stats* ws, double now, padsim_action* act) {
+    if (!ctx || !policy || !budget || !model || !st || !ws || !act) return PADSIM_EINVAL;
+    if (st->n_gpus < 2 || st->n_gpus > PADSIM_MAX_GPUS) return fail(ctx, PADSIM_EINVAL, "n_gpus");
+    int rc = validate_model(ctx, model);
+    if (rc) return rc;
+    rc = validate_policy(ctx, policy, model, st->n_gpus, budget->budget_w);
+    if (rc) return rc;
+    CK(cudaSetDevice(ctx->device));
+    if (!ctx->d_ctl_state) {
+        CK(cudaMalloc(&ctx->d_ctl_state, sizeof(padsim_ctrl_state)));
+        CK(cudaMalloc(&ctx->d_ctl_act, sizeof(padsim_action)));
+    }
+    CK(cudaMemcpy(ctx->d_ctl_state, st, sizeof(*st), cudaMemcpyHostToDevice));
+    controller_kernel<<<1, 32>>>(*policy, model->min_w, model->max_w, budget->budget_w,
+                                 ctx->d_ctl_state, *ws, now, ctx->d_ctl_act);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(st, ctx->d_ctl_state, sizeof(*st), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(act, ctx->d_ctl_act, sizeof(*act), cudaMemcpyDeviceToHost));
+    return PADSIM_OK;
+}
+
+}  // extern "C"

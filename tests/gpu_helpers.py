@@ -1,0 +1,51 @@
+"""Helpers shared by the GPU parity tests: run the same seeded inputs through
+the CUDA path (via the C ABI) and through the oracle, compare."""
+import numpy as np
+
+import oracle
+import paper_2601_12241_b200 as pkg
+
+REC = ("ttft", "tpot", "prefill_end", "completion", "transfer_end")
+RTOL = 1e-9   # north_star: FP64 per-request latencies within 1e-9 relative
+
+
+def gpu_records(traces, qps, model, role, cap, pols, slo, budget):
+    ctx = pkg.Context(0)
+    try:
+        ctx.plan(traces, qps, model, role, cap, pols, slo, budget, records=True)
+        ctx.run()
+        res = ctx.fetch()
+        rep = ctx.fetch_replays()
+        rec = ctx.fetch_records()
+    finally:
+        ctx.close()
+    return res, rep, rec
+
+
+def compare_records(traces, qps, model, role, cap, pols, slo, budget, exact=True):
+    """Per-request, per-replay comparison; returns number of requests compared."""
+    res, rep, rec = gpu_records(traces, qps, model, role, cap, pols, slo, budget)
+    n = 0
+    for c in range(role.shape[0]):
+        for q, qv in enumerate(qps):
+            for s, tr in enumerate(traces):
+                o = oracle.replay(model, role[c], cap[c], pols[c], budget, slo, tr, qv)
+                R = tr["s_unit"].size
+                for k in REC:
+                    g = rec[k][c, q, s, :R]
+                    if exact:
+                        bad = np.nonzero(g != o[k])[0]
+                    else:
+                        bad = np.nonzero(~np.isclose(g, o[k], rtol=RTOL, atol=0))[0]
+                    assert bad.size == 0, (k, c, q, s, bad[:5], g[bad[:5]], o[k][bad[:5]])
+                assert rep["met"][c, q, s] == o["met"], (c, q, s)
+                assert rep["near_boundary"][c, q, s] == o["near_boundary"]
+                assert rep["duration"][c, q, s] == o["duration"]
+                assert rep["goodput"][c, q, s] == o["goodput"]
+                n += R
+    ev = oracle.evaluate(model, role, cap, pols, budget, slo, traces, qps, n_threads=8)
+    assert np.array_equal(res["met"], ev["met"])
+    assert np.array_equal(res["argmax"], ev["argmax"])
+    assert np.array_equal(res["near_boundary"], ev["near_boundary"])
+    assert np.array_equal(res["goodput"], ev["goodput"])
+    return n

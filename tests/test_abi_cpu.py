@@ -1,0 +1,70 @@
+"""C-ABI library checks that need no GPU: it builds for sm_100a, loads, exports
+every symbol include/padsim.h declares, refuses to compute without a device
+(no CPU fallback), and its host-side enumerator (row a1) agrees with the
+oracle's brute force."""
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+import oracle
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HDR = os.path.join(ROOT, "include", "padsim.h")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2601_12241_b200.build import build
+    build()
+    import paper_2601_12241_b200 as pkg
+    return pkg.load()
+
+
+def declared_functions():
+    text = open(HDR).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(padsim_[a-z_]+)\s*\(", text)))
+
+
+def test_header_declares_north_star_calls():
+    fns = declared_functions()
+    assert "padsim_evaluate_allocations" in fns and "padsim_step_controller" in fns
+    assert len(fns) >= 12
+
+
+def test_exports_every_declared_symbol(lib):
+    from paper_2601_12241_b200.binding import LIB_PATH, EXPORTS
+    out = subprocess.check_output(["nm", "-D", "--defined-only", LIB_PATH]).decode()
+    exported = set(re.findall(r"\sT\s(padsim_\w+)", out))
+    for fn in declared_functions():
+        assert fn in exported, fn
+        assert hasattr(lib, fn)
+    assert set(EXPORTS) == set(declared_functions())
+
+
+def test_sass_is_sm100a(lib):
+    from paper_2601_12241_b200.binding import LIB_PATH
+    out = subprocess.check_output(["cuobjdump", "--list-elf", LIB_PATH]).decode()
+    assert "sm_100a" in out
+
+
+def test_no_cpu_fallback_without_device(lib):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    import paper_2601_12241_b200 as pkg
+    with pytest.raises(pkg.PadsimError) as e:
+        pkg.Context(0)
+    assert e.value.rc == -7
+
+
+@pytest.mark.parametrize("N,B,step,exact", [(8, 4800, 25, 0), (8, 4800, 25, 1), (8, 4800, 100, 0),
+                                            (64, 38400, 25, 0), (64, 38400, 50, 1), (3, 1500, 25, 0)])
+def test_enumeration_matches_oracle(lib, N, B, step, exact):
+    import paper_2601_12241_b200 as pkg
+    a = pkg.enumerate_pool_uniform(N, B, 400, 750, step, exact)
+    b = oracle.enumerate_pool_uniform(N, B, 400, 750, step, exact)
+    assert np.array_equal(a, b)

@@ -1,0 +1,224 @@
+"""GPU ↔ oracle parity through the C ABI (north_star bar: chosen allocation and
+SLO-met counts bit-exact; FP64 per-request latencies and goodput within 1e-9
+relative — the implementation in fact reproduces them bit for bit, which is
+what these tests demand).  Inputs are the seeded synthetic traces of
+workloads/ at the shapes of BASELINE.json's configs."""
+import numpy as np
+import pytest
+
+import oracle
+from gpu_helpers import compare_records, gpu_records
+from workloads import (DEFAULT_MODEL, DEFAULT_SLO, PHASE_SLO, make_trace, policy,
+                       static_candidates)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    from paper_2601_12241_b200.build import build
+    build()
+    import paper_2601_12241_b200 as p
+    return p
+
+
+XPD = [(1, 750, 575), (2, 700, 550), (3, 675, 525), (4, 600, 600), (4, 750, 450), (5, 600, 600),
+       (6, 550, 700), (7, 500, 750), (4, 400, 400), (2, 425, 750)]
+
+
+@pytest.mark.parametrize("family", ["lb", "lb_bursty"])
+def test_static_records_exact(pkg, family):
+    role, cap = static_candidates(8, XPD)
+    pols = [policy("static")] * len(XPD)
+    traces = [make_trace(family, s, 300) for s in range(2)]
+    qps = [0.25, 1.0, 1.5, 2.5, 4.0]
+    n = compare_records(traces, qps, DEFAULT_MODEL, role, cap, pols, DEFAULT_SLO, 4800)
+    assert n == len(XPD) * len(qps) * 600
+
+
+@pytest.mark.parametrize("kind", ["dyn-power", "dyn-gpu", "dyn-both"])
+def test_dynamic_records_exact(pkg, kind):
+    xpd = [(4, 600, 600), (5, 600, 600), (3, 600, 600), (4, 750, 450)]
+    role, cap = static_candidates(8, xpd)
+    pols = [policy(kind, cooldown_s=2.0), policy(kind, threshold=2, window_s=2.5, cooldown_s=3.0),
+            policy(kind, step_w=25), policy(kind, step_w=100, window_s=10.0)]
+    traces = [make_trace("phase", s, 800) for s in range(2)]
+    qps = [1.5, 2.0, 3.0]
+    compare_records(traces, qps, DEFAULT_MODEL, role, cap, pols, PHASE_SLO, 4800)
+
+
+def test_mixed_static_dynamic_and_argmax(pkg):
+    cands = pkg.enumerate_pool_uniform(8, 4800, 400, 750, 50)
+    role, cap = static_candidates(8, cands)
+    pols = [policy("static")] * len(cands)
+    drole, dcap = static_candidates(8, [(x, 600, 600) for x in range(1, 8)])
+    role = np.concatenate([role, drole])
+    cap = np.concatenate([cap, dcap])
+    pols = pols + [policy("dyn-both")] * 7
+    traces = [make_trace("lb", s, 250) for s in range(2)]
+    qps = [0.5, 1.5, 2.5]
+    got = pkg.evaluate_allocations(traces, qps, DEFAULT_MODEL, role, cap, pols, DEFAULT_SLO, 4800)
+    ref = oracle.evaluate(DEFAULT_MODEL, role, cap, pols, 4800, DEFAULT_SLO, traces, qps, n_threads=8)
+    assert np.array_equal(got["met"], ref["met"])
+    assert np.array_equal(got["argmax"], ref["argmax"])
+    assert np.array_equal(got["near_boundary"], ref["near_boundary"])
+    assert np.array_equal(got["goodput"], ref["goodput"])
+
+
+def _tr(s_unit, ins, outs, phase=None):
+    n = len(s_unit)
+    return {"s_unit": np.asarray(s_unit, float), "in_tok": np.asarray(ins, np.int32),
+            "out_tok": np.asarray(outs, np.int32),
+            "phase": np.zeros(n, np.uint8) if phase is None else np.asarray(phase, np.uint8)}
+
+
+def test_edge_cases(pkg):
+    role, cap = static_candidates(8, [(4, 600, 600), (1, 750, 600), (7, 600, 450)])
+    pols = [policy("static")] * 3
+    ties = _tr(np.zeros(40), np.full(40, 512), np.full(40, 3))              # all at t=0
+    ones = _tr(np.arange(30) * 0.01, np.arange(1, 31) * 300, np.ones(30))   # out = 1
+    single = _tr([0.5], [8192], [128])
+    big = _tr(np.linspace(0, 1, 50), np.full(50, 20000), np.full(50, 2))    # head > token budget
+    traces = [ties, ones, single, big]
+    for m in (DEFAULT_MODEL, dict(DEFAULT_MODEL, slots=1), dict(DEFAULT_MODEL, max_pb=1),
+              dict(DEFAULT_MODEL, max_db=2), dict(DEFAULT_MODEL, dec_per_ctx=2e-7),
+              dict(DEFAULT_MODEL, pb_tokens=600)):
+        compare_records(traces, [0.5, 3.0], m, role, cap, pols, DEFAULT_SLO, 4800)
+
+
+def test_empty_trace(pkg):
+    role, cap = static_candidates(8, [(4, 600, 600)])
+    empty = _tr([], [], [])
+    res, rep, _ = gpu_records([empty, make_trace("lb", 0, 20)], [1.0], DEFAULT_MODEL, role, cap,
+                              [policy("static")], DEFAULT_SLO, 4800)
+    assert rep["met"][0, 0, 0] == 0 and rep["goodput"][0, 0, 0] == 0.0
+
+
+def test_small_and_large_nodes(pkg):
+    # N = 2 (tiny node) and N = 64 (cfg 5 shape, small trace)
+    r2, c2 = static_candidates(2, [(1, 600, 600), (1, 750, 450)])
+    compare_records([make_trace("lb", 3, 200)], [0.5, 1.5], DEFAULT_MODEL, r2, c2,
+                    [policy("static")] * 2, DEFAULT_SLO, 1200)
+    r64, c64 = static_candidates(64, [(32, 600, 600), (40, 675, 475), (10, 750, 550)])
+    compare_records([make_trace("long_prompt", 1, 1500), make_trace("long_output", 1, 600)],
+                    [0.5, 2.0], DEFAULT_MODEL, r64, c64, [policy("static")] * 3, DEFAULT_SLO, 38400)
+    pd = [policy("dyn-both", cooldown_s=2.0)] * 2
+    compare_records([make_trace("phase", 2, 3000)], [1.5], DEFAULT_MODEL, r64[:2], c64[:2], pd,
+                    PHASE_SLO, 38400)
+
+
+def test_cfg2_full_size_sampled(pkg):
+    # BASELINE cfg 2 at full size on the GPU (955 x 16 QPS x 8 seeds x 2000 req) in the
+    # launch configuration bench.py times; the oracle recomputes a sample of replays.
+    cands = pkg.enumerate_pool_uniform(8, 4800, 400, 750, 25)
+    assert len(cands) == 955
+    role, cap = static_candidates(8, cands)
+    pols = [policy("static")] * len(cands)
+    traces = [make_trace("lb", s, 2000) for s in range(8)]
+    qps = [0.25 * k for k in range(1, 17)]
+    ctx = pkg.Context(0)
+    ctx.plan(traces, qps, DEFAULT_MODEL, role, cap, pols, DEFAULT_SLO, 4800)
+    ctx.run()
+    res = ctx.fetch()
+    rep = ctx.fetch_replays()
+    ctx.close()
+    assert np.array_equal(res["met"], rep["met"].sum(axis=2))
+    rng = np.random.default_rng(2026)
+    for _ in range(40):
+        c, q, s = int(rng.integers(955)), int(rng.integers(16)), int(rng.integers(8))
+        o = oracle.replay(DEFAULT_MODEL, role[c], cap[c], pols[c], 4800, DEFAULT_SLO, traces[s], qps[q])
+        assert rep["met"][c, q, s] == o["met"], (c, q, s)
+        assert rep["duration"][c, q, s] == o["duration"]
+        assert rep["goodput"][c, q, s] == o["goodput"]
+    # properties at any size: attainment in [0, 1]; every replay ran to completion
+    assert (rep["met"] >= 0).all() and (rep["met"] <= 2000).all()
+    assert (rep["duration"] > 0).all() and (rep["events"] > 0).all()
+    # argmax is the per-QPS maximum of Σmet with the (Σcaps, index) tie-break
+    capsum = cap.sum(axis=1)
+    for q in range(16):
+        key = np.lexsort((np.arange(955), capsum, -res["met"][:, q]))
+        assert res["argmax"][q] == key[0]
+
+
+def test_cfg3_dynamic_sampled(pkg):
+    # cfg 3 shape (10k-request two-phase trace, dynamic policies) — sampled replays
+    xpd = [(4, 600, 600)] * 4
+    role, cap = static_candidates(8, xpd)
+    pols = [policy("dyn-power", threshold=4), policy("dyn-gpu", cooldown_s=5.0),
+            policy("dyn-both", step_w=25, window_s=2.5), policy("dyn-both", threshold=16, window_s=10.0)]
+    traces = [make_trace("phase", 0, 10000)]
+    qps = [2.0, 3.0]
+    res, rep, rec = gpu_records(traces, qps, DEFAULT_MODEL, role, cap, pols, PHASE_SLO, 4800)
+    for c in range(4):
+        for q in range(2):
+            o = oracle.replay(DEFAULT_MODEL, role[c], cap[c], pols[c], 4800, PHASE_SLO, traces[0], qps[q])
+            assert rep["met"][c, q, 0] == o["met"]
+            assert np.array_equal(rec["completion"][c, q, 0], o["completion"])
+            assert np.array_equal(rec["ttft"][c, q, 0], o["ttft"])
+
+
+def test_determinism(pkg):
+    role, cap = static_candidates(8, XPD)
+    pols = [policy("static")] * 8 + [policy("dyn-both")] * 2
+    traces = [make_trace("lb", s, 500) for s in range(3)]
+    a = pkg.evaluate_allocations(traces, [1.0, 2.0], DEFAULT_MODEL, role, cap, pols, DEFAULT_SLO, 4800)
+    b = pkg.evaluate_allocations(traces, [1.0, 2.0], DEFAULT_MODEL, role, cap, pols, DEFAULT_SLO, 4800)
+    for k in a:
+        assert a[k].tobytes() == b[k].tobytes()
+
+
+def test_validation_errors(pkg):
+    role, cap = static_candidates(8, [(4, 600, 600), (4, 700, 600)])
+    pols = [policy("static")] * 2
+    with pytest.raises(pkg.PadsimError) as e:
+        pkg.evaluate_allocations([make_trace("lb", 0, 10)], [1.0], DEFAULT_MODEL, role, cap, pols,
+                                 DEFAULT_SLO, 4800)
+    assert e.value.rc == -3 and e.value.bad_index == 1
+    bad = dict(DEFAULT_MODEL, prefill=[(400, 1.0), (700, 0.9), (750, 1.8)])
+    with pytest.raises(pkg.PadsimError) as e:
+        pkg.evaluate_allocations([make_trace("lb", 0, 10)], [1.0], bad, role[:1], cap[:1], pols[:1],
+                                 DEFAULT_SLO, 4800)
+    assert e.value.rc == -5
+    tr = make_trace("lb", 0, 10)
+    tr["in_tok"][3] = 0
+    with pytest.raises(pkg.PadsimError) as e:
+        pkg.evaluate_allocations([tr], [1.0], DEFAULT_MODEL, role[:1], cap[:1], pols[:1], DEFAULT_SLO, 4800)
+    assert e.value.rc == -6
+
+
+def test_step_controller_parity(pkg):
+    rng = np.random.default_rng(5)
+    ctx = pkg.Context(0)
+    try:
+        for trial in range(300):
+            n = int(rng.integers(2, 9))
+            x = int(rng.integers(1, n))
+            role = [0] * x + [1] * (n - x)
+            cmd = [int(v) for v in rng.choice(np.arange(400, 751, 25), n)]
+            drain = [0] * n
+            if rng.random() < 0.2:
+                drain[int(rng.integers(n))] = 1
+            st = dict(role=role, cmd=cmd, draining=drain, drain_pending=int(sum(drain) > 0),
+                      last_move=float(rng.choice([0.0, 3.0, 9.5])))
+            stats = dict(ttft_stat=float(rng.choice([0.0, 0.5, 1.0, 1.4])),
+                         tpot_stat=float(rng.choice([0.0, 0.02, 0.04, 0.05])),
+                         ttft_slo=1.0, tpot_slo=0.04, q_prefill=int(rng.integers(0, 20)),
+                         load=[int(v) for v in rng.integers(0, 5, n)])
+            kind = ["static", "dyn-power", "dyn-gpu", "dyn-both"][trial % 4]
+            pol = policy(kind, step_w=int(rng.choice([25, 50, 100])),
+                         dec_ceiling_w=int(rng.choice([600, 750])))
+            budget = max(4800, 400 * n)
+            now = float(rng.choice([5.0, 10.0, 13.5]))
+            a1, s1 = ctx.step_controller(pol, DEFAULT_MODEL, budget, st, stats, now)
+            a2, s2 = oracle.step_controller(pol, DEFAULT_MODEL, budget,
+                                            dict(st), dict(stats), now)
+            assert a1 == a2, (trial, a1, a2)
+            assert s1 == s2, (trial, s1, s2)
+    finally:
+        ctx.close()
+
+
+def test_enumeration_on_gpu_build(pkg):
+    for N, B in ((8, 4800), (64, 38400)):
+        assert np.array_equal(pkg.enumerate_pool_uniform(N, B, 400, 750, 25),
+                              oracle.enumerate_pool_uniform(N, B, 400, 750, 25))
