@@ -180,6 +180,11 @@ typedef struct {
 } padsim_device_results;
 int padsim_get_device_results(padsim_ctx* ctx, padsim_device_results* out);
 
+/* Device time of the replay kernel(s) of the last padsim_run in ms, measured
+ * with CUDA events recorded on the run's stream around the replay launches
+ * (synchronises on the end event).                                          */
+int padsim_replay_kernel_ms(padsim_ctx* ctx, float* ms);
+
 /* Per-replay host copies (synchronises): arrays of C*Q*S, any may be NULL. */
 int padsim_fetch_replays(padsim_ctx* ctx, void* stream, int32_t* met, int32_t* near_boundary,
                          double* duration, double* goodput, int64_t* events);

@@ -101,7 +101,8 @@ class Action(C.Structure):
 EXPORTS = ["padsim_create", "padsim_destroy", "padsim_last_error", "padsim_version",
            "padsim_evaluate_allocations", "padsim_plan", "padsim_run", "padsim_fetch",
            "padsim_get_device_results", "padsim_fetch_replays", "padsim_fetch_records",
-           "padsim_argmax_device", "padsim_step_controller", "padsim_enumerate_pool_uniform"]
+           "padsim_argmax_device", "padsim_step_controller", "padsim_enumerate_pool_uniform",
+           "padsim_replay_kernel_ms"]
 
 _lib = None
 _P = C.POINTER
@@ -130,6 +131,7 @@ def load(path: str = LIB_PATH):
     L.padsim_run.argtypes = [vp, vp]
     L.padsim_fetch.argtypes = [vp, vp, _P(Result)]
     L.padsim_get_device_results.argtypes = [vp, _P(DeviceResults)]
+    L.padsim_replay_kernel_ms.argtypes = [vp, _P(C.c_float)]
     L.padsim_fetch_replays.argtypes = [vp, vp, _P(C.c_int32), _P(C.c_int32), _P(C.c_double),
                                        _P(C.c_double), _P(C.c_int64)]
     L.padsim_fetch_records.argtypes = [vp, vp] + [_P(C.c_double)] * 5 + [_P(C.c_int32)]
@@ -282,6 +284,11 @@ class Context:
                      _p(am, C.c_int32), -1)
         self._check(self.L.padsim_fetch(self.ptr, C.c_void_p(stream or 0), C.byref(res)), "fetch")
         return {"met": met, "goodput": good, "near_boundary": near, "argmax": am}
+
+    def replay_kernel_ms(self) -> float:
+        ms = C.c_float(0.0)
+        self._check(self.L.padsim_replay_kernel_ms(self.ptr, C.byref(ms)), "replay_kernel_ms")
+        return float(ms.value)
 
     def fetch_replays(self, stream=None):
         Cn, Q, S, _ = self.shape

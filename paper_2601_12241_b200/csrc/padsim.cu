@@ -70,6 +70,8 @@ struct padsim_ctx {
     // host staging for the one-shot API
     padsim_ctrl_state* d_ctl_state = nullptr;
     padsim_action* d_ctl_act = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    bool ev_recorded = false;
 };
 
 static const char* kVersion = "padsim 0.1 (sm_100a)";
@@ -324,6 +326,8 @@ void padsim_destroy(padsim_ctx* ctx) {
     free_plan(ctx);
     if (ctx->d_ctl_state) cudaFree(ctx->d_ctl_state);
     if (ctx->d_ctl_act) cudaFree(ctx->d_ctl_act);
+    if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+    if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     delete ctx;
 }
 
@@ -588,6 +592,11 @@ int padsim_run(padsim_ctx* ctx, void* stream) {
     CK(cudaSetDevice(ctx->device));
     cudaStream_t st = (cudaStream_t)stream;
     CK(cudaMemsetAsync(ctx->d_work, 0, 2 * sizeof(unsigned), st));
+    if (!ctx->ev0) {
+        CK(cudaEventCreate(&ctx->ev0));
+        CK(cudaEventCreate(&ctx->ev1));
+    }
+    CK(cudaEventRecord(ctx->ev0, st));
     for (int dyn = 0; dyn < 2; dyn++) {
         const Plan& P = dyn ? ctx->plan_dyn : ctx->plan_static;
         if (P.n_clist == 0) continue;
@@ -602,6 +611,8 @@ int padsim_run(padsim_ctx* ctx, void* stream) {
         }
         CK(cudaGetLastError());
     }
+    CK(cudaEventRecord(ctx->ev1, st));
+    ctx->ev_recorded = true;
     const int CQ = ctx->C * ctx->Q;
     reduce_kernel<<<(CQ + 255) / 256, 256, 0, st>>>(ctx->d_rep_met, ctx->d_rep_near, ctx->d_rep_good,
                                                     CQ, ctx->S, ctx->d_met, ctx->d_good, ctx->d_near);
@@ -636,6 +647,15 @@ int padsim_get_device_results(padsim_ctx* ctx, padsim_device_results* o) {
     o->d_rep_duration = ctx->d_rep_dur; o->d_rep_goodput = ctx->d_rep_good;
     o->d_rep_events = (int64_t*)ctx->d_rep_events;
     o->n_cand = ctx->C; o->n_qps = ctx->Q; o->n_traces = ctx->S;
+    return PADSIM_OK;
+}
+
+int padsim_replay_kernel_ms(padsim_ctx* ctx, float* ms) {
+    if (!ctx || !ms) return PADSIM_EINVAL;
+    if (!ctx->ev_recorded) return fail(ctx, PADSIM_EINVAL, "no run recorded");
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaEventSynchronize(ctx->ev1));
+    CK(cudaEventElapsedTime(ms, ctx->ev0, ctx->ev1));
     return PADSIM_OK;
 }
 

@@ -23,7 +23,7 @@ def pkg():
 
 
 XPD = [(1, 750, 575), (2, 700, 550), (3, 675, 525), (4, 600, 600), (4, 750, 450), (5, 600, 600),
-       (6, 550, 700), (7, 500, 750), (4, 400, 400), (2, 425, 750)]
+       (6, 550, 700), (7, 500, 750), (4, 400, 400), (2, 450, 650)]
 
 
 @pytest.mark.parametrize("family", ["lb", "lb_bursty"])
