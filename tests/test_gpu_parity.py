@@ -73,7 +73,7 @@ def _tr(s_unit, ins, outs, phase=None):
 
 
 def test_edge_cases(pkg):
-    role, cap = static_candidates(8, [(4, 600, 600), (1, 750, 600), (7, 600, 450)])
+    role, cap = static_candidates(8, [(4, 600, 600), (1, 750, 575), (7, 600, 450)])
     pols = [policy("static")] * 3
     ties = _tr(np.zeros(40), np.full(40, 512), np.full(40, 3))              # all at t=0
     ones = _tr(np.arange(30) * 0.01, np.arange(1, 31) * 300, np.ones(30))   # out = 1

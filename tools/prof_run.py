@@ -1,0 +1,35 @@
+"""One padsim_run of a (reduced) BASELINE config for ncu captures.
+
+    python tools/prof_run.py [--config cfg2] [--traces 2] [--runs 2]
+"""
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "bench_support"))
+
+from bench import build_workload  # noqa: E402
+from workloads import DEFAULT_MODEL, get_config  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="cfg2")
+ap.add_argument("--traces", type=int, default=0, help="limit traces (0 = all)")
+ap.add_argument("--runs", type=int, default=2)
+a = ap.parse_args()
+
+import paper_2601_12241_b200 as pkg  # noqa: E402
+from paper_2601_12241_b200.build import build  # noqa: E402
+
+build()
+cfg = get_config(a.config)
+role, cap, pols, traces, qps = build_workload(cfg, 0, pkg.enumerate_pool_uniform)
+if a.traces:
+    traces = traces[: a.traces]
+ctx = pkg.Context(0)
+ctx.plan(traces, qps, DEFAULT_MODEL, role, cap, pols, cfg["slo"], cfg["budget_w"])
+for _ in range(a.runs):
+    ctx.run()
+    print("replay ms", ctx.replay_kernel_ms())
+ctx.close()
