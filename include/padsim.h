@@ -177,6 +177,9 @@ typedef struct {
     int32_t* d_rep_met; int32_t* d_rep_near; double* d_rep_duration; double* d_rep_goodput;
     int64_t* d_rep_events;
     int32_t n_cand, n_qps, n_traces;
+    int64_t* d_aux_events;   /* DES instants of shared prefill stages (factorized static
+                                path: one per prefill group x QPS x trace), n_aux_events */
+    int32_t n_aux_events;
 } padsim_device_results;
 int padsim_get_device_results(padsim_ctx* ctx, padsim_device_results* out);
 

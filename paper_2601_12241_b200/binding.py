@@ -78,7 +78,7 @@ class DeviceResults(C.Structure):
                 ("d_argmax", C.c_void_p), ("d_rep_met", C.c_void_p), ("d_rep_near", C.c_void_p),
                 ("d_rep_duration", C.c_void_p), ("d_rep_goodput", C.c_void_p),
                 ("d_rep_events", C.c_void_p), ("n_cand", C.c_int32), ("n_qps", C.c_int32),
-                ("n_traces", C.c_int32)]
+                ("n_traces", C.c_int32), ("d_aux_events", C.c_void_p), ("n_aux_events", C.c_int32)]
 
 
 class CtrlState(C.Structure):

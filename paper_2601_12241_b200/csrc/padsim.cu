@@ -18,6 +18,9 @@
 #include "common.cuh"
 #include "controller.cuh"
 #include "replay.cuh"
+#include "static_path.cuh"
+
+#include <map>
 
 using namespace padsim;
 
@@ -72,6 +75,13 @@ struct padsim_ctx {
     padsim_action* d_ctl_act = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     bool ev_recorded = false;
+    // factorized static path (N <= 8)
+    bool fact = false;
+    FPlan fplan{};
+    int fA_grid = 0, fC_grid = 0;
+    size_t fC_smem = 0;
+    long long* d_evA = nullptr;
+    int n_evA = 0;
 };
 
 static const char* kVersion = "padsim 0.1 (sm_100a)";
@@ -295,6 +305,136 @@ static int validate_policy(padsim_ctx* ctx, const padsim_policy* p, const padsim
     return PADSIM_OK;
 }
 
+// Groups static candidates by their prefill pool (caps of the prefill GPUs in
+// GPU-id order) and lays out stage A / stage C (static_path.cuh).
+static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const padsim_slo* slo, int Q,
+                           int S, int Rmax, long long tot, const padsim_candidates* cands) {
+    const int N = ctx->N;
+    std::map<std::vector<int>, int> gid;
+    std::vector<int> gx, gcap;
+    struct CC { int group, cand, y; int dcap[kNW]; };
+    std::vector<CC> ccs;
+    for (int c : ctx->static_list) {
+        std::vector<int> pc, dc;
+        for (int g = 0; g < N; g++) {
+            const int w = cands->cap_w[(size_t)c * N + g];
+            (cands->role[(size_t)c * N + g] == 0 ? pc : dc).push_back(w);
+        }
+        auto it = gid.find(pc);
+        int gi;
+        if (it == gid.end()) {
+            gi = (int)gid.size();
+            gid.emplace(pc, gi);
+            gx.push_back((int)pc.size());
+            for (int w = 0; w < kNW; w++) gcap.push_back(w < (int)pc.size() ? pc[w] : model->min_w);
+        } else {
+            gi = it->second;
+        }
+        CC e{};
+        e.group = gi;
+        e.cand = c;
+        e.y = (int)dc.size();
+        for (int w = 0; w < kNW; w++) e.dcap[w] = w < e.y ? dc[w] : model->min_w;
+        ccs.push_back(e);
+    }
+    std::stable_sort(ccs.begin(), ccs.end(), [](const CC& a, const CC& b) { return a.group < b.group; });
+    const int G = (int)gx.size(), NC = (int)ccs.size();
+    std::vector<int> cc_cand(NC), cc_group(NC), cc_y(NC), cc_dcap((size_t)NC * kNW);
+    for (int k = 0; k < NC; k++) {
+        cc_cand[k] = ccs[k].cand; cc_group[k] = ccs[k].group; cc_y[k] = ccs[k].y;
+        for (int w = 0; w < kNW; w++) cc_dcap[(size_t)k * kNW + w] = ccs[k].dcap[w];
+    }
+    FPlan& F = ctx->fplan;
+    std::memset(&F, 0, sizeof(F));
+    F.m.min_w = model->min_w; F.m.max_w = model->max_w; F.m.ncap = model->max_w - model->min_w + 1;
+    F.m.rate = model->prefill_base_rate; F.m.eff = model->prefill_batch_eff;
+    F.m.dec_fixed = model->decode_fixed_s; F.m.dec_per_seq = model->decode_per_seq_s;
+    F.m.dec_per_ctx = model->decode_per_ctx_tok_s; F.m.kvb = model->kv_bytes_per_token;
+    F.m.bw = model->fabric_bw_Bps; F.m.ovh = model->transfer_overhead_s;
+    F.m.max_pb = model->max_prefill_batch; F.m.pb_tokens = model->prefill_token_budget;
+    F.m.max_db = model->max_decode_batch; F.m.slots = model->transfer_slots;
+    F.m.spre = ctx->d_spre; F.m.sdec = ctx->d_sdec; F.m.den = ctx->d_den; F.m.ltab = ctx->d_ltab;
+    F.N = N; F.Q = Q; F.S = S; F.Rmax = std::max(Rmax, 1);
+    F.toff = ctx->d_toff; F.nreq = ctx->d_nreq; F.s_unit = ctx->d_s_unit; F.kv = ctx->d_kv;
+    F.in_tok = ctx->d_in; F.out_tok = ctx->d_out; F.phase = ctx->d_phase; F.qps = ctx->d_qps;
+    F.ttft_slo = slo->ttft_s; F.tpot_slo0 = slo->tpot_s[0]; F.tpot_slo1 = slo->tpot_s[1];
+    F.n_groups = G;
+    F.n_cc = NC;
+    int *d_gx, *d_gcap, *d_ccc, *d_ccg, *d_ccy, *d_ccd;
+    double *d_te, *d_pe;
+    int* d_id;
+    long long* d_evA;
+    const long long GQS = (long long)G * Q * S;
+    const size_t Rm = (size_t)F.Rmax;
+#define AL(p, n) do { int r_ = dalloc(ctx, &(p), (size_t)(n)); if (r_) return r_; } while (0)
+    AL(d_gx, G); AL(d_gcap, (size_t)G * kNW); AL(d_ccc, NC); AL(d_ccg, NC); AL(d_ccy, NC);
+    AL(d_ccd, (size_t)NC * kNW);
+    AL(d_te, GQS * Rm); AL(d_pe, GQS * Rm); AL(d_id, GQS * Rm); AL(d_evA, GQS);
+    CK(cudaMemcpy(d_gx, gx.data(), sizeof(int) * G, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_gcap, gcap.data(), sizeof(int) * G * kNW, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_ccc, cc_cand.data(), sizeof(int) * NC, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_ccg, cc_group.data(), sizeof(int) * NC, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_ccy, cc_y.data(), sizeof(int) * NC, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_ccd, cc_dcap.data(), sizeof(int) * NC * kNW, cudaMemcpyHostToDevice));
+    F.gx = d_gx; F.gcap = d_gcap; F.cc_cand = d_ccc; F.cc_group = d_ccg; F.cc_y = d_ccy; F.cc_dcap = d_ccd;
+    F.st_te = d_te; F.st_pe = d_pe; F.st_id = d_id; F.evA = d_evA;
+    ctx->d_evA = d_evA;
+    ctx->n_evA = (int)GQS;
+    // stage A scratch: one lane-interleaved slot per thread
+    {
+        size_t off = 0;
+        auto take = [&](size_t b) { size_t o = off; off += (b + 255) & ~(size_t)255; return o; };
+        take(Rm * 32 * sizeof(int));
+        F.a_off_tte = take((size_t)PADSIM_MAX_SLOTS * 32 * sizeof(double));
+        F.a_off_tid = take((size_t)PADSIM_MAX_SLOTS * 32 * sizeof(int));
+        F.a_warp_bytes = off;
+        const long long warps = (GQS + 31) / 32;
+        char* scr;
+        AL(scr, (size_t)warps * off);
+        F.scrA = scr;
+        ctx->fA_grid = (int)((GQS + kThreads - 1) / kThreads);
+    }
+    // stage C: persistent CTAs, trace staged in smem by TMA bulk copies
+    {
+        size_t off = 0;
+        auto take = [&](size_t b) { size_t o = off; off += (b + 255) & ~(size_t)255; return o; };
+        take(Rm * 32 * sizeof(int));
+        F.c_off_mem = take((size_t)kNW * model->max_decode_batch * 32 * sizeof(int2));
+        F.c_warp_bytes = off;
+        F.items_per_trace = (int)(((long long)Q * NC + kThreads - 1) / kThreads);
+        F.n_items = F.items_per_trace * S;
+        F.work = ctx->d_work + 2;
+        const bool ctxm = model->decode_per_ctx_tok_s != 0.0;
+        const size_t Rp = (Rm + 15) & ~(size_t)15;
+        const size_t tbytes = Rp * (8 + 4 + (ctxm ? 4 : 0) + 1);
+        F.smem_trace = tbytes <= 64 * 1024 ? 1 : 0;
+        ctx->fC_smem = F.smem_trace ? tbytes : 0;
+        const void* fn = ctxm ? (const void*)stageC_kernel<true> : (const void*)stageC_kernel<false>;
+        CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->fC_smem));
+        int occ = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, ctx->fC_smem));
+        occ = std::max(occ, 1);
+        long long grid = std::min<long long>((long long)ctx->n_sm * occ, F.n_items);
+        size_t fr = 0, tm = 0;
+        CK(cudaMemGetInfo(&fr, &tm));
+        const size_t per_cta = off * kWarps;
+        grid = std::max<long long>(1, std::min<long long>(grid, (long long)((fr * 2 / 5) / per_cta)));
+        char* scr;
+        AL(scr, (size_t)grid * per_cta);
+        F.scrC = scr;
+        ctx->fC_grid = (int)grid;
+    }
+    F.rep_met = ctx->d_rep_met; F.rep_near = ctx->d_rep_near; F.rep_dur = ctx->d_rep_dur;
+    F.rep_good = ctx->d_rep_good; F.rep_events = ctx->d_rep_events;
+    if (ctx->flags & PADSIM_RECORDS) {
+        F.rec_ttft = ctx->d_rec[0]; F.rec_tpot = ctx->d_rec[1]; F.rec_pe = ctx->d_rec[2];
+        F.rec_comp = ctx->d_rec[3]; F.rec_te = ctx->d_rec[4];
+    }
+#undef AL
+    (void)tot;
+    return PADSIM_OK;
+}
+
 extern "C" {
 
 const char* padsim_version(void) { return kVersion; }
@@ -485,7 +625,7 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
     AL(ctx->d_good, CQ);
     AL(ctx->d_near, CQ);
     AL(ctx->d_argmax, n_qps);
-    AL(ctx->d_work, 2);
+    AL(ctx->d_work, 4);
     if (flags & PADSIM_RECORDS) {
         for (auto& r : ctx->d_rec) AL(r, (size_t)R_all * std::max(Rmax, 1));
     }
@@ -510,8 +650,15 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
                                                     ctx->d_ltab, ctx->d_in, ctx->d_kv, tot);
     CK(cudaGetLastError());
 
-    // replay launch plans (static and dynamic candidates run in separate kernels)
+    // factorized static path (stage A prefill groups -> stage C decode) for N <= 8
+    ctx->fact = N <= 8 && !ctx->static_list.empty();
+    if (ctx->fact) {
+        int r_ = plan_factorized(ctx, model, slo, n_qps, n_traces, Rmax, tot, cands);
+        if (r_) return r_;
+    }
+    // replay launch plans for the joint kernel (dynamic candidates; static ones when N > 8)
     for (int dyn = 0; dyn < 2; dyn++) {
+        if (!dyn && ctx->fact) { std::memset(&ctx->plan_static, 0, sizeof(Plan)); continue; }
         const std::vector<int>& lst = dyn ? ctx->dyn_list : ctx->static_list;
         Plan& P = dyn ? ctx->plan_dyn : ctx->plan_static;
         std::memset(&P, 0, sizeof(P));
@@ -591,12 +738,22 @@ int padsim_run(padsim_ctx* ctx, void* stream) {
     if (!ctx->planned) return fail(ctx, PADSIM_EINVAL, "padsim_run before padsim_plan");
     CK(cudaSetDevice(ctx->device));
     cudaStream_t st = (cudaStream_t)stream;
-    CK(cudaMemsetAsync(ctx->d_work, 0, 2 * sizeof(unsigned), st));
+    CK(cudaMemsetAsync(ctx->d_work, 0, 4 * sizeof(unsigned), st));
     if (!ctx->ev0) {
         CK(cudaEventCreate(&ctx->ev0));
         CK(cudaEventCreate(&ctx->ev1));
     }
     CK(cudaEventRecord(ctx->ev0, st));
+    if (ctx->fact) {
+        const FPlan& F = ctx->fplan;
+        stageA_kernel<<<ctx->fA_grid, kThreads, 0, st>>>(F);
+        CK(cudaGetLastError());
+        if (ctx->model.decode_per_ctx_tok_s == 0.0)
+            stageC_kernel<false><<<ctx->fC_grid, kThreads, ctx->fC_smem, st>>>(F);
+        else
+            stageC_kernel<true><<<ctx->fC_grid, kThreads, ctx->fC_smem, st>>>(F);
+        CK(cudaGetLastError());
+    }
     for (int dyn = 0; dyn < 2; dyn++) {
         const Plan& P = dyn ? ctx->plan_dyn : ctx->plan_static;
         if (P.n_clist == 0) continue;
@@ -647,6 +804,8 @@ int padsim_get_device_results(padsim_ctx* ctx, padsim_device_results* o) {
     o->d_rep_duration = ctx->d_rep_dur; o->d_rep_goodput = ctx->d_rep_good;
     o->d_rep_events = (int64_t*)ctx->d_rep_events;
     o->n_cand = ctx->C; o->n_qps = ctx->Q; o->n_traces = ctx->S;
+    o->d_aux_events = (int64_t*)ctx->d_evA;
+    o->n_aux_events = ctx->fact ? ctx->n_evA : 0;
     return PADSIM_OK;
 }
 

@@ -1,0 +1,463 @@
+// static_path.cuh — the factorized static replay (rows a4 + a5) for nodes of
+// up to 8 simulated GPUs, with all per-replay worker state in registers.
+//
+// Why it is exact: for a static candidate nothing on the decode side feeds
+// back into prefill routing, batching or the KV buffer (A8, A9, A12: routing
+// reads only prefill state, the buffer has no decode back-pressure, the
+// controller never acts).  So the joint replay factorises into
+//   stage A (prefill + KV buffer), a function of (prefill caps in P-id order,
+//            QPS, trace) only — shared by every candidate with the same
+//            prefill pool (94 groups for the 955 candidates of cfg 2), and
+//   stage C (decode), a function of stage A's transfer-end stream plus the
+//            decode caps.
+// Same-instant ordering survives the split: in the joint replay prefill ends
+// precede transfer ends (A10) and only prefill state touches the KV buffer;
+// decode step boundaries precede transfer ends and only decode state sees
+// them.  Stage A emits transfer ends in exactly the joint replay's (time, id)
+// order.  Parity tests compare both stages against the joint CPU oracle.
+//
+// Design: one thread per replay; worker state lives in fully unrolled
+// per-worker register arrays indexed only by compile-time constants (a
+// routed-to worker is updated by a predicated unrolled loop), so no local
+// memory is touched; queues are linked through a lane-interleaved per-request
+// `link` scratch array; decode batches ({finish step, id}) live in
+// lane-interleaved scratch.  Stage C stages its CTA's trace in shared memory
+// with cp.async.bulk (TMA) and reads the stream written by stage A.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "replay.cuh"
+
+namespace padsim {
+
+constexpr int kNW = 7;   // ≤ 7 workers per role when N ≤ 8 (each role has ≥ 1 GPU)
+
+struct FPlan {
+    DevModel m;
+    int N, Q, S, Rmax;
+    const long long* toff;
+    const int* nreq;
+    const double* s_unit;
+    const double* kv;
+    const int* in_tok;
+    const int* out_tok;
+    const unsigned char* phase;
+    const double* qps;
+    double ttft_slo, tpot_slo0, tpot_slo1;
+    // prefill groups (stage A)
+    int n_groups;
+    const int* gx;          // [G] prefill workers
+    const int* gcap;        // [G][kNW] their caps, P-id order
+    // stage A → C stream, per (g, q, s) block of Rmax entries
+    double* st_te;          // transfer-end times in (te, id) order
+    int* st_id;             //   and the request ids
+    double* st_pe;          // prefill end, indexed by request id
+    long long* evA;         // [G*Q*S] stage-A instants
+    char* scrA;
+    size_t a_warp_bytes, a_off_tte, a_off_tid;
+    // stage C
+    int n_cc;
+    const int* cc_cand;     // [n_cc] candidate index
+    const int* cc_group;    // [n_cc] prefill group
+    const int* cc_y;        // [n_cc] decode workers
+    const int* cc_dcap;     // [n_cc][kNW] decode caps, D-id order
+    int items_per_trace, n_items;
+    unsigned* work;
+    char* scrC;
+    size_t c_warp_bytes, c_off_mem;
+    int smem_trace;
+    // outputs (r = (c*Q + q)*S + s)
+    int* rep_met;
+    int* rep_near;
+    double* rep_dur;
+    double* rep_good;
+    long long* rep_events;
+    double *rec_ttft, *rec_tpot, *rec_pe, *rec_comp, *rec_te;
+};
+
+// ---------------------------------------------------------------------------
+// stage A: prefill workers + 32-slot KV request buffer → transfer-end stream
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) stageA_kernel(const __grid_constant__ FPlan P) {
+    const long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long U = (long long)P.S * P.Q * P.n_groups;
+    if (u >= U) return;
+    const int g = (int)(u % P.n_groups);
+    const long long sq = u / P.n_groups;
+    const int q = (int)(sq % P.Q), s = (int)(sq / P.Q);
+    const int lane = threadIdx.x & 31;
+    char* wb = P.scrA + (size_t)(u >> 5) * P.a_warp_bytes;
+    int* link = (int*)wb + lane;
+    double* tte = (double*)(wb + P.a_off_tte) + lane;
+    int* tid = (int*)(wb + P.a_off_tid) + lane;
+    const long long off = P.toff[s];
+    const int R = P.nreq[s];
+    const double* su = P.s_unit + off;
+    const double* kv = P.kv + off;
+    const int* it = P.in_tok + off;
+    const long long sb = ((long long)(g * P.Q + q) * P.S + s) * P.Rmax;
+    double* ote = P.st_te + sb;
+    int* oid = P.st_id + sb;
+    double* ope = P.st_pe + sb;
+    const double inv_lam = 1.0 / (P.qps[q] * (double)P.N);
+    const int x = P.gx[g];
+    const int slots = P.m.slots, max_pb = P.m.max_pb, pb_tokens = P.m.pb_tokens;
+
+    double tnext[kNW], sp[kNW];
+    long long a0[kNW];
+    int qh[kNW], qt[kNW], ql[kNW], bh[kNW], bn[kNW];
+#pragma unroll
+    for (int w = 0; w < kNW; w++) {
+        tnext[w] = PAD_INF;
+        a0[w] = w < x ? 0 : 0x7fffffffffffffffLL;
+        qh[w] = qt[w] = kNoIdx;
+        ql[w] = bh[w] = bn[w] = 0;
+        sp[w] = w < x ? P.m.spre[P.gcap[g * kNW + w] - P.m.min_w] : 1.0;
+    }
+    int tbusy = 0, mk = 0, mid = 0, twh = kNoIdx, twt = kNoIdx, twl = 0;
+    double mte = PAD_INF;
+    int na = 0, k = 0;
+    double ta = R > 0 ? su[0] * inv_lam : PAD_INF;
+    long long inst = 0;
+    while (k < R) {
+        double t = fmin(ta, mte);
+#pragma unroll
+        for (int w = 0; w < kNW; w++) t = fmin(t, tnext[w]);
+        inst++;
+        // kind 2: prefill batch ends, worker order; members enter the KV buffer
+#pragma unroll
+        for (int w = 0; w < kNW; w++) {
+            if (tnext[w] == t) {
+                int i = bh[w];
+                const int n = bn[w];
+                for (int z = 0; z < n; z++) {
+                    const int nx = link[(size_t)i * 32];
+                    ope[i] = t;
+                    a0[w] -= it[i];
+                    if (tbusy < slots) {
+                        const double te = t + kv[i];
+                        tte[tbusy * 32] = te;
+                        tid[tbusy * 32] = i;
+                        if (tbusy == 0 || te < mte || (te == mte && i < mid)) { mte = te; mid = i; mk = tbusy; }
+                        tbusy++;
+                    } else {
+                        link[(size_t)i * 32] = kNoIdx;
+                        if (twl == 0) twh = i; else link[(size_t)twt * 32] = i;
+                        twt = i;
+                        twl++;
+                    }
+                    i = nx;
+                }
+                tnext[w] = PAD_INF;
+            }
+        }
+        // kind 4: transfer ends, earliest (te, id) first → the stream
+        while (tbusy > 0 && mte == t) {
+            ote[k] = t;
+            oid[k] = mid;
+            k++;
+            tbusy--;
+            if (mk != tbusy) { tte[mk * 32] = tte[tbusy * 32]; tid[mk * 32] = tid[tbusy * 32]; }
+            if (twl > 0) {
+                const int j = twh;
+                twh = link[(size_t)j * 32];
+                twl--;
+                tte[tbusy * 32] = t + kv[j];
+                tid[tbusy * 32] = j;
+                tbusy++;
+            }
+            mte = PAD_INF;
+            for (int z = 0; z < tbusy; z++) {
+                const double e = tte[z * 32];
+                const int d = tid[z * 32];
+                if (e < mte || (e == mte && d < mid)) { mte = e; mid = d; mk = z; }
+            }
+        }
+        // kind 5: arrivals → least outstanding prefill worker, lowest id (A8)
+        while (ta == t) {
+            const int i = na;
+            int best = 0;
+            long long bl = a0[0];
+#pragma unroll
+            for (int w = 1; w < kNW; w++)
+                if (a0[w] < bl) { bl = a0[w]; best = w; }
+            link[(size_t)i * 32] = kNoIdx;
+            const int tin = it[i];
+#pragma unroll
+            for (int w = 0; w < kNW; w++) {
+                if (w == best) {
+                    if (ql[w] == 0) qh[w] = i; else link[(size_t)qt[w] * 32] = i;
+                    qt[w] = i;
+                    ql[w]++;
+                    a0[w] += tin;
+                }
+            }
+            na++;
+            ta = na < R ? su[na] * inv_lam : PAD_INF;
+        }
+        // dispatch: idle prefill workers take a FIFO prefix (A9)
+#pragma unroll
+        for (int w = 0; w < kNW; w++) {
+            if (tnext[w] == PAD_INF && ql[w] > 0) {
+                const int h = qh[w];
+                long long tok = it[h];
+                int b = 1, j = h;
+                const int qn = ql[w];
+                while (b < max_pb && b < qn) {
+                    const int nx = link[(size_t)j * 32];
+                    const long long tt = tok + it[nx];
+                    if (tt > pb_tokens) break;
+                    tok = tt;
+                    j = nx;
+                    b++;
+                }
+                bh[w] = h;
+                bn[w] = b;
+                ql[w] = qn - b;
+                if (qn > b) qh[w] = link[(size_t)j * 32];
+                tnext[w] = t + ((double)tok / P.m.den[b]) / sp[w];
+            }
+        }
+    }
+    P.evA[(g * P.Q + q) * (long long)P.S + s] = inst;
+}
+
+__device__ __forceinline__ int first_boundary_ge(double tseg, double L, int st0, int stm, double tau) {
+    const float xf = __fdividef((float)(tau - tseg), (float)L);
+    int s = st0 + (int)ceilf(xf);
+    if (s <= stm) s = stm + 1;
+    while (tseg + (double)(s - st0) * L < tau) s++;
+    while (s - 1 > stm && tseg + (double)(s - 1 - st0) * L >= tau) s--;
+    return s;
+}
+
+// ---------------------------------------------------------------------------
+// stage C: decode workers consume the transfer-end stream (A13, A14)
+// ---------------------------------------------------------------------------
+template <bool CTX>
+__global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant__ FPlan P) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ unsigned long long bar;
+    __shared__ int s_item;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    char* wb = P.scrC + ((size_t)blockIdx.x * kWarps + warp) * P.c_warp_bytes;
+    int* link = (int*)wb + lane;
+    int2* mem = (int2*)(wb + P.c_off_mem) + lane;
+    const int max_db = P.m.max_db;
+    if (tid == 0) mbar_init(&bar, 1);
+    __syncthreads();
+    unsigned phase_bit = 0;
+    int cur_s = -1;
+    const int QC = P.Q * P.n_cc;
+    for (;;) {
+        if (tid == 0) s_item = (int)atomicAdd(P.work, 1u);
+        __syncthreads();
+        const int item = s_item;
+        if (item >= P.n_items) break;
+        const int s = item / P.items_per_trace;
+        const int u = (item - s * P.items_per_trace) * kThreads + tid;
+        const long long off = P.toff[s];
+        const int R = P.nreq[s];
+        const double* su;
+        const int* ot;
+        const int* itk;
+        const unsigned char* ph;
+        if (P.smem_trace) {
+            const int Rp = (R + 15) & ~15;
+            double* d_su = (double*)smem;
+            int* d_ot = (int*)(d_su + Rp);
+            int* d_in = d_ot + Rp;
+            unsigned char* d_ph = (unsigned char*)(d_in + (CTX ? Rp : 0));
+            if (s != cur_s) {
+                if (tid == 0 && Rp > 0) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    const unsigned b8 = (unsigned)Rp * 8u, b4 = (unsigned)Rp * 4u, b1 = (unsigned)Rp;
+                    mbar_expect_tx(&bar, b8 + b4 + (CTX ? b4 : 0u) + b1);
+                    bulk_g2s(d_su, P.s_unit + off, b8, &bar);
+                    bulk_g2s(d_ot, P.out_tok + off, b4, &bar);
+                    if (CTX) bulk_g2s(d_in, P.in_tok + off, b4, &bar);
+                    bulk_g2s(d_ph, P.phase + off, b1, &bar);
+                }
+                if (Rp > 0) {
+                    mbar_wait(&bar, phase_bit);
+                    phase_bit ^= 1;
+                }
+                cur_s = s;
+            }
+            su = d_su; ot = d_ot; itk = d_in; ph = d_ph;
+        } else {
+            su = P.s_unit + off; ot = P.out_tok + off; itk = P.in_tok + off; ph = P.phase + off;
+        }
+        if (u < QC) {
+            const int q = u / P.n_cc;
+            const int cc = u - q * P.n_cc;
+            const int c = P.cc_cand[cc];
+            const int g = P.cc_group[cc];
+            const int y = P.cc_y[cc];
+            const long long r = ((long long)c * P.Q + q) * P.S + s;
+            const long long sb = ((long long)(g * P.Q + q) * P.S + s) * P.Rmax;
+            const double* ste = P.st_te + sb;
+            const int* sid = P.st_id + sb;
+            const double* spe = P.st_pe + sb;
+            const long long rb = P.rec_ttft ? r * P.Rmax : -1;
+            const double inv_lam = 1.0 / (P.qps[q] * (double)P.N);
+            double tnext[kNW], tseg[kNW], Ls[kNW];
+            int nact[kNW], qh[kNW], qt[kNW], ql[kNW], stm[kNW], nxs[kNW], st0[kNW], mfin[kNW], ci[kNW];
+            long long ctx[kNW];
+#pragma unroll
+            for (int w = 0; w < kNW; w++) {
+                tnext[w] = PAD_INF; tseg[w] = 0.0; Ls[w] = 1.0;
+                nact[w] = 0; qh[w] = qt[w] = kNoIdx; ql[w] = 0; stm[w] = nxs[w] = st0[w] = 0;
+                mfin[w] = 0x7fffffff;
+                ci[w] = (w < y ? P.cc_dcap[cc * kNW + w] : P.m.min_w) - P.m.min_w;
+                ctx[w] = 0;
+            }
+            unsigned bnd = 0, chg = 0;
+            int completed = 0, met = 0, near = 0, k = 0;
+            double maxcomp = -PAD_INF;
+            double tk = R > 0 ? ste[0] : PAD_INF;
+            long long inst = 0;
+            auto complete = [&](int id, double t, double tpot) {
+                completed++;
+                const double pe = spe[id];
+                const double ttft = pe - su[id] * inv_lam;
+                const double ts = ph[id] ? P.tpot_slo1 : P.tpot_slo0;
+                met += (ttft <= P.ttft_slo && tpot <= ts) ? 1 : 0;
+                near += (fabs(ttft - P.ttft_slo) <= 1e-9 * P.ttft_slo || fabs(tpot - ts) <= 1e-9 * ts) ? 1 : 0;
+                maxcomp = fmax(maxcomp, t);
+                if (rb >= 0) {
+                    P.rec_ttft[rb + id] = ttft;
+                    P.rec_tpot[rb + id] = tpot;
+                    P.rec_pe[rb + id] = pe;
+                    P.rec_comp[rb + id] = t;
+                }
+            };
+            while (completed < R) {
+                double t = tk;
+#pragma unroll
+                for (int w = 0; w < kNW; w++) t = fmin(t, tnext[w]);
+                inst++;
+                // kind 3: materialised decode step boundaries (leaves)
+#pragma unroll
+                for (int w = 0; w < kNW; w++) {
+                    if (tnext[w] == t) {
+                        const int sN = nxs[w];
+                        stm[w] = sN;
+                        bnd |= 1u << w;
+                        tnext[w] = PAD_INF;
+                        if (sN == mfin[w]) {
+                            int n = nact[w], mf = 0x7fffffff, z = 0;
+                            while (z < n) {
+                                const int2 e = mem[((size_t)w * max_db + z) * 32];
+                                if (e.x == sN) {
+                                    const int id = e.y;
+                                    complete(id, t, (t - spe[id]) / (double)(ot[id] - 1));
+                                    if (CTX) ctx[w] -= itk[id];
+                                    n--;
+                                    mem[((size_t)w * max_db + z) * 32] = mem[((size_t)w * max_db + n) * 32];
+                                } else {
+                                    mf = e.x < mf ? e.x : mf;
+                                    z++;
+                                }
+                            }
+                            nact[w] = n;
+                            mfin[w] = mf;
+                            chg |= 1u << w;
+                        }
+                    }
+                }
+                // kind 4: transfer ends from the stream, (te, id) order
+                while (tk == t) {
+                    const int id = sid[k];
+                    k++;
+                    tk = k < R ? ste[k] : PAD_INF;
+                    if (rb >= 0) P.rec_te[rb + id] = t;
+                    if (ot[id] == 1) {
+                        complete(id, t, 0.0);            // S:280 D4
+                    } else {
+                        int best = 0, bl = 0x7fffffff;
+#pragma unroll
+                        for (int w = 0; w < kNW; w++) {
+                            const int l = nact[w] + ql[w];
+                            if (w < y && l < bl) { bl = l; best = w; }
+                        }
+                        link[(size_t)id * 32] = kNoIdx;
+#pragma unroll
+                        for (int w = 0; w < kNW; w++) {
+                            if (w == best) {
+                                if (ql[w] == 0) qh[w] = id; else link[(size_t)qt[w] * 32] = id;
+                                qt[w] = id;
+                                ql[w]++;
+                                if (nact[w] > 0 && !(bnd & (1u << w)) && nact[w] < max_db && ql[w] == 1) {
+                                    const int sj = first_boundary_ge(tseg[w], Ls[w], st0[w], stm[w], t);
+                                    if (sj < nxs[w]) {
+                                        nxs[w] = sj;
+                                        tnext[w] = tseg[w] + (double)(sj - st0[w]) * Ls[w];
+                                    }
+                                }
+                            }
+                        }
+                    }
+                }
+                // dispatch: admissions + segment (re)starts, worker order
+#pragma unroll
+                for (int w = 0; w < kNW; w++) {
+                    if (w >= y) continue;
+                    bool ab = (bnd >> w) & 1u;
+                    bool go = true;
+                    if (nact[w] > 0 && !ab) {
+                        if (tnext[w] == t) { stm[w] = nxs[w]; ab = true; } else go = false;
+                    }
+                    if (go && (ab || ql[w] > 0)) {
+                        const bool was_idle = !ab;
+                        bool joined = false;
+                        int n = nact[w];
+                        const int step = stm[w];
+                        while (n < max_db && ql[w] > 0) {
+                            const int i = qh[w];
+                            ql[w]--;
+                            if (ql[w] > 0) qh[w] = link[(size_t)i * 32];
+                            const int fin = step + (ot[i] - 1);
+                            mem[((size_t)w * max_db + n) * 32] = make_int2(fin, i);
+                            n++;
+                            if (CTX) ctx[w] += itk[i];
+                            mfin[w] = fin < mfin[w] ? fin : mfin[w];
+                            joined = true;
+                        }
+                        nact[w] = n;
+                        if (n > 0) {
+                            if (was_idle || joined || ((chg >> w) & 1u)) {
+                                tseg[w] = t;
+                                st0[w] = step;
+                                if (CTX) {
+                                    double xv = P.m.dec_fixed + P.m.dec_per_seq * (double)n;
+                                    xv = xv + P.m.dec_per_ctx * (double)ctx[w];
+                                    Ls[w] = xv / P.m.sdec[ci[w]];
+                                } else {
+                                    Ls[w] = P.m.ltab[(size_t)ci[w] * max_db + (n - 1)];
+                                }
+                            }
+                            nxs[w] = mfin[w];
+                            tnext[w] = tseg[w] + (double)(mfin[w] - st0[w]) * Ls[w];
+                        } else {
+                            tnext[w] = PAD_INF;
+                            mfin[w] = 0x7fffffff;
+                        }
+                    }
+                }
+                bnd = 0;
+                chg = 0;
+            }
+            P.rep_met[r] = met;
+            P.rep_near[r] = near;
+            const double dur = R > 0 ? maxcomp - su[0] * inv_lam : 0.0;
+            P.rep_dur[r] = dur;
+            P.rep_good[r] = dur > 0 ? (double)met / dur : 0.0;
+            P.rep_events[r] = inst;
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace padsim
