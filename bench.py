@@ -156,13 +156,8 @@ def run_reference(args, cfg, rank, world):
     """--impl reference: the CPU oracle as it stands, bounded sample per step."""
     if rank != 0:
         return
-    import paper_2601_12241_b200 as pkg  # only for the candidate enumeration call
-    try:
-        enum = pkg.enumerate_pool_uniform
-    except Exception:
-        import oracle
-        enum = oracle.enumerate_pool_uniform
-    role, cap, pols, traces, qps = build_workload(cfg, 0, enum)
+    import oracle                       # the reference arm is the oracle alone
+    role, cap, pols, traces, qps = build_workload(cfg, 0, oracle.enumerate_pool_uniform)
     vals = []
     last = None
     for k in range(args.warmup + args.steps):
@@ -277,13 +272,15 @@ def main():
     units = C * Q * S * world
     value = units * args.steps / t_max
     events_per_launch = int(ev_dev.sum().item())
+    if d.n_aux_events > 0:
+        events_per_launch += int(as_tensor(d.d_aux_events, d.n_aux_events, torch.int64, "<i8").sum().item())
 
     # e2e: the public one-shot C-ABI call with host buffers
     e2e_times = []
     h2d = sum(t["s_unit"].nbytes + 4 * t["in_tok"].size * 2 + t["s_unit"].size for t in traces)
     h2d += role.nbytes + cap.nbytes + 48 * C + 8 * Q
     d2h = C * Q * 24 + Q * 4
-    for k in range(args.e2e_steps + 1):
+    for k in range(args.e2e_steps + 1 if args.e2e_steps > 0 else 0):
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
@@ -295,7 +292,7 @@ def main():
             mg.cpu()
         if k > 0:
             e2e_times.append(time.perf_counter() - t0)
-    e2e_t = float(np.mean(e2e_times))
+    e2e_t = float(np.mean(e2e_times)) if e2e_times else float("nan")
     if world > 1:
         tt = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
