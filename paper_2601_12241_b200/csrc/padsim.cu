@@ -82,6 +82,7 @@ struct padsim_ctx {
     size_t fC_smem = 0;
     long long* d_evA = nullptr;
     int n_evA = 0;
+    unsigned* d_workC = nullptr;
 };
 
 static const char* kVersion = "padsim 0.1 (sm_100a)";
@@ -394,31 +395,38 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
         F.scrA = scr;
         ctx->fA_grid = (int)((GQS + kThreads - 1) / kThreads);
     }
-    // stage C: persistent CTAs, trace staged in smem by TMA bulk copies
+    // stage C: CTAs bound to one trace each (staged in smem by TMA bulk copies),
+    // warps pull 32-replay items from that trace's counter
     {
         size_t off = 0;
         auto take = [&](size_t b) { size_t o = off; off += (b + 255) & ~(size_t)255; return o; };
         take(Rm * 32 * sizeof(int));
         F.c_off_mem = take((size_t)kNW * model->max_decode_batch * 32 * sizeof(int2));
         F.c_warp_bytes = off;
-        F.items_per_trace = (int)(((long long)Q * NC + kThreads - 1) / kThreads);
-        F.n_items = F.items_per_trace * S;
-        F.work = ctx->d_work + 2;
+        unsigned* d_wc;
+        AL(d_wc, S);
+        F.work = d_wc;
+        ctx->d_workC = d_wc;
         const bool ctxm = model->decode_per_ctx_tok_s != 0.0;
         const size_t Rp = (Rm + 15) & ~(size_t)15;
         const size_t tbytes = Rp * (8 + 4 + (ctxm ? 4 : 0) + 1);
-        F.smem_trace = tbytes <= 64 * 1024 ? 1 : 0;
-        ctx->fC_smem = F.smem_trace ? tbytes : 0;
+        const size_t wbytes = kCWorkBytes + (ctxm ? kCWorkCtxBytes : 0);
+        F.smem_trace = wbytes + tbytes <= 75 * 1024 ? 1 : 0;
+        ctx->fC_smem = wbytes + (F.smem_trace ? tbytes : 0);
         const void* fn = ctxm ? (const void*)stageC_kernel<true> : (const void*)stageC_kernel<false>;
         CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->fC_smem));
         int occ = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, ctx->fC_smem));
         occ = std::max(occ, 1);
-        long long grid = std::min<long long>((long long)ctx->n_sm * occ, F.n_items);
+        const long long items = ((long long)Q * NC + 31) / 32;        // warp items per trace
+        long long per_trace = std::max<long long>(1, ((long long)ctx->n_sm * occ) / S);
+        per_trace = std::min<long long>(per_trace, (items + kWarps - 1) / kWarps);
         size_t fr = 0, tm = 0;
         CK(cudaMemGetInfo(&fr, &tm));
         const size_t per_cta = off * kWarps;
-        grid = std::max<long long>(1, std::min<long long>(grid, (long long)((fr * 2 / 5) / per_cta)));
+        const long long cap_ctas = std::max<long long>(S, (long long)((fr * 2 / 5) / per_cta));
+        long long grid = std::min<long long>(per_trace * S, (cap_ctas / S) * S);
+        grid = std::max<long long>(grid, S);
         char* scr;
         AL(scr, (size_t)grid * per_cta);
         F.scrC = scr;
@@ -746,6 +754,7 @@ int padsim_run(padsim_ctx* ctx, void* stream) {
     CK(cudaEventRecord(ctx->ev0, st));
     if (ctx->fact) {
         const FPlan& F = ctx->fplan;
+        CK(cudaMemsetAsync(ctx->d_workC, 0, (size_t)ctx->S * sizeof(unsigned), st));
         stageA_kernel<<<ctx->fA_grid, kThreads, 0, st>>>(F);
         CK(cudaGetLastError());
         if (ctx->model.decode_per_ctx_tok_s == 0.0)

@@ -234,229 +234,269 @@ __device__ __forceinline__ int first_boundary_ge(double tseg, double L, int st0,
 
 // ---------------------------------------------------------------------------
 // stage C: decode workers consume the transfer-end stream (A13, A14)
+//
+// Layout: the CTA owns one trace (s = blockIdx.x mod S), staged once in shared
+// memory by TMA bulk copies; its warps pull 32-replay work items from that
+// trace's counter (no CTA barrier per item).  Per decode worker, the next
+// event time and the routing load (active + pending) are register arrays;
+// the rest of its state is a [field][worker][thread] shared-memory SoA, so
+// every handler body is one shared code path indexed by a run-time worker id
+// (lanes at different workers stay convergent) and bank-conflict free.
 // ---------------------------------------------------------------------------
+struct CWork {            // per-thread shared-memory SoA views (stride kThreads)
+    double* tseg;
+    double* Ls;
+    int* nact; int* qh; int* qt; int* ql; int* stm; int* nxs; int* st0; int* mfin; int* ci;
+    long long* ctx;
+};
+
+constexpr size_t kCWorkBytes = (size_t)kNW * kThreads * (2 * sizeof(double) + 9 * sizeof(int));
+constexpr size_t kCWorkCtxBytes = (size_t)kNW * kThreads * sizeof(long long);
+
 template <bool CTX>
 __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant__ FPlan P) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ unsigned long long bar;
-    __shared__ int s_item;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     char* wb = P.scrC + ((size_t)blockIdx.x * kWarps + warp) * P.c_warp_bytes;
     int* link = (int*)wb + lane;
     int2* mem = (int2*)(wb + P.c_off_mem) + lane;
     const int max_db = P.m.max_db;
-    if (tid == 0) mbar_init(&bar, 1);
-    __syncthreads();
-    unsigned phase_bit = 0;
-    int cur_s = -1;
+    // shared memory: worker SoA, then the trace
+    CWork W;
+    {
+        unsigned char* p = smem;
+        const int n = kNW * kThreads;
+        W.tseg = (double*)p + tid; p += n * sizeof(double);
+        W.Ls = (double*)p + tid; p += n * sizeof(double);
+        int* ib = (int*)p;
+        W.nact = ib + 0 * n + tid; W.qh = ib + 1 * n + tid; W.qt = ib + 2 * n + tid;
+        W.ql = ib + 3 * n + tid; W.stm = ib + 4 * n + tid; W.nxs = ib + 5 * n + tid;
+        W.st0 = ib + 6 * n + tid; W.mfin = ib + 7 * n + tid; W.ci = ib + 8 * n + tid;
+        p += 9 * n * sizeof(int);
+        W.ctx = CTX ? (long long*)p + tid : nullptr;
+    }
+    unsigned char* tsm = smem + kCWorkBytes + (CTX ? kCWorkCtxBytes : 0);
+    const int s = blockIdx.x % P.S;
+    const long long off = P.toff[s];
+    const int R = P.nreq[s];
+    const double* su;
+    const int* ot;
+    const int* itk;
+    const unsigned char* ph;
+    if (P.smem_trace) {
+        const int Rp = (R + 15) & ~15;
+        double* d_su = (double*)tsm;
+        int* d_ot = (int*)(d_su + Rp);
+        int* d_in = d_ot + Rp;
+        unsigned char* d_ph = (unsigned char*)(d_in + (CTX ? Rp : 0));
+        if (tid == 0) mbar_init(&bar, 1);
+        __syncthreads();
+        if (tid == 0 && Rp > 0) {
+            const unsigned b8 = (unsigned)Rp * 8u, b4 = (unsigned)Rp * 4u, b1 = (unsigned)Rp;
+            mbar_expect_tx(&bar, b8 + b4 + (CTX ? b4 : 0u) + b1);
+            bulk_g2s(d_su, P.s_unit + off, b8, &bar);
+            bulk_g2s(d_ot, P.out_tok + off, b4, &bar);
+            if (CTX) bulk_g2s(d_in, P.in_tok + off, b4, &bar);
+            bulk_g2s(d_ph, P.phase + off, b1, &bar);
+        }
+        if (Rp > 0) mbar_wait(&bar, 0);
+        su = d_su; ot = d_ot; itk = d_in; ph = d_ph;
+    } else {
+        su = P.s_unit + off; ot = P.out_tok + off; itk = P.in_tok + off; ph = P.phase + off;
+    }
     const int QC = P.Q * P.n_cc;
     for (;;) {
-        if (tid == 0) s_item = (int)atomicAdd(P.work, 1u);
-        __syncthreads();
-        const int item = s_item;
-        if (item >= P.n_items) break;
-        const int s = item / P.items_per_trace;
-        const int u = (item - s * P.items_per_trace) * kThreads + tid;
-        const long long off = P.toff[s];
-        const int R = P.nreq[s];
-        const double* su;
-        const int* ot;
-        const int* itk;
-        const unsigned char* ph;
-        if (P.smem_trace) {
-            const int Rp = (R + 15) & ~15;
-            double* d_su = (double*)smem;
-            int* d_ot = (int*)(d_su + Rp);
-            int* d_in = d_ot + Rp;
-            unsigned char* d_ph = (unsigned char*)(d_in + (CTX ? Rp : 0));
-            if (s != cur_s) {
-                if (tid == 0 && Rp > 0) {
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    const unsigned b8 = (unsigned)Rp * 8u, b4 = (unsigned)Rp * 4u, b1 = (unsigned)Rp;
-                    mbar_expect_tx(&bar, b8 + b4 + (CTX ? b4 : 0u) + b1);
-                    bulk_g2s(d_su, P.s_unit + off, b8, &bar);
-                    bulk_g2s(d_ot, P.out_tok + off, b4, &bar);
-                    if (CTX) bulk_g2s(d_in, P.in_tok + off, b4, &bar);
-                    bulk_g2s(d_ph, P.phase + off, b1, &bar);
-                }
-                if (Rp > 0) {
-                    mbar_wait(&bar, phase_bit);
-                    phase_bit ^= 1;
-                }
-                cur_s = s;
-            }
-            su = d_su; ot = d_ot; itk = d_in; ph = d_ph;
-        } else {
-            su = P.s_unit + off; ot = P.out_tok + off; itk = P.in_tok + off; ph = P.phase + off;
+        int item = 0;
+        if (lane == 0) item = (int)atomicAdd(P.work + s, 1u);
+        item = __shfl_sync(0xffffffffu, item, 0);
+        if (item * 32 >= QC) break;
+        const int u = item * 32 + lane;
+        if (u >= QC) continue;
+        const int q = u / P.n_cc;
+        const int cc = u - q * P.n_cc;
+        const int c = P.cc_cand[cc];
+        const int g = P.cc_group[cc];
+        const int y = P.cc_y[cc];
+        const long long r = ((long long)c * P.Q + q) * P.S + s;
+        const long long sb = ((long long)(g * P.Q + q) * P.S + s) * P.Rmax;
+        const double* ste = P.st_te + sb;
+        const int* sid = P.st_id + sb;
+        const double* spe = P.st_pe + sb;
+        const long long rb = P.rec_ttft ? r * P.Rmax : -1;
+        const double inv_lam = 1.0 / (P.qps[q] * (double)P.N);
+        double tnext[kNW];
+        int ld[kNW];                       // routing load: active + pending (A13)
+#pragma unroll
+        for (int w = 0; w < kNW; w++) {
+            const int o = w * kThreads;
+            tnext[w] = PAD_INF;
+            ld[w] = w < y ? 0 : 0x7fffffff;
+            W.tseg[o] = 0.0; W.Ls[o] = 1.0;
+            W.nact[o] = 0; W.qh[o] = kNoIdx; W.qt[o] = kNoIdx; W.ql[o] = 0;
+            W.stm[o] = 0; W.nxs[o] = 0; W.st0[o] = 0; W.mfin[o] = 0x7fffffff;
+            W.ci[o] = (w < y ? P.cc_dcap[cc * kNW + w] : P.m.min_w) - P.m.min_w;
+            if (CTX) W.ctx[o] = 0;
         }
-        if (u < QC) {
-            const int q = u / P.n_cc;
-            const int cc = u - q * P.n_cc;
-            const int c = P.cc_cand[cc];
-            const int g = P.cc_group[cc];
-            const int y = P.cc_y[cc];
-            const long long r = ((long long)c * P.Q + q) * P.S + s;
-            const long long sb = ((long long)(g * P.Q + q) * P.S + s) * P.Rmax;
-            const double* ste = P.st_te + sb;
-            const int* sid = P.st_id + sb;
-            const double* spe = P.st_pe + sb;
-            const long long rb = P.rec_ttft ? r * P.Rmax : -1;
-            const double inv_lam = 1.0 / (P.qps[q] * (double)P.N);
-            double tnext[kNW], tseg[kNW], Ls[kNW];
-            int nact[kNW], qh[kNW], qt[kNW], ql[kNW], stm[kNW], nxs[kNW], st0[kNW], mfin[kNW], ci[kNW];
-            long long ctx[kNW];
+        int completed = 0, met = 0, near = 0, k = 0;
+        double maxcomp = -PAD_INF;
+        double tk = R > 0 ? ste[0] : PAD_INF;
+        long long inst = 0;
+        auto set_tnext = [&](int wd, double v) {
 #pragma unroll
-            for (int w = 0; w < kNW; w++) {
-                tnext[w] = PAD_INF; tseg[w] = 0.0; Ls[w] = 1.0;
-                nact[w] = 0; qh[w] = qt[w] = kNoIdx; ql[w] = 0; stm[w] = nxs[w] = st0[w] = 0;
-                mfin[w] = 0x7fffffff;
-                ci[w] = (w < y ? P.cc_dcap[cc * kNW + w] : P.m.min_w) - P.m.min_w;
-                ctx[w] = 0;
+            for (int w = 0; w < kNW; w++) if (w == wd) tnext[w] = v;
+        };
+        auto complete = [&](int id, double t, double tpot) {
+            completed++;
+            const double pe = spe[id];
+            const double ttft = pe - su[id] * inv_lam;
+            const double ts = ph[id] ? P.tpot_slo1 : P.tpot_slo0;
+            met += (ttft <= P.ttft_slo && tpot <= ts) ? 1 : 0;
+            near += (fabs(ttft - P.ttft_slo) <= 1e-9 * P.ttft_slo || fabs(tpot - ts) <= 1e-9 * ts) ? 1 : 0;
+            maxcomp = fmax(maxcomp, t);
+            if (rb >= 0) {
+                P.rec_ttft[rb + id] = ttft;
+                P.rec_tpot[rb + id] = tpot;
+                P.rec_pe[rb + id] = pe;
+                P.rec_comp[rb + id] = t;
             }
-            unsigned bnd = 0, chg = 0;
-            int completed = 0, met = 0, near = 0, k = 0;
-            double maxcomp = -PAD_INF;
-            double tk = R > 0 ? ste[0] : PAD_INF;
-            long long inst = 0;
-            auto complete = [&](int id, double t, double tpot) {
-                completed++;
-                const double pe = spe[id];
-                const double ttft = pe - su[id] * inv_lam;
-                const double ts = ph[id] ? P.tpot_slo1 : P.tpot_slo0;
-                met += (ttft <= P.ttft_slo && tpot <= ts) ? 1 : 0;
-                near += (fabs(ttft - P.ttft_slo) <= 1e-9 * P.ttft_slo || fabs(tpot - ts) <= 1e-9 * ts) ? 1 : 0;
-                maxcomp = fmax(maxcomp, t);
-                if (rb >= 0) {
-                    P.rec_ttft[rb + id] = ttft;
-                    P.rec_tpot[rb + id] = tpot;
-                    P.rec_pe[rb + id] = pe;
-                    P.rec_comp[rb + id] = t;
-                }
-            };
-            while (completed < R) {
-                double t = tk;
+        };
+        while (completed < R) {
+            double t = tk;
 #pragma unroll
-                for (int w = 0; w < kNW; w++) t = fmin(t, tnext[w]);
-                inst++;
-                // kind 3: materialised decode step boundaries (leaves)
+            for (int w = 0; w < kNW; w++) t = fmin(t, tnext[w]);
+            inst++;
+            unsigned bnd = 0, touched = 0;
 #pragma unroll
-                for (int w = 0; w < kNW; w++) {
-                    if (tnext[w] == t) {
-                        const int sN = nxs[w];
-                        stm[w] = sN;
-                        bnd |= 1u << w;
-                        tnext[w] = PAD_INF;
-                        if (sN == mfin[w]) {
-                            int n = nact[w], mf = 0x7fffffff, z = 0;
-                            while (z < n) {
-                                const int2 e = mem[((size_t)w * max_db + z) * 32];
-                                if (e.x == sN) {
-                                    const int id = e.y;
-                                    complete(id, t, (t - spe[id]) / (double)(ot[id] - 1));
-                                    if (CTX) ctx[w] -= itk[id];
-                                    n--;
-                                    mem[((size_t)w * max_db + z) * 32] = mem[((size_t)w * max_db + n) * 32];
-                                } else {
-                                    mf = e.x < mf ? e.x : mf;
-                                    z++;
-                                }
-                            }
-                            nact[w] = n;
-                            mfin[w] = mf;
-                            chg |= 1u << w;
-                        }
-                    }
-                }
-                // kind 4: transfer ends from the stream, (te, id) order
-                while (tk == t) {
-                    const int id = sid[k];
-                    k++;
-                    tk = k < R ? ste[k] : PAD_INF;
-                    if (rb >= 0) P.rec_te[rb + id] = t;
-                    if (ot[id] == 1) {
-                        complete(id, t, 0.0);            // S:280 D4
-                    } else {
-                        int best = 0, bl = 0x7fffffff;
-#pragma unroll
-                        for (int w = 0; w < kNW; w++) {
-                            const int l = nact[w] + ql[w];
-                            if (w < y && l < bl) { bl = l; best = w; }
-                        }
-                        link[(size_t)id * 32] = kNoIdx;
-#pragma unroll
-                        for (int w = 0; w < kNW; w++) {
-                            if (w == best) {
-                                if (ql[w] == 0) qh[w] = id; else link[(size_t)qt[w] * 32] = id;
-                                qt[w] = id;
-                                ql[w]++;
-                                if (nact[w] > 0 && !(bnd & (1u << w)) && nact[w] < max_db && ql[w] == 1) {
-                                    const int sj = first_boundary_ge(tseg[w], Ls[w], st0[w], stm[w], t);
-                                    if (sj < nxs[w]) {
-                                        nxs[w] = sj;
-                                        tnext[w] = tseg[w] + (double)(sj - st0[w]) * Ls[w];
-                                    }
-                                }
-                            }
-                        }
-                    }
-                }
-                // dispatch: admissions + segment (re)starts, worker order
-#pragma unroll
-                for (int w = 0; w < kNW; w++) {
-                    if (w >= y) continue;
-                    bool ab = (bnd >> w) & 1u;
-                    bool go = true;
-                    if (nact[w] > 0 && !ab) {
-                        if (tnext[w] == t) { stm[w] = nxs[w]; ab = true; } else go = false;
-                    }
-                    if (go && (ab || ql[w] > 0)) {
-                        const bool was_idle = !ab;
-                        bool joined = false;
-                        int n = nact[w];
-                        const int step = stm[w];
-                        while (n < max_db && ql[w] > 0) {
-                            const int i = qh[w];
-                            ql[w]--;
-                            if (ql[w] > 0) qh[w] = link[(size_t)i * 32];
-                            const int fin = step + (ot[i] - 1);
-                            mem[((size_t)w * max_db + n) * 32] = make_int2(fin, i);
-                            n++;
-                            if (CTX) ctx[w] += itk[i];
-                            mfin[w] = fin < mfin[w] ? fin : mfin[w];
-                            joined = true;
-                        }
-                        nact[w] = n;
-                        if (n > 0) {
-                            if (was_idle || joined || ((chg >> w) & 1u)) {
-                                tseg[w] = t;
-                                st0[w] = step;
-                                if (CTX) {
-                                    double xv = P.m.dec_fixed + P.m.dec_per_seq * (double)n;
-                                    xv = xv + P.m.dec_per_ctx * (double)ctx[w];
-                                    Ls[w] = xv / P.m.sdec[ci[w]];
-                                } else {
-                                    Ls[w] = P.m.ltab[(size_t)ci[w] * max_db + (n - 1)];
-                                }
-                            }
-                            nxs[w] = mfin[w];
-                            tnext[w] = tseg[w] + (double)(mfin[w] - st0[w]) * Ls[w];
+            for (int w = 0; w < kNW; w++) if (tnext[w] == t) bnd |= 1u << w;
+            // kind 3: materialised step boundaries, worker order
+            for (unsigned m = bnd; m; m &= m - 1) {
+                const int w = __ffs(m) - 1;
+                const int o = w * kThreads;
+                const int sN = W.nxs[o];
+                W.stm[o] = sN;
+                set_tnext(w, PAD_INF);
+                if (sN == W.mfin[o]) {
+                    int n = W.nact[o], mf = 0x7fffffff, z = 0, left = 0;
+                    int2* mw = mem + (size_t)w * max_db * 32;
+                    while (z < n) {
+                        const int2 e = mw[(size_t)z * 32];
+                        if (e.x == sN) {
+                            const int id = e.y;
+                            complete(id, t, (t - spe[id]) / (double)(ot[id] - 1));
+                            if (CTX) W.ctx[o] -= itk[id];
+                            n--;
+                            left++;
+                            mw[(size_t)z * 32] = mw[(size_t)n * 32];
                         } else {
-                            tnext[w] = PAD_INF;
-                            mfin[w] = 0x7fffffff;
+                            mf = e.x < mf ? e.x : mf;
+                            z++;
                         }
                     }
+                    W.nact[o] = n;
+                    W.mfin[o] = mf;
+#pragma unroll
+                    for (int v = 0; v < kNW; v++) if (v == w) ld[v] -= left;
+                    touched |= 1u << (w + 16);          // composition changed
                 }
-                bnd = 0;
-                chg = 0;
             }
-            P.rep_met[r] = met;
-            P.rep_near[r] = near;
-            const double dur = R > 0 ? maxcomp - su[0] * inv_lam : 0.0;
-            P.rep_dur[r] = dur;
-            P.rep_good[r] = dur > 0 ? (double)met / dur : 0.0;
-            P.rep_events[r] = inst;
+            // kind 4: transfer ends from the stream, (te, id) order
+            while (tk == t) {
+                const int id = sid[k];
+                k++;
+                tk = k < R ? ste[k] : PAD_INF;
+                if (rb >= 0) P.rec_te[rb + id] = t;
+                if (ot[id] == 1) { complete(id, t, 0.0); continue; }   // S:280 D4
+                int best = 0, bl = ld[0];
+#pragma unroll
+                for (int w = 1; w < kNW; w++) if (ld[w] < bl) { bl = ld[w]; best = w; }
+#pragma unroll
+                for (int w = 0; w < kNW; w++) if (w == best) ld[w]++;
+                const int o = best * kThreads;
+                link[(size_t)id * 32] = kNoIdx;
+                const int qn = W.ql[o];
+                if (qn == 0) W.qh[o] = id; else link[(size_t)W.qt[o] * 32] = id;
+                W.qt[o] = id;
+                W.ql[o] = qn + 1;
+                touched |= 1u << best;
+                const int na = W.nact[o];
+                if (na > 0 && !((bnd >> best) & 1u) && na < max_db && qn == 0) {
+                    const double ts0 = W.tseg[o], L = W.Ls[o];
+                    const int s0 = W.st0[o];
+                    const int sj = first_boundary_ge(ts0, L, s0, W.stm[o], t);
+                    if (sj < W.nxs[o]) {
+                        W.nxs[o] = sj;
+                        set_tnext(best, ts0 + (double)(sj - s0) * L);
+                    }
+                }
+            }
+            // dispatch over the workers this instant touched, worker order
+            for (unsigned m = (bnd | touched) & 0xffffu; m; m &= m - 1) {
+                const int w = __ffs(m) - 1;
+                const int o = w * kThreads;
+                bool ab = (bnd >> w) & 1u;
+                int n = W.nact[o];
+                if (n > 0 && !ab) {
+                    double tw = PAD_INF;
+#pragma unroll
+                    for (int v = 0; v < kNW; v++) if (v == w) tw = tnext[v];
+                    if (tw != t) continue;               // mid-step
+                    W.stm[o] = W.nxs[o];                 // join boundary exactly at t
+                    ab = true;
+                }
+                int qn = W.ql[o];
+                if (!ab && qn == 0) continue;
+                const bool was_idle = !ab;
+                bool joined = false;
+                const int step = W.stm[o];
+                int mf = W.mfin[o];
+                int h = W.qh[o];
+                int2* mw = mem + (size_t)w * max_db * 32;
+                while (n < max_db && qn > 0) {
+                    const int i = h;
+                    qn--;
+                    if (qn > 0) h = link[(size_t)i * 32];
+                    const int fin = step + (ot[i] - 1);
+                    mw[(size_t)n * 32] = make_int2(fin, i);
+                    n++;
+                    if (CTX) W.ctx[o] += itk[i];
+                    mf = fin < mf ? fin : mf;
+                    joined = true;
+                }
+                W.ql[o] = qn;
+                W.qh[o] = h;
+                W.nact[o] = n;
+                if (n > 0) {
+                    double ts0 = W.tseg[o], L = W.Ls[o];
+                    int s0 = W.st0[o];
+                    if (was_idle || joined || ((touched >> (w + 16)) & 1u)) {
+                        ts0 = t;
+                        s0 = step;
+                        const int cix = W.ci[o];
+                        if (CTX) {
+                            double xv = P.m.dec_fixed + P.m.dec_per_seq * (double)n;
+                            xv = xv + P.m.dec_per_ctx * (double)W.ctx[o];
+                            L = xv / P.m.sdec[cix];
+                        } else {
+                            L = P.m.ltab[(size_t)cix * max_db + (n - 1)];
+                        }
+                        W.tseg[o] = ts0; W.st0[o] = s0; W.Ls[o] = L;
+                    }
+                    W.mfin[o] = mf;
+                    W.nxs[o] = mf;
+                    set_tnext(w, ts0 + (double)(mf - s0) * L);
+                } else {
+                    W.mfin[o] = 0x7fffffff;
+                    set_tnext(w, PAD_INF);
+                }
+            }
         }
-        __syncthreads();
+        P.rep_met[r] = met;
+        P.rep_near[r] = near;
+        const double dur = R > 0 ? maxcomp - su[0] * inv_lam : 0.0;
+        P.rep_dur[r] = dur;
+        P.rep_good[r] = dur > 0 ? (double)met / dur : 0.0;
+        P.rep_events[r] = inst;
     }
 }
 
