@@ -204,6 +204,7 @@ def main():
     import torch.distributed as dist
     import paper_2601_12241_b200 as pkg
     from paper_2601_12241_b200.build import build
+    from paper_2601_12241_b200.distributed import allreduce_met, max_over_ranks
     if rank == 0:
         build()
     if world > 1:
@@ -239,7 +240,7 @@ def main():
         ctx.run(stream.cuda_stream)
         if world > 1:
             met_glob.copy_(met_dev)
-            dist.all_reduce(met_glob, op=dist.ReduceOp.SUM)
+            allreduce_met(met_glob)
             ctx.argmax_device(met_glob.data_ptr(), C, Q, am_glob.data_ptr(), stream.cuda_stream)
         return 3 + (1 if world > 1 else 0) + (1 if any(p["kind"] for p in pols) else 0)
 
@@ -264,11 +265,7 @@ def main():
             times.append(e0.elapsed_time(e1))
             replay_ms.append(ctx.replay_kernel_ms())
     t_local = sum(times) / 1e3
-    t_max = t_local
-    if world > 1:
-        tt = torch.tensor([t_local], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_max = float(tt.item())
+    t_max = max_over_ranks(t_local, device=dev)
     units = C * Q * S * world
     value = units * args.steps / t_max
     events_per_launch = int(ev_dev.sum().item())
@@ -288,15 +285,11 @@ def main():
                                        cfg["budget_w"], ctx=ctx)
         if world > 1:
             mg = torch.as_tensor(out["met"].ravel()).to(dev)
-            dist.all_reduce(mg, op=dist.ReduceOp.SUM)
+            allreduce_met(mg)
             mg.cpu()
         if k > 0:
             e2e_times.append(time.perf_counter() - t0)
-    e2e_t = float(np.mean(e2e_times)) if e2e_times else float("nan")
-    if world > 1:
-        tt = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_t = float(tt.item())
+    e2e_t = max_over_ranks(float(np.mean(e2e_times)) if e2e_times else float("nan"), device=dev)
     # restore the plan timed above (evaluate_allocations re-planned the ctx)
 
     if rank == 0:

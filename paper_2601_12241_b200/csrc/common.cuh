@@ -62,6 +62,7 @@ struct Plan {
     char* scratch;
     size_t scratch_per_cta;
     size_t off_link, off_pe, off_mem, off_ordt, off_tst, off_tfl;   // per-warp offsets
+    size_t off_tte, off_tti;           // KV-buffer slots (joint8 kernel)
     size_t warp_bytes;
     int smem_trace;                    // stage the trace in shared memory (TMA bulk)
     size_t smem_trace_bytes;

@@ -1,0 +1,616 @@
+// dynamic_path.cuh — joint replay for nodes of up to 8 simulated GPUs (rows
+// a4–a7, and a6 for dynamic candidates): prefill, KV buffer, decode and the
+// Algorithm 1 controller in one event loop per replay (one thread per replay).
+//
+// Same semantics as replay.cuh (DESIGN.md §3 c.2/c.3), different storage:
+//  * per-GPU next event time and the two routing keys (prefill: outstanding
+//    tokens; decode: active + pending; INT_MAX when the GPU is not eligible —
+//    other role or draining) are register arrays, role masks are bitmasks;
+//  * the remaining per-GPU state is a [field][gpu][thread] shared-memory SoA,
+//    so every handler body is shared across GPUs (run-time GPU index) and
+//    bank-conflict free;
+//  * handlers run only for the GPUs that have an event at the instant, and
+//    the dispatch pass visits only GPUs touched at the instant;
+//  * CTAs are bound to one trace; warps pull 32-replay items from that
+//    trace's counter (no CTA barrier per item);
+//  * window p90 comparisons are exact integer counts (controller.cuh).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "controller.cuh"
+#include "replay.cuh"
+
+namespace padsim {
+
+constexpr int kJG = 8;     // GPU slots (N ≤ 8)
+constexpr int kIntMax = 0x7fffffff;
+
+// smem SoA, stride kThreads
+struct JWork {
+    double* tseg; double* L;
+    int* a0;    // P: outstanding tokens | D: active count
+    int* qh; int* qt; int* ql;        // P: prompt FIFO | D: pending joins
+    int* b0;    // P: batch head | D: last materialised step
+    int* b1;    // P: batch size | D: next boundary to materialise
+    int* st0; int* mfin; int* eff; int* cmd; int* rse; int* ctx;
+    unsigned char* fl;
+};
+constexpr size_t kJWorkBytes = (size_t)kJG * kThreads * (2 * sizeof(double) + 13 * sizeof(int) + 1);
+
+enum : unsigned char { JF_DRAIN = 1, JF_DIRTY = 2 };
+
+struct JCtlView {
+    const JWork* W;
+    unsigned pmask;
+    __device__ int role(int g) const { return ((pmask >> g) & 1u) ? 0 : 1; }
+    __device__ bool draining(int g) const { return (W->fl[g * kThreads] & JF_DRAIN) != 0; }
+    __device__ int target(int g) const {
+        const int r = W->rse[g * kThreads];
+        return r > 0 ? r : W->cmd[g * kThreads];
+    }
+    __device__ long long load(int g) const {
+        const int o = g * kThreads;
+        return ((pmask >> g) & 1u) ? (long long)W->a0[o] : (long long)W->a0[o] + W->ql[o];
+    }
+};
+
+template <bool DYN>
+struct JReplay {
+    const Plan& P;
+    const TraceView& T;
+    const Scratch& X;
+    const JWork& W;
+    int N, R, max_db;
+    double inv_lam;
+    double tnext[kJG];
+    int kp[kJG], kd[kJG];
+    unsigned pmask, dmask;
+    // KV buffer: slots in lane-interleaved scratch (X.tst/X.ordt reused? no: own arrays)
+    double* tte;
+    int* tti;
+    int tbusy, mk, mid, twh, twt, twl;
+    double mte;
+    int completed, met, near;
+    double maxcomp;
+    long long rec_base;
+    // dynamic
+    padsim_policy pol;
+    double tick_t, settle_t, flip_t, last_move;
+    long long tick_k;
+    int flip_g, drain_pending, phase2;
+    int w_th, w_tlo, w_tle, w_tlt, w_ph, w_plo, w_ple0, w_plt0, w_ple1, w_plt1;
+    unsigned touched;
+
+    __device__ JReplay(const Plan& p, const TraceView& t, const Scratch& x, const JWork& w)
+        : P(p), T(t), X(x), W(w) {}
+
+    __device__ __forceinline__ int& LNK(int i) { return X.link[(size_t)i * 32]; }
+    __device__ __forceinline__ double& PE(int i) { return X.pe[(size_t)i * 32]; }
+    __device__ __forceinline__ int2& MEM(int g, int k) { return X.mem[((size_t)g * max_db + k) * 32]; }
+    __device__ __forceinline__ double arr(int i) const { return T.s_unit[i] * inv_lam; }
+    __device__ __forceinline__ void set_tnext(int gd, double v) {
+#pragma unroll
+        for (int g = 0; g < kJG; g++) if (g == gd) tnext[g] = v;
+    }
+    __device__ __forceinline__ double get_tnext(int gd) const {
+        double v = PAD_INF;
+#pragma unroll
+        for (int g = 0; g < kJG; g++) if (g == gd) v = tnext[g];
+        return v;
+    }
+    __device__ __forceinline__ void add_kp(int gd, int d) {
+#pragma unroll
+        for (int g = 0; g < kJG; g++) if (g == gd) kp[g] += d;
+    }
+    __device__ __forceinline__ void add_kd(int gd, int d) {
+#pragma unroll
+        for (int g = 0; g < kJG; g++) if (g == gd) kd[g] += d;
+    }
+    __device__ __forceinline__ double bnd(int o, int s) const {
+        return W.tseg[o] + (double)(s - W.st0[o]) * W.L[o];
+    }
+    __device__ int first_bnd_ge(int o, double tau) const {
+        const double ts = W.tseg[o], L = W.L[o];
+        const int s0 = W.st0[o], stm = W.b0[o];
+        const float xf = __fdividef((float)(tau - ts), (float)L);
+        int s = s0 + (int)ceilf(xf);
+        if (s <= stm) s = stm + 1;
+        while (ts + (double)(s - s0) * L < tau) s++;
+        while (s - 1 > stm && ts + (double)(s - 1 - s0) * L >= tau) s--;
+        return s;
+    }
+
+    __device__ void complete(int i, double t, double tpot) {
+        completed++;
+        const double pe = PE(i);
+        const double ttft = pe - arr(i);
+        const double ts = T.phase[i] ? P.tpot_slo1 : P.tpot_slo0;
+        met += (ttft <= P.ttft_slo && tpot <= ts) ? 1 : 0;
+        near += (fabs(ttft - P.ttft_slo) <= 1e-9 * P.ttft_slo || fabs(tpot - ts) <= 1e-9 * ts) ? 1 : 0;
+        maxcomp = fmax(maxcomp, t);
+        if (DYN) {
+            const unsigned char f = (tpot <= P.tpot_slo0 ? 1 : 0) | (tpot < P.tpot_slo0 ? 2 : 0) |
+                                    (tpot <= P.tpot_slo1 ? 4 : 0) | (tpot < P.tpot_slo1 ? 8 : 0);
+            X.tst[(size_t)w_ph * 32] = t;
+            X.tfl[(size_t)w_ph * 32] = f;
+            w_ph++;
+            w_ple0 += f & 1; w_plt0 += (f >> 1) & 1; w_ple1 += (f >> 2) & 1; w_plt1 += (f >> 3) & 1;
+        }
+        if (rec_base >= 0) {
+            P.rec_ttft[rec_base + i] = ttft;
+            P.rec_tpot[rec_base + i] = tpot;
+            P.rec_pe[rec_base + i] = pe;
+            P.rec_comp[rec_base + i] = t;
+        }
+    }
+
+    // A8: least outstanding non-draining prefill GPU, lowest id
+    __device__ void route_prompt(int i) {
+        int best = 0, bl = kp[0];
+#pragma unroll
+        for (int g = 1; g < kJG; g++) if (kp[g] < bl) { bl = kp[g]; best = g; }
+        const int tin = T.in_tok[i];
+        add_kp(best, tin);
+        const int o = best * kThreads;
+        W.a0[o] += tin;
+        LNK(i) = kNoIdx;
+        const int qn = W.ql[o];
+        if (qn == 0) W.qh[o] = i; else LNK(W.qt[o]) = i;
+        W.qt[o] = i;
+        W.ql[o] = qn + 1;
+        touched |= 1u << best;
+    }
+
+    // A13/A14: fewest active+pending non-draining decode GPU, lowest id; joins
+    // at the first step boundary at or after t
+    __device__ void route_decode(int i, double t, unsigned bm_now) {
+        int best = 0, bl = kd[0];
+#pragma unroll
+        for (int g = 1; g < kJG; g++) if (kd[g] < bl) { bl = kd[g]; best = g; }
+        add_kd(best, 1);
+        const int o = best * kThreads;
+        LNK(i) = kNoIdx;
+        const int qn = W.ql[o];
+        if (qn == 0) W.qh[o] = i; else LNK(W.qt[o]) = i;
+        W.qt[o] = i;
+        W.ql[o] = qn + 1;
+        touched |= 1u << best;
+        const int na = W.a0[o];
+        if (na > 0 && !((bm_now >> best) & 1u) && na < max_db && qn == 0) {
+            const int s = first_bnd_ge(o, t);
+            if (s < W.b1[o]) { W.b1[o] = s; set_tnext(best, bnd(o, s)); }
+        }
+    }
+
+    __device__ void batch_end(int g, double t) {
+        const int o = g * kThreads;
+        int i = W.b0[o];
+        const int n = W.b1[o];
+        int dec = 0;
+        for (int z = 0; z < n; z++) {
+            const int nx = LNK(i);
+            PE(i) = t;
+            dec += T.in_tok[i];
+            if (DYN) {
+                const double ttft = t - arr(i);
+                X.ordt[(size_t)w_th * 32] = i;
+                w_th++;
+                w_tle += ttft <= P.ttft_slo ? 1 : 0;
+                w_tlt += ttft < P.ttft_slo ? 1 : 0;
+            }
+            if (tbusy < P.m.slots) {
+                const double te = t + T.kv[i];
+                tte[tbusy * 32] = te;
+                tti[tbusy * 32] = i;
+                if (tbusy == 0 || te < mte || (te == mte && i < mid)) { mte = te; mid = i; mk = tbusy; }
+                tbusy++;
+            } else {
+                LNK(i) = kNoIdx;
+                if (twl == 0) twh = i; else LNK(twt) = i;
+                twt = i;
+                twl++;
+            }
+            i = nx;
+        }
+        W.a0[o] -= dec;
+        if (!(W.fl[o] & JF_DRAIN)) add_kp(g, -dec);
+        W.b1[o] = 0;
+        set_tnext(g, PAD_INF);
+    }
+
+    // returns true when the composition changed (leaves)
+    __device__ bool boundary(int g, double t) {
+        const int o = g * kThreads;
+        const int s = W.b1[o];
+        W.b0[o] = s;
+        set_tnext(g, PAD_INF);
+        if (s != W.mfin[o]) return false;
+        int n = W.a0[o], mf = kIntMax, z = 0, left = 0;
+        while (z < n) {
+            const int2 e = MEM(g, z);
+            if (e.x == s) {
+                const int id = e.y;
+                complete(id, t, (t - PE(id)) / (double)(T.out_tok[id] - 1));
+                W.ctx[o] -= T.in_tok[id];
+                n--;
+                left++;
+                MEM(g, z) = MEM(g, n);
+            } else {
+                mf = e.x < mf ? e.x : mf;
+                z++;
+            }
+        }
+        W.a0[o] = n;
+        W.mfin[o] = mf;
+        if (!(W.fl[o] & JF_DRAIN)) add_kd(g, -left);
+        return true;
+    }
+
+    __device__ void transfer_end(double t, unsigned bm_now) {
+        const int i = mid;
+        tbusy--;
+        if (mk != tbusy) { tte[mk * 32] = tte[tbusy * 32]; tti[mk * 32] = tti[tbusy * 32]; }
+        if (twl > 0) {
+            const int j = twh;
+            twh = LNK(j);
+            twl--;
+            tte[tbusy * 32] = t + T.kv[j];
+            tti[tbusy * 32] = j;
+            tbusy++;
+        }
+        mte = PAD_INF;
+        for (int z = 0; z < tbusy; z++) {
+            const double e = tte[z * 32];
+            const int d = tti[z * 32];
+            if (e < mte || (e == mte && d < mid)) { mte = e; mid = d; mk = z; }
+        }
+        if (rec_base >= 0) P.rec_te[rec_base + i] = t;
+        if (T.out_tok[i] == 1) complete(i, t, 0.0);
+        else route_decode(i, t, bm_now);
+    }
+
+    __device__ void dispatch_prefill(int g, double t) {
+        const int o = g * kThreads;
+        const int qn = W.ql[o];
+        if (get_tnext(g) != PAD_INF || qn == 0) return;
+        const int h = W.qh[o];
+        long long tok = T.in_tok[h];
+        int b = 1, j = h;
+        while (b < P.m.max_pb && b < qn) {
+            const int nx = LNK(j);
+            const long long tt = tok + T.in_tok[nx];
+            if (tt > P.m.pb_tokens) break;
+            tok = tt;
+            j = nx;
+            b++;
+        }
+        W.b0[o] = h;
+        W.b1[o] = b;
+        W.ql[o] = qn - b;
+        if (qn > b) W.qh[o] = LNK(j);
+        set_tnext(g, t + ((double)tok / P.m.den[b]) / P.m.spre[W.eff[o] - P.m.min_w]);
+    }
+
+    __device__ void dispatch_decode(int g, double t, bool at_bnd, bool changed) {
+        const int o = g * kThreads;
+        int n = W.a0[o];
+        if (n > 0 && !at_bnd) {
+            if (get_tnext(g) != t) return;      // mid-step
+            W.b0[o] = W.b1[o];                  // join boundary exactly at t
+            at_bnd = true;
+        }
+        int qn = W.ql[o];
+        if (!at_bnd && qn == 0) return;
+        const bool was_idle = !at_bnd;
+        bool joined = false;
+        const int step = W.b0[o];
+        int mf = W.mfin[o];
+        int h = W.qh[o];
+        while (n < max_db && qn > 0) {
+            const int i = h;
+            qn--;
+            if (qn > 0) h = LNK(i);
+            const int fin = step + (T.out_tok[i] - 1);
+            MEM(g, n) = make_int2(fin, i);
+            n++;
+            W.ctx[o] += T.in_tok[i];
+            mf = fin < mf ? fin : mf;
+            joined = true;
+        }
+        W.ql[o] = qn;
+        W.qh[o] = h;
+        W.a0[o] = n;
+        if (n > 0) {
+            const unsigned char f = W.fl[o];
+            if (was_idle || joined || changed || (f & JF_DIRTY)) {
+                W.tseg[o] = t;
+                W.st0[o] = step;
+                const int ci = W.eff[o] - P.m.min_w;
+                if (P.m.dec_per_ctx == 0.0) {
+                    W.L[o] = P.m.ltab[(size_t)ci * max_db + (n - 1)];
+                } else {
+                    double xv = P.m.dec_fixed + P.m.dec_per_seq * (double)n;
+                    xv = xv + P.m.dec_per_ctx * (double)W.ctx[o];
+                    W.L[o] = xv / P.m.sdec[ci];
+                }
+                W.fl[o] = f & (unsigned char)~JF_DIRTY;
+            }
+            W.mfin[o] = mf;
+            W.b1[o] = mf;
+            set_tnext(g, bnd(o, mf));
+        } else {
+            W.mfin[o] = kIntMax;
+            set_tnext(g, PAD_INF);
+        }
+    }
+
+    // ---- dynamic ---------------------------------------------------------
+    __device__ void settle(double t) {
+        for (int g = 0; g < N; g++) {
+            const int o = g * kThreads;
+            bool changed = false;
+            int e = W.eff[o], c = W.cmd[o];
+            const int r = W.rse[o];
+            if (c < e) { e = c; changed = true; }
+            if (r > 0) { e = c = r; W.rse[o] = 0; changed = true; }
+            W.eff[o] = e;
+            W.cmd[o] = c;
+            if (changed && ((dmask >> g) & 1u)) {
+                W.fl[o] |= JF_DIRTY;
+                if (W.a0[o] > 0) {
+                    const int s = first_bnd_ge(o, t);
+                    if (s < W.b1[o]) { W.b1[o] = s; set_tnext(g, bnd(o, s)); }
+                }
+            }
+        }
+        settle_t = PAD_INF;
+    }
+
+    __device__ void flip() {
+        const int g = flip_g, o = g * kThreads;
+        const bool to_p = ((dmask >> g) & 1u) != 0;
+        pmask ^= 1u << g;
+        dmask ^= 1u << g;
+        W.fl[o] = 0;
+        W.a0[o] = 0; W.ql[o] = 0; W.b0[o] = 0; W.b1[o] = 0; W.st0[o] = 0;
+        W.mfin[o] = kIntMax; W.ctx[o] = 0;
+        set_tnext(g, PAD_INF);
+#pragma unroll
+        for (int v = 0; v < kJG; v++) {
+            if (v == g) { kp[v] = to_p ? 0 : kIntMax; kd[v] = to_p ? kIntMax : 0; }
+        }
+        drain_pending = 0;
+        flip_g = -1;
+        flip_t = PAD_INF;
+    }
+
+    __device__ void tick(double t, unsigned bm_now) {
+        if ((t - last_move) > pol.cooldown_s) {
+            const double lo = t - pol.window_s;
+            while (w_tlo < w_th) {
+                const int id = X.ordt[(size_t)w_tlo * 32];
+                const double pe = PE(id);
+                if (!(pe < lo)) break;
+                const double ttft = pe - arr(id);
+                w_tle -= ttft <= P.ttft_slo ? 1 : 0;
+                w_tlt -= ttft < P.ttft_slo ? 1 : 0;
+                w_tlo++;
+            }
+            while (w_plo < w_ph && X.tst[(size_t)w_plo * 32] < lo) {
+                const unsigned char f = X.tfl[(size_t)w_plo * 32];
+                w_ple0 -= f & 1; w_plt0 -= (f >> 1) & 1; w_ple1 -= (f >> 2) & 1; w_plt1 -= (f >> 3) & 1;
+                w_plo++;
+            }
+            const int nt = w_th - w_tlo, np = w_ph - w_plo;
+            const int kt = (90 * nt + 99) / 100, kq = (90 * np + 99) / 100;
+            CtlSignals sg;
+            sg.ttft_gt = w_tle < kt;
+            sg.ttft_lt = w_tlt >= kt;
+            sg.tpot_gt = (phase2 ? w_ple1 : w_ple0) < kq;
+            sg.tpot_lt = (phase2 ? w_plt1 : w_plt0) >= kq;
+            int qp = 0;
+            for (unsigned m = pmask; m; m &= m - 1) qp += W.ql[(__ffs(m) - 1) * kThreads];
+            sg.q_prefill = qp;
+            int newcap[kJG];
+            int gsel, dir;
+            JCtlView view{&W, pmask};
+            const int act = ctl_step(pol, P.m.min_w, P.m.max_w, P.B, N, view, drain_pending != 0,
+                                     last_move, t, sg, newcap, &gsel, &dir);
+            if (act == ACT_MOVE_POWER || act == ACT_MOVE_GPU) {
+                last_move = t;
+                if (act == ACT_MOVE_GPU) {
+                    const int g = gsel, o = g * kThreads;
+                    W.fl[o] |= JF_DRAIN;
+                    drain_pending = 1;
+                    flip_g = g;
+                    int i = W.qh[o];
+                    const int n = W.ql[o];
+                    W.ql[o] = 0;
+                    if ((pmask >> g) & 1u) {
+#pragma unroll
+                        for (int v = 0; v < kJG; v++) if (v == g) kp[v] = kIntMax;
+                        for (int z = 0; z < n; z++) {
+                            const int nx = LNK(i);
+                            W.a0[o] -= T.in_tok[i];
+                            route_prompt(i);
+                            i = nx;
+                        }
+                    } else {
+#pragma unroll
+                        for (int v = 0; v < kJG; v++) if (v == g) kd[v] = kIntMax;
+                        for (int z = 0; z < n; z++) {
+                            const int nx = LNK(i);
+                            route_decode(i, t, bm_now);
+                            i = nx;
+                        }
+                    }
+                }
+                for (int g = 0; g < N; g++) {
+                    const int o = g * kThreads;
+                    const int tg = newcap[g];
+                    if (tg < W.cmd[o]) W.cmd[o] = tg;
+                    else if (tg > W.cmd[o]) W.rse[o] = tg;
+                }
+                settle_t = t + pol.settle_s;
+            }
+        }
+        tick_k++;
+        tick_t = (double)tick_k * pol.tick_s;
+    }
+
+    __device__ ReplayResult run(int c, int q, long long rec) {
+        N = P.N;
+        R = T.R;
+        max_db = P.m.max_db;
+        inv_lam = 1.0 / (P.qps[q] * (double)N);
+        rec_base = rec;
+        const unsigned char* crole = P.role + (size_t)c * N;
+        const int* ccap = P.cap + (size_t)c * N;
+        pmask = dmask = 0;
+#pragma unroll
+        for (int g = 0; g < kJG; g++) {
+            const int o = g * kThreads;
+            const bool on = g < N;
+            const int r = on ? crole[g] : 2;
+            if (r == 0) pmask |= 1u << g;
+            if (r == 1) dmask |= 1u << g;
+            tnext[g] = PAD_INF;
+            kp[g] = r == 0 ? 0 : kIntMax;
+            kd[g] = r == 1 ? 0 : kIntMax;
+            W.tseg[o] = 0.0; W.L[o] = 1.0;
+            W.a0[o] = 0; W.qh[o] = kNoIdx; W.qt[o] = kNoIdx; W.ql[o] = 0;
+            W.b0[o] = 0; W.b1[o] = 0; W.st0[o] = 0; W.mfin[o] = kIntMax;
+            W.eff[o] = W.cmd[o] = on ? ccap[g] : P.m.min_w;
+            W.rse[o] = 0; W.ctx[o] = 0; W.fl[o] = 0;
+        }
+        tbusy = 0; mk = 0; mid = 0; twh = twt = kNoIdx; twl = 0;
+        mte = PAD_INF;
+        completed = 0; met = 0; near = 0;
+        maxcomp = -PAD_INF;
+        if (DYN) {
+            pol = P.pol[c];
+            tick_k = 1;
+            tick_t = (double)tick_k * pol.tick_s;
+            settle_t = flip_t = PAD_INF;
+            last_move = 0.0;
+            flip_g = -1; drain_pending = 0; phase2 = 0;
+            w_th = w_tlo = w_tle = w_tlt = 0;
+            w_ph = w_plo = w_ple0 = w_plt0 = w_ple1 = w_plt1 = 0;
+        } else {
+            tick_t = settle_t = flip_t = PAD_INF;
+        }
+        long long events = 0;
+        int na = 0;
+        double ta = R > 0 ? arr(0) : PAD_INF;
+        while (completed < R) {
+            double t = fmin(ta, mte);
+#pragma unroll
+            for (int g = 0; g < kJG; g++) t = fmin(t, tnext[g]);
+            if (DYN) t = fmin(t, fmin(tick_t, fmin(settle_t, flip_t)));
+            events++;
+            touched = 0;
+            if (DYN) {
+                if (settle_t == t) settle(t);
+                if (flip_t == t) flip();
+            }
+            unsigned bm = 0;
+#pragma unroll
+            for (int g = 0; g < kJG; g++) if (tnext[g] == t) bm |= 1u << g;
+            const unsigned bp = bm & pmask, bd = bm & dmask;
+            for (unsigned m = bp; m; m &= m - 1) batch_end(__ffs(m) - 1, t);
+            unsigned chg = 0;
+            for (unsigned m = bd; m; m &= m - 1) {
+                const int g = __ffs(m) - 1;
+                if (boundary(g, t)) chg |= 1u << g;
+            }
+            while (tbusy > 0 && mte == t) transfer_end(t, bd);
+            while (ta == t) {
+                if (DYN && T.phase[na] == 1) phase2 = 1;
+                route_prompt(na);
+                na++;
+                ta = na < R ? arr(na) : PAD_INF;
+            }
+            if (DYN && tick_t == t) tick(t, bd);
+            for (unsigned m = bm | touched; m; m &= m - 1) {
+                const int g = __ffs(m) - 1;
+                if ((pmask >> g) & 1u) dispatch_prefill(g, t);
+                else dispatch_decode(g, t, (bd >> g) & 1u, (chg >> g) & 1u);
+            }
+            if (DYN && flip_g >= 0 && flip_t == PAD_INF) {
+                const int o = flip_g * kThreads;
+                const bool empty = ((pmask >> flip_g) & 1u)
+                                       ? (get_tnext(flip_g) == PAD_INF && W.ql[o] == 0)
+                                       : (W.a0[o] == 0 && W.ql[o] == 0);
+                if (empty) flip_t = t + pol.reassign_s;
+            }
+        }
+        ReplayResult res;
+        res.met = met;
+        res.near = near;
+        res.duration = R > 0 ? maxcomp - arr(0) : 0.0;
+        res.goodput = res.duration > 0 ? (double)met / res.duration : 0.0;
+        res.events = events;
+        return res;
+    }
+};
+
+// CTAs bound to one trace (s = blockIdx.x mod S); warps pull 32-replay items.
+template <bool DYN>
+__global__ void __launch_bounds__(kThreads) joint8_kernel(const __grid_constant__ Plan P) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    JWork W;
+    {
+        const int n = kJG * kThreads;
+        unsigned char* p = smem;
+        W.tseg = (double*)p + tid; p += n * sizeof(double);
+        W.L = (double*)p + tid; p += n * sizeof(double);
+        int* ib = (int*)p;
+        W.a0 = ib + 0 * n + tid; W.qh = ib + 1 * n + tid; W.qt = ib + 2 * n + tid;
+        W.ql = ib + 3 * n + tid; W.b0 = ib + 4 * n + tid; W.b1 = ib + 5 * n + tid;
+        W.st0 = ib + 6 * n + tid; W.mfin = ib + 7 * n + tid; W.eff = ib + 8 * n + tid;
+        W.cmd = ib + 9 * n + tid; W.rse = ib + 10 * n + tid; W.ctx = ib + 11 * n + tid;
+        p += 13 * n * sizeof(int);
+        W.fl = p + tid;
+    }
+    char* wbase = P.scratch + ((size_t)blockIdx.x * kWarps + warp) * P.warp_bytes;
+    Scratch X;
+    X.link = (int*)(wbase + P.off_link) + lane;
+    X.pe = (double*)(wbase + P.off_pe) + lane;
+    X.mem = (int2*)(wbase + P.off_mem) + lane;
+    X.ordt = DYN ? (int*)(wbase + P.off_ordt) + lane : nullptr;
+    X.tst = DYN ? (double*)(wbase + P.off_tst) + lane : nullptr;
+    X.tfl = DYN ? (unsigned char*)(wbase + P.off_tfl) + lane : nullptr;
+    double* tte = (double*)(wbase + P.off_tte) + lane;
+    int* tti = (int*)(wbase + P.off_tti) + lane;
+    const int s = blockIdx.x % P.S;
+    const long long off = P.toff[s];
+    TraceView T;
+    T.R = P.nreq[s];
+    T.s_unit = P.s_unit + off; T.kv = P.kv + off; T.in_tok = P.in_tok + off;
+    T.out_tok = P.out_tok + off; T.phase = P.phase + off;
+    const int QC = P.Q * P.n_clist;
+    for (;;) {
+        int item = 0;
+        if (lane == 0) item = (int)atomicAdd(P.work + s, 1u);
+        item = __shfl_sync(0xffffffffu, item, 0);
+        if (item * 32 >= QC) break;
+        const int u = item * 32 + lane;
+        if (u >= QC) continue;
+        const int q = u / P.n_clist;
+        const int c = P.clist[u - q * P.n_clist];
+        const long long r = ((long long)c * P.Q + q) * P.S + s;
+        JReplay<DYN> rp(P, T, X, W);
+        rp.tte = tte;
+        rp.tti = tti;
+        const ReplayResult res = rp.run(c, q, P.rec_ttft ? r * P.Rmax : -1);
+        P.rep_met[r] = res.met;
+        P.rep_near[r] = res.near;
+        P.rep_dur[r] = res.duration;
+        P.rep_good[r] = res.goodput;
+        P.rep_events[r] = res.events;
+    }
+}
+
+}  // namespace padsim

@@ -19,6 +19,7 @@
 #include "controller.cuh"
 #include "replay.cuh"
 #include "static_path.cuh"
+#include "dynamic_path.cuh"
 
 #include <map>
 
@@ -83,6 +84,8 @@ struct padsim_ctx {
     long long* d_evA = nullptr;
     int n_evA = 0;
     unsigned* d_workC = nullptr;
+    bool j8 = false;            // dynamic candidates on the joint8 kernel (N <= 8)
+    unsigned* d_workJ = nullptr;
 };
 
 static const char* kVersion = "padsim 0.1 (sm_100a)";
@@ -121,6 +124,8 @@ static void free_plan(padsim_ctx* ctx) {
     for (void* p : ctx->bufs) cudaFree(p);
     ctx->bufs.clear();
     ctx->planned = false;
+    ctx->fact = false;
+    ctx->j8 = false;
     ctx->static_list.clear();
     ctx->dyn_list.clear();
     for (auto& r : ctx->d_rec) r = nullptr;
@@ -394,6 +399,8 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
         AL(scr, (size_t)warps * off);
         F.scrA = scr;
         ctx->fA_grid = (int)((GQS + kThreads - 1) / kThreads);
+        CK(cudaFuncSetAttribute((const void*)stageA_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)kAWorkBytes));
     }
     // stage C: CTAs bound to one trace each (staged in smem by TMA bulk copies),
     // warps pull 32-replay items from that trace's counter
@@ -707,8 +714,41 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
             P.off_tst = take(R * 32 * sizeof(double));
             P.off_tfl = take(R * 32);
         }
+        const bool j8 = dyn && N <= 8;
+        if (j8) {
+            P.off_tte = take((size_t)PADSIM_MAX_SLOTS * 32 * sizeof(double));
+            P.off_tti = take((size_t)PADSIM_MAX_SLOTS * 32 * sizeof(int));
+        }
         P.warp_bytes = off;
         P.scratch_per_cta = off * kWarps;
+        if (j8) {
+            ctx->j8 = true;
+            unsigned* d_wj;
+            AL(d_wj, n_traces);
+            ctx->d_workJ = d_wj;
+            P.work = d_wj;
+            P.smem_trace = 0;
+            P.smem_trace_bytes = kJWorkBytes;
+            const void* fnj = (const void*)joint8_kernel<true>;
+            CK(cudaFuncSetAttribute(fnj, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kJWorkBytes));
+            int occj = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occj, fnj, kThreads, kJWorkBytes));
+            occj = std::max(occj, 1);
+            const long long items = ((long long)n_qps * P.n_clist + 31) / 32;
+            long long per_trace = std::max<long long>(1, ((long long)ctx->n_sm * occj) / n_traces);
+            per_trace = std::min<long long>(per_trace, (items + kWarps - 1) / kWarps);
+            size_t frj = 0, tmj = 0;
+            CK(cudaMemGetInfo(&frj, &tmj));
+            const long long cap_ctas = std::max<long long>(n_traces, (long long)((frj * 2 / 5) / P.scratch_per_cta));
+            long long gridj = std::min<long long>(per_trace * n_traces, (cap_ctas / n_traces) * n_traces);
+            gridj = std::max<long long>(gridj, n_traces);
+            char* scrj = nullptr;
+            AL(scrj, (size_t)gridj * P.scratch_per_cta);
+            P.scratch = scrj;
+            ctx->grid_dyn = (int)gridj;
+            ctx->smem_dyn = kJWorkBytes;
+            continue;
+        }
         // trace staging in shared memory via TMA bulk copies when it fits
         const size_t Rp = ((size_t)Rmax + 15) & ~(size_t)15;
         const size_t tbytes = Rp * (8 + 8 + 4 + 4 + 1);
@@ -755,7 +795,7 @@ int padsim_run(padsim_ctx* ctx, void* stream) {
     if (ctx->fact) {
         const FPlan& F = ctx->fplan;
         CK(cudaMemsetAsync(ctx->d_workC, 0, (size_t)ctx->S * sizeof(unsigned), st));
-        stageA_kernel<<<ctx->fA_grid, kThreads, 0, st>>>(F);
+        stageA_kernel<<<ctx->fA_grid, kThreads, kAWorkBytes, st>>>(F);
         CK(cudaGetLastError());
         if (ctx->model.decode_per_ctx_tok_s == 0.0)
             stageC_kernel<false><<<ctx->fC_grid, kThreads, ctx->fC_smem, st>>>(F);
@@ -768,7 +808,10 @@ int padsim_run(padsim_ctx* ctx, void* stream) {
         if (P.n_clist == 0) continue;
         const int grid = dyn ? ctx->grid_dyn : ctx->grid_static;
         const size_t smem = dyn ? ctx->smem_dyn : ctx->smem_static;
-        if (ctx->N <= 8) {
+        if (dyn && ctx->j8) {
+            CK(cudaMemsetAsync(ctx->d_workJ, 0, (size_t)ctx->S * sizeof(unsigned), st));
+            joint8_kernel<true><<<grid, kThreads, smem, st>>>(P);
+        } else if (ctx->N <= 8) {
             if (dyn) replay_kernel<8, true><<<grid, kThreads, smem, st>>>(P);
             else replay_kernel<8, false><<<grid, kThreads, smem, st>>>(P);
         } else {

@@ -78,11 +78,29 @@ struct FPlan {
 
 // ---------------------------------------------------------------------------
 // stage A: prefill workers + 32-slot KV request buffer → transfer-end stream
+//
+// Next event time and routing key (outstanding tokens) per prefill worker are
+// register arrays; queue / batch / speedup state is a [field][worker][thread]
+// shared-memory SoA so handler bodies are shared across workers (run-time
+// worker index, convergent lanes).  The ≤ 32 in-flight transfers live in
+// lane-interleaved scratch with the earliest (te, id) cached in registers.
 // ---------------------------------------------------------------------------
+constexpr size_t kAWorkBytes = (size_t)kNW * kThreads * (sizeof(double) + 5 * sizeof(int));
+
 __global__ void __launch_bounds__(kThreads) stageA_kernel(const __grid_constant__ FPlan P) {
+    extern __shared__ __align__(128) unsigned char smem[];
     const long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long U = (long long)P.S * P.Q * P.n_groups;
     if (u >= U) return;
+    const int tid = threadIdx.x;
+    const int n_sm = kNW * kThreads;
+    double* Wsp = (double*)smem + tid;
+    int* ib = (int*)(smem + (size_t)n_sm * sizeof(double));
+    int* Wqh = ib + 0 * n_sm + tid;
+    int* Wqt = ib + 1 * n_sm + tid;
+    int* Wql = ib + 2 * n_sm + tid;
+    int* Wbh = ib + 3 * n_sm + tid;
+    int* Wbn = ib + 4 * n_sm + tid;
     const int g = (int)(u % P.n_groups);
     const long long sq = u / P.n_groups;
     const int q = (int)(sq % P.Q), s = (int)(sq / P.Q);
@@ -90,7 +108,7 @@ __global__ void __launch_bounds__(kThreads) stageA_kernel(const __grid_constant_
     char* wb = P.scrA + (size_t)(u >> 5) * P.a_warp_bytes;
     int* link = (int*)wb + lane;
     double* tte = (double*)(wb + P.a_off_tte) + lane;
-    int* tid = (int*)(wb + P.a_off_tid) + lane;
+    int* tidb = (int*)(wb + P.a_off_tid) + lane;
     const long long off = P.toff[s];
     const int R = P.nreq[s];
     const double* su = P.s_unit + off;
@@ -104,17 +122,20 @@ __global__ void __launch_bounds__(kThreads) stageA_kernel(const __grid_constant_
     const int x = P.gx[g];
     const int slots = P.m.slots, max_pb = P.m.max_pb, pb_tokens = P.m.pb_tokens;
 
-    double tnext[kNW], sp[kNW];
-    long long a0[kNW];
-    int qh[kNW], qt[kNW], ql[kNW], bh[kNW], bn[kNW];
+    double tnext[kNW];
+    long long a0[kNW];              // outstanding tokens = routing key (A8)
 #pragma unroll
     for (int w = 0; w < kNW; w++) {
+        const int o = w * kThreads;
         tnext[w] = PAD_INF;
         a0[w] = w < x ? 0 : 0x7fffffffffffffffLL;
-        qh[w] = qt[w] = kNoIdx;
-        ql[w] = bh[w] = bn[w] = 0;
-        sp[w] = w < x ? P.m.spre[P.gcap[g * kNW + w] - P.m.min_w] : 1.0;
+        Wqh[o] = kNoIdx; Wqt[o] = kNoIdx; Wql[o] = 0; Wbh[o] = 0; Wbn[o] = 0;
+        Wsp[o] = w < x ? P.m.spre[P.gcap[g * kNW + w] - P.m.min_w] : 1.0;
     }
+    auto set_tnext = [&](int wd, double v) {
+#pragma unroll
+        for (int w = 0; w < kNW; w++) if (w == wd) tnext[w] = v;
+    };
     int tbusy = 0, mk = 0, mid = 0, twh = kNoIdx, twt = kNoIdx, twl = 0;
     double mte = PAD_INF;
     int na = 0, k = 0;
@@ -125,32 +146,37 @@ __global__ void __launch_bounds__(kThreads) stageA_kernel(const __grid_constant_
 #pragma unroll
         for (int w = 0; w < kNW; w++) t = fmin(t, tnext[w]);
         inst++;
-        // kind 2: prefill batch ends, worker order; members enter the KV buffer
+        unsigned bm = 0, touched = 0;
 #pragma unroll
-        for (int w = 0; w < kNW; w++) {
-            if (tnext[w] == t) {
-                int i = bh[w];
-                const int n = bn[w];
-                for (int z = 0; z < n; z++) {
-                    const int nx = link[(size_t)i * 32];
-                    ope[i] = t;
-                    a0[w] -= it[i];
-                    if (tbusy < slots) {
-                        const double te = t + kv[i];
-                        tte[tbusy * 32] = te;
-                        tid[tbusy * 32] = i;
-                        if (tbusy == 0 || te < mte || (te == mte && i < mid)) { mte = te; mid = i; mk = tbusy; }
-                        tbusy++;
-                    } else {
-                        link[(size_t)i * 32] = kNoIdx;
-                        if (twl == 0) twh = i; else link[(size_t)twt * 32] = i;
-                        twt = i;
-                        twl++;
-                    }
-                    i = nx;
+        for (int w = 0; w < kNW; w++) if (tnext[w] == t) bm |= 1u << w;
+        // kind 2: prefill batch ends, worker order; members enter the KV buffer
+        for (unsigned m = bm; m; m &= m - 1) {
+            const int w = __ffs(m) - 1;
+            const int o = w * kThreads;
+            int i = Wbh[o];
+            const int n = Wbn[o];
+            long long dec = 0;
+            for (int z = 0; z < n; z++) {
+                const int nx = link[(size_t)i * 32];
+                ope[i] = t;
+                dec += it[i];
+                if (tbusy < slots) {
+                    const double te = t + kv[i];
+                    tte[tbusy * 32] = te;
+                    tidb[tbusy * 32] = i;
+                    if (tbusy == 0 || te < mte || (te == mte && i < mid)) { mte = te; mid = i; mk = tbusy; }
+                    tbusy++;
+                } else {
+                    link[(size_t)i * 32] = kNoIdx;
+                    if (twl == 0) twh = i; else link[(size_t)twt * 32] = i;
+                    twt = i;
+                    twl++;
                 }
-                tnext[w] = PAD_INF;
+                i = nx;
             }
+#pragma unroll
+            for (int v = 0; v < kNW; v++) if (v == w) a0[v] -= dec;
+            set_tnext(w, PAD_INF);
         }
         // kind 4: transfer ends, earliest (te, id) first → the stream
         while (tbusy > 0 && mte == t) {
@@ -158,19 +184,19 @@ __global__ void __launch_bounds__(kThreads) stageA_kernel(const __grid_constant_
             oid[k] = mid;
             k++;
             tbusy--;
-            if (mk != tbusy) { tte[mk * 32] = tte[tbusy * 32]; tid[mk * 32] = tid[tbusy * 32]; }
+            if (mk != tbusy) { tte[mk * 32] = tte[tbusy * 32]; tidb[mk * 32] = tidb[tbusy * 32]; }
             if (twl > 0) {
                 const int j = twh;
                 twh = link[(size_t)j * 32];
                 twl--;
                 tte[tbusy * 32] = t + kv[j];
-                tid[tbusy * 32] = j;
+                tidb[tbusy * 32] = j;
                 tbusy++;
             }
             mte = PAD_INF;
             for (int z = 0; z < tbusy; z++) {
                 const double e = tte[z * 32];
-                const int d = tid[z * 32];
+                const int d = tidb[z * 32];
                 if (e < mte || (e == mte && d < mid)) { mte = e; mid = d; mk = z; }
             }
         }
@@ -182,42 +208,44 @@ __global__ void __launch_bounds__(kThreads) stageA_kernel(const __grid_constant_
 #pragma unroll
             for (int w = 1; w < kNW; w++)
                 if (a0[w] < bl) { bl = a0[w]; best = w; }
-            link[(size_t)i * 32] = kNoIdx;
             const int tin = it[i];
 #pragma unroll
-            for (int w = 0; w < kNW; w++) {
-                if (w == best) {
-                    if (ql[w] == 0) qh[w] = i; else link[(size_t)qt[w] * 32] = i;
-                    qt[w] = i;
-                    ql[w]++;
-                    a0[w] += tin;
-                }
-            }
+            for (int w = 0; w < kNW; w++) if (w == best) a0[w] += tin;
+            link[(size_t)i * 32] = kNoIdx;
+            const int o = best * kThreads;
+            const int qn = Wql[o];
+            if (qn == 0) Wqh[o] = i; else link[(size_t)Wqt[o] * 32] = i;
+            Wqt[o] = i;
+            Wql[o] = qn + 1;
+            touched |= 1u << best;
             na++;
             ta = na < R ? su[na] * inv_lam : PAD_INF;
         }
         // dispatch: idle prefill workers take a FIFO prefix (A9)
+        for (unsigned m = bm | touched; m; m &= m - 1) {
+            const int w = __ffs(m) - 1;
+            const int o = w * kThreads;
+            double tw = 0.0;
 #pragma unroll
-        for (int w = 0; w < kNW; w++) {
-            if (tnext[w] == PAD_INF && ql[w] > 0) {
-                const int h = qh[w];
-                long long tok = it[h];
-                int b = 1, j = h;
-                const int qn = ql[w];
-                while (b < max_pb && b < qn) {
-                    const int nx = link[(size_t)j * 32];
-                    const long long tt = tok + it[nx];
-                    if (tt > pb_tokens) break;
-                    tok = tt;
-                    j = nx;
-                    b++;
-                }
-                bh[w] = h;
-                bn[w] = b;
-                ql[w] = qn - b;
-                if (qn > b) qh[w] = link[(size_t)j * 32];
-                tnext[w] = t + ((double)tok / P.m.den[b]) / sp[w];
+            for (int v = 0; v < kNW; v++) if (v == w) tw = tnext[v];
+            const int qn = Wql[o];
+            if (tw != PAD_INF || qn == 0) continue;
+            const int h = Wqh[o];
+            long long tok = it[h];
+            int b = 1, j = h;
+            while (b < max_pb && b < qn) {
+                const int nx = link[(size_t)j * 32];
+                const long long tt = tok + it[nx];
+                if (tt > pb_tokens) break;
+                tok = tt;
+                j = nx;
+                b++;
             }
+            Wbh[o] = h;
+            Wbn[o] = b;
+            Wql[o] = qn - b;
+            if (qn > b) Wqh[o] = link[(size_t)j * 32];
+            set_tnext(w, t + ((double)tok / P.m.den[b]) / Wsp[o]);
         }
     }
     P.evA[(g * P.Q + q) * (long long)P.S + s] = inst;
