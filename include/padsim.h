@@ -188,6 +188,11 @@ int padsim_get_device_results(padsim_ctx* ctx, padsim_device_results* out);
  * (synchronises on the end event).                                          */
 int padsim_replay_kernel_ms(padsim_ctx* ctx, float* ms);
 
+/* Per-kernel device times of the last padsim_run in ms (CUDA events on the
+ * run's stream): [0] stage A (static prefill), [1] stage C (static decode),
+ * [2] joint replay (dynamic candidates / static when N > 8); 0 if not run.   */
+int padsim_kernel_times_ms(padsim_ctx* ctx, float* ms3);
+
 /* Per-replay host copies (synchronises): arrays of C*Q*S, any may be NULL. */
 int padsim_fetch_replays(padsim_ctx* ctx, void* stream, int32_t* met, int32_t* near_boundary,
                          double* duration, double* goodput, int64_t* events);

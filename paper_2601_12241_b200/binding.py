@@ -102,7 +102,7 @@ EXPORTS = ["padsim_create", "padsim_destroy", "padsim_last_error", "padsim_versi
            "padsim_evaluate_allocations", "padsim_plan", "padsim_run", "padsim_fetch",
            "padsim_get_device_results", "padsim_fetch_replays", "padsim_fetch_records",
            "padsim_argmax_device", "padsim_step_controller", "padsim_enumerate_pool_uniform",
-           "padsim_replay_kernel_ms"]
+           "padsim_replay_kernel_ms", "padsim_kernel_times_ms"]
 
 _lib = None
 _P = C.POINTER
@@ -132,6 +132,7 @@ def load(path: str = LIB_PATH):
     L.padsim_fetch.argtypes = [vp, vp, _P(Result)]
     L.padsim_get_device_results.argtypes = [vp, _P(DeviceResults)]
     L.padsim_replay_kernel_ms.argtypes = [vp, _P(C.c_float)]
+    L.padsim_kernel_times_ms.argtypes = [vp, _P(C.c_float)]
     L.padsim_fetch_replays.argtypes = [vp, vp, _P(C.c_int32), _P(C.c_int32), _P(C.c_double),
                                        _P(C.c_double), _P(C.c_int64)]
     L.padsim_fetch_records.argtypes = [vp, vp] + [_P(C.c_double)] * 5 + [_P(C.c_int32)]
@@ -289,6 +290,12 @@ class Context:
         ms = C.c_float(0.0)
         self._check(self.L.padsim_replay_kernel_ms(self.ptr, C.byref(ms)), "replay_kernel_ms")
         return float(ms.value)
+
+    def kernel_times_ms(self):
+        """[stage A, stage C, joint] device ms of the last run."""
+        ms = (C.c_float * 3)()
+        self._check(self.L.padsim_kernel_times_ms(self.ptr, ms), "kernel_times_ms")
+        return [float(v) for v in ms]
 
     def fetch_replays(self, stream=None):
         Cn, Q, S, _ = self.shape

@@ -74,7 +74,7 @@ struct padsim_ctx {
     // host staging for the one-shot API
     padsim_ctrl_state* d_ctl_state = nullptr;
     padsim_action* d_ctl_act = nullptr;
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, evA = nullptr, evC = nullptr;
     bool ev_recorded = false;
     // factorized static path (N <= 8)
     bool fact = false;
@@ -84,6 +84,7 @@ struct padsim_ctx {
     long long* d_evA = nullptr;
     int n_evA = 0;
     unsigned* d_workC = nullptr;
+    std::vector<int> max_out;   // per trace
     bool j8 = false;            // dynamic candidates on the joint8 kernel (N <= 8)
     unsigned* d_workJ = nullptr;
 };
@@ -408,7 +409,13 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
         size_t off = 0;
         auto take = [&](size_t b) { size_t o = off; off += (b + 255) & ~(size_t)255; return o; };
         take(Rm * 32 * sizeof(int));
-        F.c_off_mem = take((size_t)kNW * model->max_decode_batch * 32 * sizeof(int2));
+        int maxo = 2;
+        for (int s2 = 0; s2 < S; s2++) maxo = std::max(maxo, ctx->max_out[s2]);
+        int wheel = 32;
+        while (wheel < maxo) wheel <<= 1;        // finish steps lie in (step, step + out − 1]
+        F.wheel = wheel;
+        F.c_off_heads = take((size_t)kNW * wheel * 32 * sizeof(int));
+        F.c_off_bits = take((size_t)kNW * (wheel / 32) * 32 * sizeof(unsigned));
         F.c_warp_bytes = off;
         unsigned* d_wc;
         AL(d_wc, S);
@@ -483,6 +490,8 @@ void padsim_destroy(padsim_ctx* ctx) {
     if (ctx->d_ctl_act) cudaFree(ctx->d_ctl_act);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    if (ctx->evA) cudaEventDestroy(ctx->evA);
+    if (ctx->evC) cudaEventDestroy(ctx->evC);
     delete ctx;
 }
 
@@ -601,6 +610,10 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
     std::vector<int> hin(tot, 1), hout(tot, 1);
     std::vector<unsigned char> hph(tot, 0);
     std::vector<int> nreq(n_traces);
+    ctx->max_out.assign(n_traces, 1);
+    for (int s2 = 0; s2 < n_traces; s2++)
+        for (int i = 0; i < traces[s2].n_req; i++)
+            ctx->max_out[s2] = std::max(ctx->max_out[s2], (int)traces[s2].out_tok[i]);
     for (int s = 0; s < n_traces; s++) {
         const padsim_trace& t = traces[s];
         nreq[s] = t.n_req;
@@ -790,6 +803,8 @@ int padsim_run(padsim_ctx* ctx, void* stream) {
     if (!ctx->ev0) {
         CK(cudaEventCreate(&ctx->ev0));
         CK(cudaEventCreate(&ctx->ev1));
+        CK(cudaEventCreate(&ctx->evA));
+        CK(cudaEventCreate(&ctx->evC));
     }
     CK(cudaEventRecord(ctx->ev0, st));
     if (ctx->fact) {
@@ -797,12 +812,16 @@ int padsim_run(padsim_ctx* ctx, void* stream) {
         CK(cudaMemsetAsync(ctx->d_workC, 0, (size_t)ctx->S * sizeof(unsigned), st));
         stageA_kernel<<<ctx->fA_grid, kThreads, kAWorkBytes, st>>>(F);
         CK(cudaGetLastError());
+        CK(cudaEventRecord(ctx->evA, st));
         if (ctx->model.decode_per_ctx_tok_s == 0.0)
             stageC_kernel<false><<<ctx->fC_grid, kThreads, ctx->fC_smem, st>>>(F);
         else
             stageC_kernel<true><<<ctx->fC_grid, kThreads, ctx->fC_smem, st>>>(F);
         CK(cudaGetLastError());
+    } else {
+        CK(cudaEventRecord(ctx->evA, st));
     }
+    CK(cudaEventRecord(ctx->evC, st));
     for (int dyn = 0; dyn < 2; dyn++) {
         const Plan& P = dyn ? ctx->plan_dyn : ctx->plan_static;
         if (P.n_clist == 0) continue;
@@ -867,6 +886,17 @@ int padsim_replay_kernel_ms(padsim_ctx* ctx, float* ms) {
     CK(cudaSetDevice(ctx->device));
     CK(cudaEventSynchronize(ctx->ev1));
     CK(cudaEventElapsedTime(ms, ctx->ev0, ctx->ev1));
+    return PADSIM_OK;
+}
+
+int padsim_kernel_times_ms(padsim_ctx* ctx, float* ms3) {
+    if (!ctx || !ms3) return PADSIM_EINVAL;
+    if (!ctx->ev_recorded) return fail(ctx, PADSIM_EINVAL, "no run recorded");
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaEventSynchronize(ctx->ev1));
+    CK(cudaEventElapsedTime(&ms3[0], ctx->ev0, ctx->evA));
+    CK(cudaEventElapsedTime(&ms3[1], ctx->evA, ctx->evC));
+    CK(cudaEventElapsedTime(&ms3[2], ctx->evC, ctx->ev1));
     return PADSIM_OK;
 }
 

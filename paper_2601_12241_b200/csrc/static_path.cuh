@@ -65,7 +65,8 @@ struct FPlan {
     int items_per_trace, n_items;
     unsigned* work;
     char* scrC;
-    size_t c_warp_bytes, c_off_mem;
+    size_t c_warp_bytes, c_off_heads, c_off_bits;
+    int wheel;              // decode timing wheel size (power of 2 > max out_tok − 1, ≥ 32)
     int smem_trace;
     // outputs (r = (c*Q + q)*S + s)
     int* rep_met;
@@ -288,8 +289,10 @@ __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant_
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     char* wb = P.scrC + ((size_t)blockIdx.x * kWarps + warp) * P.c_warp_bytes;
     int* link = (int*)wb + lane;
-    int2* mem = (int2*)(wb + P.c_off_mem) + lane;
+    int* heads = (int*)(wb + P.c_off_heads) + lane;       // [(w*Wh + b)*32]
+    unsigned* bits = (unsigned*)(wb + P.c_off_bits) + lane;  // [(w*Wh/32 + k)*32]
     const int max_db = P.m.max_db;
+    const int Wh = P.wheel, Wm = P.wheel - 1, nwords = P.wheel >> 5;
     // shared memory: worker SoA, then the trace
     CWork W;
     {
@@ -366,6 +369,7 @@ __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant_
             W.ci[o] = (w < y ? P.cc_dcap[cc * kNW + w] : P.m.min_w) - P.m.min_w;
             if (CTX) W.ctx[o] = 0;
         }
+        for (int z = 0; z < y * nwords; z++) bits[(size_t)z * 32] = 0u;
         int completed = 0, met = 0, near = 0, k = 0;
         double maxcomp = -PAD_INF;
         double tk = R > 0 ? ste[0] : PAD_INF;
@@ -405,23 +409,34 @@ __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant_
                 W.stm[o] = sN;
                 set_tnext(w, PAD_INF);
                 if (sN == W.mfin[o]) {
-                    int n = W.nact[o], mf = 0x7fffffff, z = 0, left = 0;
-                    int2* mw = mem + (size_t)w * max_db * 32;
-                    while (z < n) {
-                        const int2 e = mw[(size_t)z * 32];
-                        if (e.x == sN) {
-                            const int id = e.y;
-                            complete(id, t, (t - spe[id]) / (double)(ot[id] - 1));
-                            if (CTX) W.ctx[o] -= itk[id];
-                            n--;
-                            left++;
-                            mw[(size_t)z * 32] = mw[(size_t)n * 32];
-                        } else {
-                            mf = e.x < mf ? e.x : mf;
-                            z++;
-                        }
+                    // timing wheel: every member finishing at step sN is in bucket sN mod Wh
+                    const int b = sN & Wm;
+                    int* hp = heads + ((size_t)w * Wh + b) * 32;
+                    int id = *hp;
+                    int left = 0;
+                    while (id != kNoIdx) {
+                        const int nx = link[(size_t)id * 32];
+                        complete(id, t, (t - spe[id]) / (double)(ot[id] - 1));
+                        if (CTX) W.ctx[o] -= itk[id];
+                        left++;
+                        id = nx;
                     }
+                    unsigned* bw = bits + (size_t)w * nwords * 32;
+                    bw[(size_t)(b >> 5) * 32] &= ~(1u << (b & 31));
+                    const int n = W.nact[o] - left;
                     W.nact[o] = n;
+                    int mf = 0x7fffffff;
+                    if (n > 0) {   // next occupied bucket after b (all finish steps lie in (sN, sN+Wh))
+                        const int st = (b + 1) & Wm;
+                        int wi = st >> 5;
+                        unsigned mword = bw[(size_t)wi * 32] & (0xffffffffu << (st & 31));
+                        while (mword == 0u) {
+                            wi = (wi + 1) & (nwords - 1);
+                            mword = bw[(size_t)wi * 32];
+                        }
+                        const int b2 = (wi << 5) + __ffs(mword) - 1;
+                        mf = sN + ((b2 - b) & Wm);
+                    }
                     W.mfin[o] = mf;
 #pragma unroll
                     for (int v = 0; v < kNW; v++) if (v == w) ld[v] -= left;
@@ -479,13 +494,21 @@ __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant_
                 const int step = W.stm[o];
                 int mf = W.mfin[o];
                 int h = W.qh[o];
-                int2* mw = mem + (size_t)w * max_db * 32;
+                int* hw = heads + (size_t)w * Wh * 32;
+                unsigned* bw = bits + (size_t)w * nwords * 32;
                 while (n < max_db && qn > 0) {
                     const int i = h;
                     qn--;
                     if (qn > 0) h = link[(size_t)i * 32];
                     const int fin = step + (ot[i] - 1);
-                    mw[(size_t)n * 32] = make_int2(fin, i);
+                    const int b = fin & Wm;
+                    int* hp = hw + (size_t)b * 32;
+                    unsigned* wp = bw + (size_t)(b >> 5) * 32;
+                    const unsigned bit = 1u << (b & 31);
+                    const unsigned old = *wp;
+                    link[(size_t)i * 32] = (old & bit) ? *hp : kNoIdx;
+                    *hp = i;
+                    *wp = old | bit;
                     n++;
                     if (CTX) W.ctx[o] += itk[i];
                     mf = fin < mf ? fin : mf;
