@@ -69,6 +69,9 @@ struct JReplay {
     // KV buffer: slots in lane-interleaved scratch (X.tst/X.ordt reused? no: own arrays)
     double* tte;
     int* tti;
+    int* heads;          // [(g*wheel + b)*32]
+    unsigned* bits;      // [(g*wheel/32 + k)*32]
+    int Wh, Wm, nwords;
     int tbusy, mk, mid, twh, twt, twl;
     double mte;
     int completed, met, near;
@@ -87,7 +90,6 @@ struct JReplay {
 
     __device__ __forceinline__ int& LNK(int i) { return X.link[(size_t)i * 32]; }
     __device__ __forceinline__ double& PE(int i) { return X.pe[(size_t)i * 32]; }
-    __device__ __forceinline__ int2& MEM(int g, int k) { return X.mem[((size_t)g * max_db + k) * 32]; }
     __device__ __forceinline__ double arr(int i) const { return T.s_unit[i] * inv_lam; }
     __device__ __forceinline__ void set_tnext(int gd, double v) {
 #pragma unroll
@@ -219,29 +221,40 @@ struct JReplay {
         set_tnext(g, PAD_INF);
     }
 
-    // returns true when the composition changed (leaves)
+    // returns true when the composition changed (leaves).  Decode batches are
+    // a timing wheel: bucket (finish step mod Wh) chains its members through
+    // link[]; an occupancy bitmap gives the next finish step.
     __device__ bool boundary(int g, double t) {
         const int o = g * kThreads;
         const int s = W.b1[o];
         W.b0[o] = s;
         set_tnext(g, PAD_INF);
         if (s != W.mfin[o]) return false;
-        int n = W.a0[o], mf = kIntMax, z = 0, left = 0;
-        while (z < n) {
-            const int2 e = MEM(g, z);
-            if (e.x == s) {
-                const int id = e.y;
-                complete(id, t, (t - PE(id)) / (double)(T.out_tok[id] - 1));
-                W.ctx[o] -= T.in_tok[id];
-                n--;
-                left++;
-                MEM(g, z) = MEM(g, n);
-            } else {
-                mf = e.x < mf ? e.x : mf;
-                z++;
-            }
+        const int b = s & Wm;
+        int id = heads[((size_t)g * Wh + b) * 32];
+        int left = 0;
+        while (id != kNoIdx) {
+            const int nx = LNK(id);
+            complete(id, t, (t - PE(id)) / (double)(T.out_tok[id] - 1));
+            W.ctx[o] -= T.in_tok[id];
+            left++;
+            id = nx;
         }
+        unsigned* bw = bits + (size_t)g * nwords * 32;
+        bw[(size_t)(b >> 5) * 32] &= ~(1u << (b & 31));
+        const int n = W.a0[o] - left;
         W.a0[o] = n;
+        int mf = kIntMax;
+        if (n > 0) {
+            const int st = (b + 1) & Wm;
+            int wi = st >> 5;
+            unsigned mword = bw[(size_t)wi * 32] & (0xffffffffu << (st & 31));
+            while (mword == 0u) {
+                wi = (wi + 1) & (nwords - 1);
+                mword = bw[(size_t)wi * 32];
+            }
+            mf = s + ((((wi << 5) + __ffs(mword) - 1) - b) & Wm);
+        }
         W.mfin[o] = mf;
         if (!(W.fl[o] & JF_DRAIN)) add_kd(g, -left);
         return true;
@@ -307,12 +320,20 @@ struct JReplay {
         const int step = W.b0[o];
         int mf = W.mfin[o];
         int h = W.qh[o];
+        int* hw = heads + (size_t)g * Wh * 32;
+        unsigned* bw = bits + (size_t)g * nwords * 32;
         while (n < max_db && qn > 0) {
             const int i = h;
             qn--;
             if (qn > 0) h = LNK(i);
             const int fin = step + (T.out_tok[i] - 1);
-            MEM(g, n) = make_int2(fin, i);
+            const int b = fin & Wm;
+            unsigned* wp = bw + (size_t)(b >> 5) * 32;
+            const unsigned bit = 1u << (b & 31);
+            const unsigned old = *wp;
+            LNK(i) = (old & bit) ? hw[(size_t)b * 32] : kNoIdx;
+            hw[(size_t)b * 32] = i;
+            *wp = old | bit;
             n++;
             W.ctx[o] += T.in_tok[i];
             mf = fin < mf ? fin : mf;
@@ -484,6 +505,8 @@ struct JReplay {
             W.eff[o] = W.cmd[o] = on ? ccap[g] : P.m.min_w;
             W.rse[o] = 0; W.ctx[o] = 0; W.fl[o] = 0;
         }
+        Wh = P.wheel; Wm = Wh - 1; nwords = Wh >> 5;
+        for (int z = 0; z < kJG * nwords; z++) bits[(size_t)z * 32] = 0u;
         tbusy = 0; mk = 0; mid = 0; twh = twt = kNoIdx; twl = 0;
         mte = PAD_INF;
         completed = 0; met = 0; near = 0;
@@ -604,6 +627,8 @@ __global__ void __launch_bounds__(kThreads) joint8_kernel(const __grid_constant_
         JReplay<DYN> rp(P, T, X, W);
         rp.tte = tte;
         rp.tti = tti;
+        rp.heads = (int*)(wbase + P.off_heads) + lane;
+        rp.bits = (unsigned*)(wbase + P.off_bits) + lane;
         const ReplayResult res = rp.run(c, q, P.rec_ttft ? r * P.Rmax : -1);
         P.rep_met[r] = res.met;
         P.rep_near[r] = res.near;

@@ -721,16 +721,23 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
         auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~(size_t)255; return o; };
         P.off_link = take(R * 32 * sizeof(int));
         P.off_pe = take(R * 32 * sizeof(double));
-        P.off_mem = take((size_t)N * model->max_decode_batch * 32 * sizeof(int2));
+        const bool j8 = dyn && N <= 8;
+        if (!j8) P.off_mem = take((size_t)N * model->max_decode_batch * 32 * sizeof(int2));
         if (dyn) {
             P.off_ordt = take(R * 32 * sizeof(int));
             P.off_tst = take(R * 32 * sizeof(double));
             P.off_tfl = take(R * 32);
         }
-        const bool j8 = dyn && N <= 8;
         if (j8) {
             P.off_tte = take((size_t)PADSIM_MAX_SLOTS * 32 * sizeof(double));
             P.off_tti = take((size_t)PADSIM_MAX_SLOTS * 32 * sizeof(int));
+            int maxo = 2;
+            for (int s2 = 0; s2 < n_traces; s2++) maxo = std::max(maxo, ctx->max_out[s2]);
+            int wheel = 32;
+            while (wheel < maxo) wheel <<= 1;
+            P.wheel = wheel;
+            P.off_heads = take((size_t)kJG * wheel * 32 * sizeof(int));
+            P.off_bits = take((size_t)kJG * (wheel / 32) * 32 * sizeof(unsigned));
         }
         P.warp_bytes = off;
         P.scratch_per_cta = off * kWarps;
