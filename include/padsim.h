@@ -190,7 +190,8 @@ int padsim_replay_kernel_ms(padsim_ctx* ctx, float* ms);
 
 /* Per-kernel device times of the last padsim_run in ms (CUDA events on the
  * run's stream): [0] stage A (static prefill), [1] stage C (static decode),
- * [2] joint replay (dynamic candidates / static when N > 8); 0 if not run.   */
+ * [2] joint replay (dynamic candidates / static when N > 8), which runs on
+ * a side stream concurrently with [0]+[1]; 0 if not run.                   */
 int padsim_kernel_times_ms(padsim_ctx* ctx, float* ms3);
 
 /* Per-replay host copies (synchronises): arrays of C*Q*S, any may be NULL. */

@@ -406,8 +406,12 @@ struct JReplay {
         flip_t = PAD_INF;
     }
 
-    __device__ void tick(double t, unsigned bm_now) {
+    // returns 0: cooldown not elapsed (guards not evaluated), 1: evaluated, no
+    // move (none or saturated), 2: a move was made
+    __device__ int tick(double t, unsigned bm_now) {
+        int acted = 0;
         if ((t - last_move) > pol.cooldown_s) {
+            acted = 1;
             const double lo = t - pol.window_s;
             while (w_tlo < w_th) {
                 const int id = X.ordt[(size_t)w_tlo * 32];
@@ -474,10 +478,58 @@ struct JReplay {
                     else if (tg > W.cmd[o]) W.rse[o] = tg;
                 }
                 settle_t = t + pol.settle_s;
+                acted = 2;
             }
         }
         tick_k++;
         tick_t = (double)tick_k * pol.tick_s;
+        return acted;
+    }
+
+    // first tick index k >= k0 with (double)k * tick_s >= x
+    __device__ long long tick_at_or_after(double x, long long k0) const {
+        if (!(x < PAD_INF)) return 0x7fffffffffffffffLL;
+        long long k = (long long)ceil(x / pol.tick_s);
+        if (k < k0) k = k0;
+        while ((double)k * pol.tick_s < x) k++;
+        while (k - 1 >= k0 && (double)(k - 1) * pol.tick_s >= x) k--;
+        return k;
+    }
+    // first tick index k >= k0 with stamp < (double)k * tick_s − window  (sample expiry)
+    __device__ long long expiry_tick(double stamp, long long k0) const {
+        long long k = (long long)floor((stamp + pol.window_s) / pol.tick_s);
+        if (k < k0) k = k0;
+        while (!(stamp < (double)k * pol.tick_s - pol.window_s)) k++;
+        while (k - 1 >= k0 && stamp < (double)(k - 1) * pol.tick_s - pol.window_s) k--;
+        return k;
+    }
+    // first tick index k >= k0 with ((double)k * tick_s − last_move) > cooldown
+    __device__ long long cooldown_tick(long long k0) const {
+        long long k = (long long)floor((last_move + pol.cooldown_s) / pol.tick_s);
+        if (k < k0) k = k0;
+        while (!(((double)k * pol.tick_s - last_move) > pol.cooldown_s)) k++;
+        while (k - 1 >= k0 && ((double)(k - 1) * pol.tick_s - last_move) > pol.cooldown_s) k--;
+        return k;
+    }
+
+    // Tick skipping (exact): after a tick that changed nothing, no later tick can
+    // act before (a) the next pending event changes the state, (b) a sample leaves
+    // a metric window, or (c) the cooldown elapses; the decision depends on
+    // nothing else.  Jump to the first grid tick that can see one of these.
+    __device__ void skip_ticks(int outcome, double next_event) {
+        const long long k0 = tick_k;
+        long long k;
+        if (outcome == 0) {
+            k = cooldown_tick(k0);           // no tick before it can act, whatever happens
+        } else {
+            k = tick_at_or_after(next_event, k0);
+            if (w_tlo < w_th) k = min(k, expiry_tick(PE(X.ordt[(size_t)w_tlo * 32]), k0));
+            if (w_plo < w_ph) k = min(k, expiry_tick(X.tst[(size_t)w_plo * 32], k0));
+        }
+        if (k > k0 && k != 0x7fffffffffffffffLL) {
+            tick_k = k;
+            tick_t = (double)tick_k * pol.tick_s;
+        }
     }
 
     __device__ ReplayResult run(int c, int q, long long rec) {
@@ -554,7 +606,8 @@ struct JReplay {
                 na++;
                 ta = na < R ? arr(na) : PAD_INF;
             }
-            if (DYN && tick_t == t) tick(t, bd);
+            int tick_outcome = 2;
+            if (DYN && tick_t == t) tick_outcome = tick(t, bd);
             for (unsigned m = bm | touched; m; m &= m - 1) {
                 const int g = __ffs(m) - 1;
                 if ((pmask >> g) & 1u) dispatch_prefill(g, t);
@@ -566,6 +619,12 @@ struct JReplay {
                                        ? (get_tnext(flip_g) == PAD_INF && W.ql[o] == 0)
                                        : (W.a0[o] == 0 && W.ql[o] == 0);
                 if (empty) flip_t = t + pol.reassign_s;
+            }
+            if (DYN && tick_outcome < 2) {
+                double ne = fmin(fmin(ta, mte), fmin(settle_t, flip_t));
+#pragma unroll
+                for (int g = 0; g < kJG; g++) ne = fmin(ne, tnext[g]);
+                skip_ticks(tick_outcome, ne);
             }
         }
         ReplayResult res;
