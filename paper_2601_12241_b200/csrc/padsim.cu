@@ -82,7 +82,7 @@ struct padsim_ctx {
     bool fact = false;
     FPlan fplan{};
     int fA_grid = 0, fC_grid = 0;
-    size_t fC_smem = 0;
+    size_t fC_smem = 0, fA_smem = 0;
     long long* d_evA = nullptr;
     int n_evA = 0;
     unsigned* d_workC = nullptr;
@@ -370,15 +370,15 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
     F.n_groups = G;
     F.n_cc = NC;
     int *d_gx, *d_gcap, *d_ccc, *d_ccg, *d_ccy, *d_ccd;
-    double *d_te, *d_pe;
-    int* d_id;
+    double* d_pe;
+    SRec* d_rec;
     long long* d_evA;
     const long long GQS = (long long)G * Q * S;
     const size_t Rm = (size_t)F.Rmax;
 #define AL(p, n) do { int r_ = dalloc(ctx, &(p), (size_t)(n)); if (r_) return r_; } while (0)
     AL(d_gx, G); AL(d_gcap, (size_t)G * kNW); AL(d_ccc, NC); AL(d_ccg, NC); AL(d_ccy, NC);
     AL(d_ccd, (size_t)NC * kNW);
-    AL(d_te, GQS * Rm); AL(d_pe, GQS * Rm); AL(d_id, GQS * Rm); AL(d_evA, GQS);
+    AL(d_rec, GQS * Rm); AL(d_pe, GQS * Rm); AL(d_evA, GQS);
     CK(cudaMemcpy(d_gx, gx.data(), sizeof(int) * G, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(d_gcap, gcap.data(), sizeof(int) * G * kNW, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(d_ccc, cc_cand.data(), sizeof(int) * NC, cudaMemcpyHostToDevice));
@@ -386,7 +386,7 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
     CK(cudaMemcpy(d_ccy, cc_y.data(), sizeof(int) * NC, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(d_ccd, cc_dcap.data(), sizeof(int) * NC * kNW, cudaMemcpyHostToDevice));
     F.gx = d_gx; F.gcap = d_gcap; F.cc_cand = d_ccc; F.cc_group = d_ccg; F.cc_y = d_ccy; F.cc_dcap = d_ccd;
-    F.st_te = d_te; F.st_pe = d_pe; F.st_id = d_id; F.evA = d_evA;
+    F.st_rec = d_rec; F.st_pe = d_pe; F.evA = d_evA;
     ctx->d_evA = d_evA;
     ctx->n_evA = (int)GQS;
     // stage A scratch: one lane-interleaved slot per thread
@@ -396,14 +396,20 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
         take(Rm * 32 * sizeof(int));
         F.a_off_tte = take((size_t)PADSIM_MAX_SLOTS * 32 * sizeof(double));
         F.a_off_tid = take((size_t)PADSIM_MAX_SLOTS * 32 * sizeof(int));
+        F.a_off_tpe = take((size_t)PADSIM_MAX_SLOTS * 32 * sizeof(double));
         F.a_warp_bytes = off;
-        const long long warps = (GQS + 31) / 32;
+        F.a_blocks_per_trace = (int)(((long long)Q * G + kThreads - 1) / kThreads);
+        const long long ctas = (long long)F.a_blocks_per_trace * S;
         char* scr;
-        AL(scr, (size_t)warps * off);
+        AL(scr, (size_t)ctas * kWarps * off);
         F.scrA = scr;
-        ctx->fA_grid = (int)((GQS + kThreads - 1) / kThreads);
+        ctx->fA_grid = (int)ctas;
+        const size_t Rp = (Rm + 15) & ~(size_t)15;
+        const size_t tb = Rp * (8 + 8 + 4 + 4 + 1);
+        F.a_smem_trace = kAWorkBytes + tb <= 200 * 1024 ? 1 : 0;
+        ctx->fA_smem = kAWorkBytes + (F.a_smem_trace ? tb : 0);
         CK(cudaFuncSetAttribute((const void*)stageA_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)kAWorkBytes));
+                                (int)ctx->fA_smem));
     }
     // stage C: CTAs bound to one trace each (staged in smem by TMA bulk copies),
     // warps pull 32-replay items from that trace's counter
@@ -416,7 +422,7 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
         int wheel = 32;
         while (wheel < maxo) wheel <<= 1;        // finish steps lie in (step, step + out − 1]
         F.wheel = wheel;
-        F.c_off_heads = take((size_t)kNW * wheel * 32 * sizeof(int));
+        F.c_off_heads = take((size_t)32 * kNW * wheel * sizeof(unsigned));
         F.c_off_bits = take((size_t)kNW * (wheel / 32) * 32 * sizeof(unsigned));
         F.c_warp_bytes = off;
         unsigned* d_wc;
@@ -424,11 +430,11 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
         F.work = d_wc;
         ctx->d_workC = d_wc;
         const bool ctxm = model->decode_per_ctx_tok_s != 0.0;
-        const size_t Rp = (Rm + 15) & ~(size_t)15;
-        const size_t tbytes = Rp * (8 + 4 + (ctxm ? 4 : 0) + 1);
         const size_t wbytes = kCWorkBytes + (ctxm ? kCWorkCtxBytes : 0);
-        F.smem_trace = wbytes + tbytes <= 75 * 1024 ? 1 : 0;
-        ctx->fC_smem = wbytes + (F.smem_trace ? tbytes : 0);
+        const size_t bbytes = (size_t)kNW * (wheel / 32) * kThreads * sizeof(unsigned);
+        F.bits_in_smem = wheel <= 256 ? 1 : 0;
+        F.smem_trace = 0;
+        ctx->fC_smem = wbytes + (F.bits_in_smem ? bbytes : 0);
         const void* fn = ctxm ? (const void*)stageC_kernel<true> : (const void*)stageC_kernel<false>;
         CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->fC_smem));
         int occ = 0;
@@ -849,7 +855,7 @@ int padsim_run(padsim_ctx* ctx, void* stream) {
     if (ctx->fact) {
         const FPlan& F = ctx->fplan;
         CK(cudaMemsetAsync(ctx->d_workC, 0, (size_t)ctx->S * sizeof(unsigned), st));
-        stageA_kernel<<<ctx->fA_grid, kThreads, kAWorkBytes, st>>>(F);
+        stageA_kernel<<<ctx->fA_grid, kThreads, ctx->fA_smem, st>>>(F);
         CK(cudaGetLastError());
         CK(cudaEventRecord(ctx->evA, st));
         if (ctx->model.decode_per_ctx_tok_s == 0.0)

@@ -33,6 +33,15 @@ namespace padsim {
 
 constexpr int kNW = 7;   // ≤ 7 workers per role when N ≤ 8 (each role has ≥ 1 GPU)
 
+// One transfer-end record of the stage A → stage C stream (32 B).
+struct __align__(16) SRec {
+    double te;      // transfer end (event time in stage C)
+    double pe;      // prefill end (first token)
+    double ttft;    // pe − a_i, computed once in stage A
+    int id;         // request id
+    int meta;       // out_tok | phase << 31
+};
+
 struct FPlan {
     DevModel m;
     int N, Q, S, Rmax;
@@ -49,13 +58,14 @@ struct FPlan {
     int n_groups;
     const int* gx;          // [G] prefill workers
     const int* gcap;        // [G][kNW] their caps, P-id order
-    // stage A → C stream, per (g, q, s) block of Rmax entries
-    double* st_te;          // transfer-end times in (te, id) order
-    int* st_id;             //   and the request ids
-    double* st_pe;          // prefill end, indexed by request id
+    // stage A → C stream, per (g, q, s) block of Rmax records in (te, id) order
+    struct SRec* st_rec;
+    double* st_pe;          // prefill end, indexed by request id (stage A scratch)
     long long* evA;         // [G*Q*S] stage-A instants
     char* scrA;
-    size_t a_warp_bytes, a_off_tte, a_off_tid;
+    size_t a_warp_bytes, a_off_tte, a_off_tid, a_off_tpe;
+    int a_blocks_per_trace;   // stage A grid = S × this; a CTA never straddles traces
+    int a_smem_trace;         // stage A stages its trace in shared memory (TMA bulk)
     // stage C
     int n_cc;
     const int* cc_cand;     // [n_cc] candidate index
@@ -66,7 +76,8 @@ struct FPlan {
     unsigned* work;
     char* scrC;
     size_t c_warp_bytes, c_off_heads, c_off_bits;
-    int wheel;              // decode timing wheel size (power of 2 > max out_tok − 1, ≥ 32)
+    int wheel;              // decode timing wheel size (power of 2 ≥ max out_tok, ≥ 32)
+    int bits_in_smem;       // wheel occupancy bitmap in shared memory (wheel ≤ 256)
     int smem_trace;
     // outputs (r = (c*Q + q)*S + s)
     int* rep_met;
@@ -90,10 +101,47 @@ constexpr size_t kAWorkBytes = (size_t)kNW * kThreads * (sizeof(double) + 5 * si
 
 __global__ void __launch_bounds__(kThreads) stageA_kernel(const __grid_constant__ FPlan P) {
     extern __shared__ __align__(128) unsigned char smem[];
-    const long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const long long U = (long long)P.S * P.Q * P.n_groups;
-    if (u >= U) return;
+    __shared__ unsigned long long bar;
     const int tid = threadIdx.x;
+    const int s = blockIdx.x / P.a_blocks_per_trace;
+    const int local = (blockIdx.x - s * P.a_blocks_per_trace) * kThreads + tid;
+    const long long off = P.toff[s];
+    const int R = P.nreq[s];
+    // the CTA's trace: staged once in shared memory by TMA bulk copies, read by
+    // every prefill group × QPS replay of the CTA
+    const double* su;
+    const double* kv;
+    const int* it;
+    const int* ot;
+    const unsigned char* ph;
+    if (P.a_smem_trace) {
+        const int Rp = (R + 15) & ~15;
+        double* d_su = (double*)(smem + kAWorkBytes);
+        double* d_kv = d_su + Rp;
+        int* d_in = (int*)(d_kv + Rp);
+        int* d_ot = d_in + Rp;
+        unsigned char* d_ph = (unsigned char*)(d_ot + Rp);
+        if (tid == 0) mbar_init(&bar, 1);
+        __syncthreads();
+        if (tid == 0 && Rp > 0) {
+            const unsigned b8 = (unsigned)Rp * 8u, b4 = (unsigned)Rp * 4u, b1 = (unsigned)Rp;
+            mbar_expect_tx(&bar, 2 * b8 + 2 * b4 + b1);
+            bulk_g2s(d_su, P.s_unit + off, b8, &bar);
+            bulk_g2s(d_kv, P.kv + off, b8, &bar);
+            bulk_g2s(d_in, P.in_tok + off, b4, &bar);
+            bulk_g2s(d_ot, P.out_tok + off, b4, &bar);
+            bulk_g2s(d_ph, P.phase + off, b1, &bar);
+        }
+        if (Rp > 0) mbar_wait(&bar, 0);
+        su = d_su; kv = d_kv; it = d_in; ot = d_ot; ph = d_ph;
+    } else {
+        su = P.s_unit + off; kv = P.kv + off; it = P.in_tok + off;
+        ot = P.out_tok + off; ph = P.phase + off;
+    }
+    if (local >= P.Q * P.n_groups) return;
+    const int q = local / P.n_groups;
+    const int g = local - q * P.n_groups;
+    const long long u = (long long)blockIdx.x * kThreads + tid;    // scratch slot
     const int n_sm = kNW * kThreads;
     double* Wsp = (double*)smem + tid;
     int* ib = (int*)(smem + (size_t)n_sm * sizeof(double));
@@ -102,22 +150,14 @@ __global__ void __launch_bounds__(kThreads) stageA_kernel(const __grid_constant_
     int* Wql = ib + 2 * n_sm + tid;
     int* Wbh = ib + 3 * n_sm + tid;
     int* Wbn = ib + 4 * n_sm + tid;
-    const int g = (int)(u % P.n_groups);
-    const long long sq = u / P.n_groups;
-    const int q = (int)(sq % P.Q), s = (int)(sq / P.Q);
     const int lane = threadIdx.x & 31;
     char* wb = P.scrA + (size_t)(u >> 5) * P.a_warp_bytes;
     int* link = (int*)wb + lane;
     double* tte = (double*)(wb + P.a_off_tte) + lane;
     int* tidb = (int*)(wb + P.a_off_tid) + lane;
-    const long long off = P.toff[s];
-    const int R = P.nreq[s];
-    const double* su = P.s_unit + off;
-    const double* kv = P.kv + off;
-    const int* it = P.in_tok + off;
+    double* tpe = (double*)(wb + P.a_off_tpe) + lane;
     const long long sb = ((long long)(g * P.Q + q) * P.S + s) * P.Rmax;
-    double* ote = P.st_te + sb;
-    int* oid = P.st_id + sb;
+    SRec* orec = P.st_rec + sb;
     double* ope = P.st_pe + sb;
     const double inv_lam = 1.0 / (P.qps[q] * (double)P.N);
     const int x = P.gx[g];
@@ -159,15 +199,16 @@ __global__ void __launch_bounds__(kThreads) stageA_kernel(const __grid_constant_
             long long dec = 0;
             for (int z = 0; z < n; z++) {
                 const int nx = link[(size_t)i * 32];
-                ope[i] = t;
                 dec += it[i];
                 if (tbusy < slots) {
                     const double te = t + kv[i];
                     tte[tbusy * 32] = te;
                     tidb[tbusy * 32] = i;
+                    tpe[tbusy * 32] = t;
                     if (tbusy == 0 || te < mte || (te == mte && i < mid)) { mte = te; mid = i; mk = tbusy; }
                     tbusy++;
                 } else {
+                    ope[i] = t;                       // waits for a KV slot
                     link[(size_t)i * 32] = kNoIdx;
                     if (twl == 0) twh = i; else link[(size_t)twt * 32] = i;
                     twt = i;
@@ -181,17 +222,29 @@ __global__ void __launch_bounds__(kThreads) stageA_kernel(const __grid_constant_
         }
         // kind 4: transfer ends, earliest (te, id) first → the stream
         while (tbusy > 0 && mte == t) {
-            ote[k] = t;
-            oid[k] = mid;
+            {
+                SRec rc;
+                rc.te = t;
+                rc.pe = tpe[mk * 32];
+                rc.ttft = rc.pe - su[mid] * inv_lam;
+                rc.id = mid;
+                rc.meta = ot[mid] | ((int)ph[mid] << 31);
+                orec[k] = rc;
+            }
             k++;
             tbusy--;
-            if (mk != tbusy) { tte[mk * 32] = tte[tbusy * 32]; tidb[mk * 32] = tidb[tbusy * 32]; }
+            if (mk != tbusy) {
+                tte[mk * 32] = tte[tbusy * 32];
+                tidb[mk * 32] = tidb[tbusy * 32];
+                tpe[mk * 32] = tpe[tbusy * 32];
+            }
             if (twl > 0) {
                 const int j = twh;
                 twh = link[(size_t)j * 32];
                 twl--;
                 tte[tbusy * 32] = t + kv[j];
                 tidb[tbusy * 32] = j;
+                tpe[tbusy * 32] = ope[j];
                 tbusy++;
             }
             mte = PAD_INF;
@@ -264,37 +317,40 @@ __device__ __forceinline__ int first_boundary_ge(double tseg, double L, int st0,
 // ---------------------------------------------------------------------------
 // stage C: decode workers consume the transfer-end stream (A13, A14)
 //
-// Layout: the CTA owns one trace (s = blockIdx.x mod S), staged once in shared
-// memory by TMA bulk copies; its warps pull 32-replay work items from that
-// trace's counter (no CTA barrier per item).  Per decode worker, the next
-// event time and the routing load (active + pending) are register arrays;
-// the rest of its state is a [field][worker][thread] shared-memory SoA, so
-// every handler body is one shared code path indexed by a run-time worker id
-// (lanes at different workers stay convergent) and bank-conflict free.
+// The CTA owns one trace (s = blockIdx.x mod S); its warps pull 32-replay work
+// items from that trace's counter (no CTA barrier per item).  Per decode
+// worker, the next event time, routing load (active + pending) and cap index
+// are register arrays; the rest is a [field][worker][thread] shared-memory SoA
+// so handler bodies are shared across workers (run-time index, convergent
+// lanes, conflict-free).  Requests are named by their stream index k; the
+// stream record carries everything a completion needs (pe, ttft, out, phase).
+// Decode batches are a timing wheel: bucket (finish step mod W) holds the
+// head k (bit 31 = "more members chained through link[]"), an occupancy
+// bitmap (shared memory when W ≤ 256) yields the next finish step.
 // ---------------------------------------------------------------------------
 struct CWork {            // per-thread shared-memory SoA views (stride kThreads)
     double* tseg;
     double* Ls;
-    int* nact; int* qh; int* qt; int* ql; int* stm; int* nxs; int* st0; int* mfin; int* ci;
+    int* nact; int* qh; int* qt; int* ql; int* stm; int* nxs; int* st0; int* mfin;
     long long* ctx;
 };
 
-constexpr size_t kCWorkBytes = (size_t)kNW * kThreads * (2 * sizeof(double) + 9 * sizeof(int));
+constexpr size_t kCWorkBytes = (size_t)kNW * kThreads * (2 * sizeof(double) + 8 * sizeof(int));
 constexpr size_t kCWorkCtxBytes = (size_t)kNW * kThreads * sizeof(long long);
+constexpr unsigned kMulti = 0x80000000u;
 
 template <bool CTX>
 __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant__ FPlan P) {
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ unsigned long long bar;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     char* wb = P.scrC + ((size_t)blockIdx.x * kWarps + warp) * P.c_warp_bytes;
-    int* link = (int*)wb + lane;
-    int* heads = (int*)(wb + P.c_off_heads) + lane;       // [(w*Wh + b)*32]
-    unsigned* bits = (unsigned*)(wb + P.c_off_bits) + lane;  // [(w*Wh/32 + k)*32]
-    const int max_db = P.m.max_db;
+    int* link = (int*)wb + lane;                                       // [k*32]
     const int Wh = P.wheel, Wm = P.wheel - 1, nwords = P.wheel >> 5;
-    // shared memory: worker SoA, then the trace
+    unsigned* heads = (unsigned*)(wb + P.c_off_heads) + (size_t)lane * kNW * Wh;   // per lane
+    const int max_db = P.m.max_db;
     CWork W;
+    unsigned* bits;
+    int bstride;
     {
         unsigned char* p = smem;
         const int n = kNW * kThreads;
@@ -303,39 +359,22 @@ __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant_
         int* ib = (int*)p;
         W.nact = ib + 0 * n + tid; W.qh = ib + 1 * n + tid; W.qt = ib + 2 * n + tid;
         W.ql = ib + 3 * n + tid; W.stm = ib + 4 * n + tid; W.nxs = ib + 5 * n + tid;
-        W.st0 = ib + 6 * n + tid; W.mfin = ib + 7 * n + tid; W.ci = ib + 8 * n + tid;
-        p += 9 * n * sizeof(int);
+        W.st0 = ib + 6 * n + tid; W.mfin = ib + 7 * n + tid;
+        p += 8 * n * sizeof(int);
         W.ctx = CTX ? (long long*)p + tid : nullptr;
+        if (CTX) p += n * sizeof(long long);
+        if (P.bits_in_smem) {
+            bits = (unsigned*)p + tid;
+            bstride = kThreads;
+        } else {
+            bits = (unsigned*)(wb + P.c_off_bits) + lane;
+            bstride = 32;
+        }
     }
-    unsigned char* tsm = smem + kCWorkBytes + (CTX ? kCWorkCtxBytes : 0);
     const int s = blockIdx.x % P.S;
     const long long off = P.toff[s];
     const int R = P.nreq[s];
-    const double* su;
-    const int* ot;
-    const int* itk;
-    const unsigned char* ph;
-    if (P.smem_trace) {
-        const int Rp = (R + 15) & ~15;
-        double* d_su = (double*)tsm;
-        int* d_ot = (int*)(d_su + Rp);
-        int* d_in = d_ot + Rp;
-        unsigned char* d_ph = (unsigned char*)(d_in + (CTX ? Rp : 0));
-        if (tid == 0) mbar_init(&bar, 1);
-        __syncthreads();
-        if (tid == 0 && Rp > 0) {
-            const unsigned b8 = (unsigned)Rp * 8u, b4 = (unsigned)Rp * 4u, b1 = (unsigned)Rp;
-            mbar_expect_tx(&bar, b8 + b4 + (CTX ? b4 : 0u) + b1);
-            bulk_g2s(d_su, P.s_unit + off, b8, &bar);
-            bulk_g2s(d_ot, P.out_tok + off, b4, &bar);
-            if (CTX) bulk_g2s(d_in, P.in_tok + off, b4, &bar);
-            bulk_g2s(d_ph, P.phase + off, b1, &bar);
-        }
-        if (Rp > 0) mbar_wait(&bar, 0);
-        su = d_su; ot = d_ot; itk = d_in; ph = d_ph;
-    } else {
-        su = P.s_unit + off; ot = P.out_tok + off; itk = P.in_tok + off; ph = P.phase + off;
-    }
+    const int* itk = P.in_tok + off;
     const int QC = P.Q * P.n_cc;
     for (;;) {
         int item = 0;
@@ -351,46 +390,42 @@ __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant_
         const int y = P.cc_y[cc];
         const long long r = ((long long)c * P.Q + q) * P.S + s;
         const long long sb = ((long long)(g * P.Q + q) * P.S + s) * P.Rmax;
-        const double* ste = P.st_te + sb;
-        const int* sid = P.st_id + sb;
-        const double* spe = P.st_pe + sb;
+        const SRec* recs = P.st_rec + sb;
         const long long rb = P.rec_ttft ? r * P.Rmax : -1;
-        const double inv_lam = 1.0 / (P.qps[q] * (double)P.N);
         double tnext[kNW];
         int ld[kNW];                       // routing load: active + pending (A13)
+        int ci[kNW];                       // decode cap index into the L table
 #pragma unroll
         for (int w = 0; w < kNW; w++) {
             const int o = w * kThreads;
             tnext[w] = PAD_INF;
             ld[w] = w < y ? 0 : 0x7fffffff;
+            ci[w] = (w < y ? P.cc_dcap[cc * kNW + w] : P.m.min_w) - P.m.min_w;
             W.tseg[o] = 0.0; W.Ls[o] = 1.0;
             W.nact[o] = 0; W.qh[o] = kNoIdx; W.qt[o] = kNoIdx; W.ql[o] = 0;
             W.stm[o] = 0; W.nxs[o] = 0; W.st0[o] = 0; W.mfin[o] = 0x7fffffff;
-            W.ci[o] = (w < y ? P.cc_dcap[cc * kNW + w] : P.m.min_w) - P.m.min_w;
             if (CTX) W.ctx[o] = 0;
         }
-        for (int z = 0; z < y * nwords; z++) bits[(size_t)z * 32] = 0u;
+        for (int z = 0; z < y * nwords; z++) bits[(size_t)z * bstride] = 0u;
         int completed = 0, met = 0, near = 0, k = 0;
         double maxcomp = -PAD_INF;
-        double tk = R > 0 ? ste[0] : PAD_INF;
+        double tk = R > 0 ? recs[0].te : PAD_INF;
         long long inst = 0;
         auto set_tnext = [&](int wd, double v) {
 #pragma unroll
             for (int w = 0; w < kNW; w++) if (w == wd) tnext[w] = v;
         };
-        auto complete = [&](int id, double t, double tpot) {
+        auto complete = [&](const SRec& rc, double t, double tpot) {
             completed++;
-            const double pe = spe[id];
-            const double ttft = pe - su[id] * inv_lam;
-            const double ts = ph[id] ? P.tpot_slo1 : P.tpot_slo0;
-            met += (ttft <= P.ttft_slo && tpot <= ts) ? 1 : 0;
-            near += (fabs(ttft - P.ttft_slo) <= 1e-9 * P.ttft_slo || fabs(tpot - ts) <= 1e-9 * ts) ? 1 : 0;
+            const double ts = (rc.meta < 0) ? P.tpot_slo1 : P.tpot_slo0;
+            met += (rc.ttft <= P.ttft_slo && tpot <= ts) ? 1 : 0;
+            near += (fabs(rc.ttft - P.ttft_slo) <= 1e-9 * P.ttft_slo || fabs(tpot - ts) <= 1e-9 * ts) ? 1 : 0;
             maxcomp = fmax(maxcomp, t);
             if (rb >= 0) {
-                P.rec_ttft[rb + id] = ttft;
-                P.rec_tpot[rb + id] = tpot;
-                P.rec_pe[rb + id] = pe;
-                P.rec_comp[rb + id] = t;
+                P.rec_ttft[rb + rc.id] = rc.ttft;
+                P.rec_tpot[rb + rc.id] = tpot;
+                P.rec_pe[rb + rc.id] = rc.pe;
+                P.rec_comp[rb + rc.id] = t;
             }
         };
         while (completed < R) {
@@ -409,33 +444,33 @@ __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant_
                 W.stm[o] = sN;
                 set_tnext(w, PAD_INF);
                 if (sN == W.mfin[o]) {
-                    // timing wheel: every member finishing at step sN is in bucket sN mod Wh
                     const int b = sN & Wm;
-                    int* hp = heads + ((size_t)w * Wh + b) * 32;
-                    int id = *hp;
+                    unsigned cur = heads[(size_t)w * Wh + b];
                     int left = 0;
-                    while (id != kNoIdx) {
-                        const int nx = link[(size_t)id * 32];
-                        complete(id, t, (t - spe[id]) / (double)(ot[id] - 1));
-                        if (CTX) W.ctx[o] -= itk[id];
+                    for (;;) {
+                        const int kk = (int)(cur & ~kMulti);
+                        const SRec rc = recs[kk];
+                        const int o1 = (rc.meta & 0x7fffffff) - 1;
+                        complete(rc, t, (t - rc.pe) / (double)o1);
+                        if (CTX) W.ctx[o] -= itk[rc.id];
                         left++;
-                        id = nx;
+                        if (!(cur & kMulti)) break;
+                        cur = (unsigned)link[(size_t)kk * 32];
                     }
-                    unsigned* bw = bits + (size_t)w * nwords * 32;
-                    bw[(size_t)(b >> 5) * 32] &= ~(1u << (b & 31));
+                    unsigned* bw = bits + (size_t)w * nwords * bstride;
+                    bw[(size_t)(b >> 5) * bstride] &= ~(1u << (b & 31));
                     const int n = W.nact[o] - left;
                     W.nact[o] = n;
                     int mf = 0x7fffffff;
-                    if (n > 0) {   // next occupied bucket after b (all finish steps lie in (sN, sN+Wh))
+                    if (n > 0) {   // next occupied bucket (finish steps lie in (sN, sN+Wh))
                         const int st = (b + 1) & Wm;
                         int wi = st >> 5;
-                        unsigned mword = bw[(size_t)wi * 32] & (0xffffffffu << (st & 31));
+                        unsigned mword = bw[(size_t)wi * bstride] & (0xffffffffu << (st & 31));
                         while (mword == 0u) {
                             wi = (wi + 1) & (nwords - 1);
-                            mword = bw[(size_t)wi * 32];
+                            mword = bw[(size_t)wi * bstride];
                         }
-                        const int b2 = (wi << 5) + __ffs(mword) - 1;
-                        mf = sN + ((b2 - b) & Wm);
+                        mf = sN + ((((wi << 5) + __ffs(mword) - 1) - b) & Wm);
                     }
                     W.mfin[o] = mf;
 #pragma unroll
@@ -445,21 +480,21 @@ __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant_
             }
             // kind 4: transfer ends from the stream, (te, id) order
             while (tk == t) {
-                const int id = sid[k];
+                const int kk = k;
+                const SRec rc = recs[kk];
                 k++;
-                tk = k < R ? ste[k] : PAD_INF;
-                if (rb >= 0) P.rec_te[rb + id] = t;
-                if (ot[id] == 1) { complete(id, t, 0.0); continue; }   // S:280 D4
+                tk = k < R ? recs[k].te : PAD_INF;
+                if (rb >= 0) P.rec_te[rb + rc.id] = t;
+                if ((rc.meta & 0x7fffffff) == 1) { complete(rc, t, 0.0); continue; }   // S:280 D4
                 int best = 0, bl = ld[0];
 #pragma unroll
                 for (int w = 1; w < kNW; w++) if (ld[w] < bl) { bl = ld[w]; best = w; }
 #pragma unroll
                 for (int w = 0; w < kNW; w++) if (w == best) ld[w]++;
                 const int o = best * kThreads;
-                link[(size_t)id * 32] = kNoIdx;
                 const int qn = W.ql[o];
-                if (qn == 0) W.qh[o] = id; else link[(size_t)W.qt[o] * 32] = id;
-                W.qt[o] = id;
+                if (qn == 0) W.qh[o] = kk; else link[(size_t)W.qt[o] * 32] = kk;
+                W.qt[o] = kk;
                 W.ql[o] = qn + 1;
                 touched |= 1u << best;
                 const int na = W.nact[o];
@@ -494,23 +529,27 @@ __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant_
                 const int step = W.stm[o];
                 int mf = W.mfin[o];
                 int h = W.qh[o];
-                int* hw = heads + (size_t)w * Wh * 32;
-                unsigned* bw = bits + (size_t)w * nwords * 32;
+                unsigned* hw = heads + (size_t)w * Wh;
+                unsigned* bw = bits + (size_t)w * nwords * bstride;
                 while (n < max_db && qn > 0) {
-                    const int i = h;
+                    const int kk = h;
                     qn--;
-                    if (qn > 0) h = link[(size_t)i * 32];
-                    const int fin = step + (ot[i] - 1);
+                    if (qn > 0) h = link[(size_t)kk * 32];
+                    const int out = recs[kk].meta & 0x7fffffff;
+                    const int fin = step + (out - 1);
                     const int b = fin & Wm;
-                    int* hp = hw + (size_t)b * 32;
-                    unsigned* wp = bw + (size_t)(b >> 5) * 32;
+                    unsigned* wp = bw + (size_t)(b >> 5) * bstride;
                     const unsigned bit = 1u << (b & 31);
                     const unsigned old = *wp;
-                    link[(size_t)i * 32] = (old & bit) ? *hp : kNoIdx;
-                    *hp = i;
-                    *wp = old | bit;
+                    if (old & bit) {                     // bucket occupied: chain
+                        link[(size_t)kk * 32] = (int)hw[b];
+                        hw[b] = (unsigned)kk | kMulti;
+                    } else {
+                        hw[b] = (unsigned)kk;
+                        *wp = old | bit;
+                    }
                     n++;
-                    if (CTX) W.ctx[o] += itk[i];
+                    if (CTX) W.ctx[o] += itk[recs[kk].id];
                     mf = fin < mf ? fin : mf;
                     joined = true;
                 }
@@ -523,7 +562,9 @@ __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant_
                     if (was_idle || joined || ((touched >> (w + 16)) & 1u)) {
                         ts0 = t;
                         s0 = step;
-                        const int cix = W.ci[o];
+                        int cix = 0;
+#pragma unroll
+                        for (int v = 0; v < kNW; v++) if (v == w) cix = ci[v];
                         if (CTX) {
                             double xv = P.m.dec_fixed + P.m.dec_per_seq * (double)n;
                             xv = xv + P.m.dec_per_ctx * (double)W.ctx[o];
@@ -544,7 +585,7 @@ __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant_
         }
         P.rep_met[r] = met;
         P.rep_near[r] = near;
-        const double dur = R > 0 ? maxcomp - su[0] * inv_lam : 0.0;
+        const double dur = R > 0 ? maxcomp - P.s_unit[off] * (1.0 / (P.qps[q] * (double)P.N)) : 0.0;
         P.rep_dur[r] = dur;
         P.rep_good[r] = dur > 0 ? (double)met / dur : 0.0;
         P.rep_events[r] = inst;
