@@ -188,6 +188,10 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend (gloo only to exercise the multi-rank path on one GPU)")
+    ap.add_argument("--same-device", action="store_true",
+                    help="all ranks on cuda:0 (multi-rank logic check on a 1-GPU box; not a scaling run)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -207,11 +211,16 @@ def main():
     from paper_2601_12241_b200.distributed import allreduce_met, max_over_ranks
     if rank == 0:
         build()
+    local_dev = 0 if args.same_device else local
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        torch.cuda.set_device(local_dev)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_dev))
+        else:
+            dist.init_process_group("gloo")
         dist.barrier()
         build()     # no-op if rank 0 built it
+    local = local_dev
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     stream = torch.cuda.current_stream(dev)

@@ -91,23 +91,24 @@ struct JReplay {
     __device__ __forceinline__ int& LNK(int i) { return X.link[(size_t)i * 32]; }
     __device__ __forceinline__ double& PE(int i) { return X.pe[(size_t)i * 32]; }
     __device__ __forceinline__ double arr(int i) const { return T.s_unit[i] * inv_lam; }
+    // register arrays, run-time index: predicated selects only
     __device__ __forceinline__ void set_tnext(int gd, double v) {
 #pragma unroll
-        for (int g = 0; g < kJG; g++) if (g == gd) tnext[g] = v;
+        for (int g = 0; g < kJG; g++) tnext[g] = (g == gd) ? v : tnext[g];
     }
     __device__ __forceinline__ double get_tnext(int gd) const {
-        double v = PAD_INF;
+        double v = tnext[0];
 #pragma unroll
-        for (int g = 0; g < kJG; g++) if (g == gd) v = tnext[g];
+        for (int g = 1; g < kJG; g++) v = (g == gd) ? tnext[g] : v;
         return v;
     }
     __device__ __forceinline__ void add_kp(int gd, int d) {
 #pragma unroll
-        for (int g = 0; g < kJG; g++) if (g == gd) kp[g] += d;
+        for (int g = 0; g < kJG; g++) kp[g] += (g == gd) ? d : 0;
     }
     __device__ __forceinline__ void add_kd(int gd, int d) {
 #pragma unroll
-        for (int g = 0; g < kJG; g++) if (g == gd) kd[g] += d;
+        for (int g = 0; g < kJG; g++) kd[g] += (g == gd) ? d : 0;
     }
     __device__ __forceinline__ double bnd(int o, int s) const {
         return W.tseg[o] + (double)(s - W.st0[o]) * W.L[o];
@@ -579,10 +580,14 @@ struct JReplay {
         int na = 0;
         double ta = R > 0 ? arr(0) : PAD_INF;
         while (completed < R) {
-            double t = fmin(ta, mte);
+            double t = ta < mte ? ta : mte;
 #pragma unroll
-            for (int g = 0; g < kJG; g++) t = fmin(t, tnext[g]);
-            if (DYN) t = fmin(t, fmin(tick_t, fmin(settle_t, flip_t)));
+            for (int g = 0; g < kJG; g++) t = tnext[g] < t ? tnext[g] : t;
+            if (DYN) {
+                t = tick_t < t ? tick_t : t;
+                t = settle_t < t ? settle_t : t;
+                t = flip_t < t ? flip_t : t;
+            }
             events++;
             touched = 0;
             if (DYN) {

@@ -33,6 +33,26 @@ namespace padsim {
 
 constexpr int kNW = 7;   // ≤ 7 workers per role when N ≤ 8 (each role has ≥ 1 GPU)
 
+// Register-array helpers: a run-time index selects with predicated moves only
+// (no branches, no local memory).
+template <int N, class T>
+__device__ __forceinline__ void rset(T (&a)[N], int i, T v) {
+#pragma unroll
+    for (int w = 0; w < N; w++) a[w] = (w == i) ? v : a[w];
+}
+template <int N, class T>
+__device__ __forceinline__ T rget(const T (&a)[N], int i) {
+    T v = a[0];
+#pragma unroll
+    for (int w = 1; w < N; w++) v = (w == i) ? a[w] : v;
+    return v;
+}
+template <int N, class T>
+__device__ __forceinline__ void radd(T (&a)[N], int i, T d) {
+#pragma unroll
+    for (int w = 0; w < N; w++) a[w] += (w == i) ? d : (T)0;
+}
+
 // One transfer-end record of the stage A → stage C stream (32 B).
 struct __align__(16) SRec {
     double te;      // transfer end (event time in stage C)
@@ -173,19 +193,16 @@ __global__ void __launch_bounds__(kThreads) stageA_kernel(const __grid_constant_
         Wqh[o] = kNoIdx; Wqt[o] = kNoIdx; Wql[o] = 0; Wbh[o] = 0; Wbn[o] = 0;
         Wsp[o] = w < x ? P.m.spre[P.gcap[g * kNW + w] - P.m.min_w] : 1.0;
     }
-    auto set_tnext = [&](int wd, double v) {
-#pragma unroll
-        for (int w = 0; w < kNW; w++) if (w == wd) tnext[w] = v;
-    };
+    auto set_tnext = [&](int wd, double v) { rset<kNW>(tnext, wd, v); };
     int tbusy = 0, mk = 0, mid = 0, twh = kNoIdx, twt = kNoIdx, twl = 0;
     double mte = PAD_INF;
     int na = 0, k = 0;
     double ta = R > 0 ? su[0] * inv_lam : PAD_INF;
     long long inst = 0;
     while (k < R) {
-        double t = fmin(ta, mte);
+        double t = ta < mte ? ta : mte;
 #pragma unroll
-        for (int w = 0; w < kNW; w++) t = fmin(t, tnext[w]);
+        for (int w = 0; w < kNW; w++) t = tnext[w] < t ? tnext[w] : t;
         inst++;
         unsigned bm = 0, touched = 0;
 #pragma unroll
@@ -216,8 +233,7 @@ __global__ void __launch_bounds__(kThreads) stageA_kernel(const __grid_constant_
                 }
                 i = nx;
             }
-#pragma unroll
-            for (int v = 0; v < kNW; v++) if (v == w) a0[v] -= dec;
+            radd<kNW, long long>(a0, w, -dec);
             set_tnext(w, PAD_INF);
         }
         // kind 4: transfer ends, earliest (te, id) first → the stream
@@ -263,8 +279,7 @@ __global__ void __launch_bounds__(kThreads) stageA_kernel(const __grid_constant_
             for (int w = 1; w < kNW; w++)
                 if (a0[w] < bl) { bl = a0[w]; best = w; }
             const int tin = it[i];
-#pragma unroll
-            for (int w = 0; w < kNW; w++) if (w == best) a0[w] += tin;
+            radd<kNW, long long>(a0, best, (long long)tin);
             link[(size_t)i * 32] = kNoIdx;
             const int o = best * kThreads;
             const int qn = Wql[o];
@@ -279,9 +294,7 @@ __global__ void __launch_bounds__(kThreads) stageA_kernel(const __grid_constant_
         for (unsigned m = bm | touched; m; m &= m - 1) {
             const int w = __ffs(m) - 1;
             const int o = w * kThreads;
-            double tw = 0.0;
-#pragma unroll
-            for (int v = 0; v < kNW; v++) if (v == w) tw = tnext[v];
+            const double tw = rget<kNW>(tnext, w);
             const int qn = Wql[o];
             if (tw != PAD_INF || qn == 0) continue;
             const int h = Wqh[o];
@@ -394,13 +407,11 @@ __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant_
         const long long rb = P.rec_ttft ? r * P.Rmax : -1;
         double tnext[kNW];
         int ld[kNW];                       // routing load: active + pending (A13)
-        int ci[kNW];                       // decode cap index into the L table
 #pragma unroll
         for (int w = 0; w < kNW; w++) {
             const int o = w * kThreads;
             tnext[w] = PAD_INF;
             ld[w] = w < y ? 0 : 0x7fffffff;
-            ci[w] = (w < y ? P.cc_dcap[cc * kNW + w] : P.m.min_w) - P.m.min_w;
             W.tseg[o] = 0.0; W.Ls[o] = 1.0;
             W.nact[o] = 0; W.qh[o] = kNoIdx; W.qt[o] = kNoIdx; W.ql[o] = 0;
             W.stm[o] = 0; W.nxs[o] = 0; W.st0[o] = 0; W.mfin[o] = 0x7fffffff;
@@ -411,10 +422,7 @@ __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant_
         double maxcomp = -PAD_INF;
         double tk = R > 0 ? recs[0].te : PAD_INF;
         long long inst = 0;
-        auto set_tnext = [&](int wd, double v) {
-#pragma unroll
-            for (int w = 0; w < kNW; w++) if (w == wd) tnext[w] = v;
-        };
+        auto set_tnext = [&](int wd, double v) { rset<kNW>(tnext, wd, v); };
         auto complete = [&](const SRec& rc, double t, double tpot) {
             completed++;
             const double ts = (rc.meta < 0) ? P.tpot_slo1 : P.tpot_slo0;
@@ -431,7 +439,7 @@ __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant_
         while (completed < R) {
             double t = tk;
 #pragma unroll
-            for (int w = 0; w < kNW; w++) t = fmin(t, tnext[w]);
+            for (int w = 0; w < kNW; w++) t = tnext[w] < t ? tnext[w] : t;
             inst++;
             unsigned bnd = 0, touched = 0;
 #pragma unroll
@@ -441,8 +449,7 @@ __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant_
                 const int w = __ffs(m) - 1;
                 const int o = w * kThreads;
                 const int sN = W.nxs[o];
-                W.stm[o] = sN;
-                set_tnext(w, PAD_INF);
+                W.stm[o] = sN;               // tnext[w] is rewritten by this instant's dispatch
                 if (sN == W.mfin[o]) {
                     const int b = sN & Wm;
                     unsigned cur = heads[(size_t)w * Wh + b];
@@ -473,8 +480,7 @@ __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant_
                         mf = sN + ((((wi << 5) + __ffs(mword) - 1) - b) & Wm);
                     }
                     W.mfin[o] = mf;
-#pragma unroll
-                    for (int v = 0; v < kNW; v++) if (v == w) ld[v] -= left;
+                    radd<kNW, int>(ld, w, -left);
                     touched |= 1u << (w + 16);          // composition changed
                 }
             }
@@ -489,8 +495,7 @@ __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant_
                 int best = 0, bl = ld[0];
 #pragma unroll
                 for (int w = 1; w < kNW; w++) if (ld[w] < bl) { bl = ld[w]; best = w; }
-#pragma unroll
-                for (int w = 0; w < kNW; w++) if (w == best) ld[w]++;
+                radd<kNW, int>(ld, best, 1);
                 const int o = best * kThreads;
                 const int qn = W.ql[o];
                 if (qn == 0) W.qh[o] = kk; else link[(size_t)W.qt[o] * 32] = kk;
@@ -515,10 +520,7 @@ __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant_
                 bool ab = (bnd >> w) & 1u;
                 int n = W.nact[o];
                 if (n > 0 && !ab) {
-                    double tw = PAD_INF;
-#pragma unroll
-                    for (int v = 0; v < kNW; v++) if (v == w) tw = tnext[v];
-                    if (tw != t) continue;               // mid-step
+                    if (rget<kNW>(tnext, w) != t) continue;   // mid-step
                     W.stm[o] = W.nxs[o];                 // join boundary exactly at t
                     ab = true;
                 }
@@ -562,9 +564,7 @@ __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant_
                     if (was_idle || joined || ((touched >> (w + 16)) & 1u)) {
                         ts0 = t;
                         s0 = step;
-                        int cix = 0;
-#pragma unroll
-                        for (int v = 0; v < kNW; v++) if (v == w) cix = ci[v];
+                        const int cix = P.cc_dcap[cc * kNW + w] - P.m.min_w;
                         if (CTX) {
                             double xv = P.m.dec_fixed + P.m.dec_per_seq * (double)n;
                             xv = xv + P.m.dec_per_ctx * (double)W.ctx[o];
