@@ -161,6 +161,8 @@ int padsim_evaluate_allocations(padsim_ctx* ctx, const padsim_trace* traces, int
  * padsim_fetch: copy the last run's results to host (synchronises stream).
  */
 #define PADSIM_RECORDS 1u
+#define PADSIM_JOINT 2u     /* N <= 8: replay static candidates in the joint kernel instead
+                               of the factorized stage A / stage C path (cross-check, ablation) */
 int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
                 const double* qps_per_gpu, int32_t n_qps, const padsim_model* model,
                 const padsim_candidates* cands, const padsim_slo* slo,

@@ -17,6 +17,7 @@ LIB_PATH = os.path.join(HERE, "libpadsim.so")
 MAX_GPUS = 64
 MAX_ANCHORS = 8
 RECORDS = 1
+JOINT = 2
 
 STATUS = {0: "OK", -1: "EINVAL", -2: "ERANGE", -3: "EBUDGET", -4: "EROLE", -5: "EMODEL",
           -6: "EDOMAIN", -7: "ECUDA", -8: "ENOMEM"}
@@ -254,7 +255,8 @@ class Context:
             msg = self.L.padsim_last_error(self.ptr)
             raise PadsimError(rc, f"{what}: {msg.decode() if msg else ''}")
 
-    def plan(self, traces, qps, model, role, cap, policies, slo, budget_w, records=False):
+    def plan(self, traces, qps, model, role, cap, policies, slo, budget_w, records=False,
+             joint=False):
         keep = _Keep()
         tr = make_traces(traces, keep)
         q = keep.arr(qps, np.float64)
@@ -262,8 +264,8 @@ class Context:
         bad = C.c_int32(-1)
         rc = self.L.padsim_plan(self.ptr, tr, len(traces), _p(q, C.c_double), q.size,
                                 C.byref(make_model(model)), C.byref(cands), C.byref(make_slo(slo)),
-                                C.byref(Budget(int(budget_w))), RECORDS if records else 0,
-                                C.byref(bad))
+                                C.byref(Budget(int(budget_w))),
+                                (RECORDS if records else 0) | (JOINT if joint else 0), C.byref(bad))
         if rc != 0:
             e = PadsimError(rc, self.L.padsim_last_error(self.ptr).decode())
             e.bad_index = bad.value

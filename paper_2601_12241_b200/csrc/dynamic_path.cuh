@@ -26,7 +26,7 @@ namespace padsim {
 constexpr int kJG = 8;     // GPU slots (N ≤ 8)
 constexpr int kIntMax = 0x7fffffff;
 
-// smem SoA, stride kThreads
+// smem SoA, stride TB (threads per CTA)
 struct JWork {
     double* tseg; double* L;
     int* a0;    // P: outstanding tokens | D: active count
@@ -36,26 +36,28 @@ struct JWork {
     int* st0; int* mfin; int* eff; int* cmd; int* rse; int* ctx;
     unsigned char* fl;
 };
-constexpr size_t kJWorkBytes = (size_t)kJG * kThreads * (2 * sizeof(double) + 13 * sizeof(int) + 1);
+template <int TB>
+__host__ __device__ constexpr size_t j_work_bytes() { return (size_t)kJG * TB * (2 * sizeof(double) + 13 * sizeof(int) + 1); }
 
 enum : unsigned char { JF_DRAIN = 1, JF_DIRTY = 2 };
 
+template <int TB>
 struct JCtlView {
     const JWork* W;
     unsigned pmask;
     __device__ int role(int g) const { return ((pmask >> g) & 1u) ? 0 : 1; }
-    __device__ bool draining(int g) const { return (W->fl[g * kThreads] & JF_DRAIN) != 0; }
+    __device__ bool draining(int g) const { return (W->fl[g * TB] & JF_DRAIN) != 0; }
     __device__ int target(int g) const {
-        const int r = W->rse[g * kThreads];
-        return r > 0 ? r : W->cmd[g * kThreads];
+        const int r = W->rse[g * TB];
+        return r > 0 ? r : W->cmd[g * TB];
     }
     __device__ long long load(int g) const {
-        const int o = g * kThreads;
+        const int o = g * TB;
         return ((pmask >> g) & 1u) ? (long long)W->a0[o] : (long long)W->a0[o] + W->ql[o];
     }
 };
 
-template <bool DYN>
+template <bool DYN, int TB>
 struct JReplay {
     const Plan& P;
     const TraceView& T;
@@ -66,11 +68,13 @@ struct JReplay {
     double tnext[kJG];
     int kp[kJG], kd[kJG];
     unsigned pmask, dmask;
-    // KV buffer: slots in lane-interleaved scratch (X.tst/X.ordt reused? no: own arrays)
+    // KV buffer: slots in lane-interleaved scratch
     double* tte;
     int* tti;
     int* heads;          // [(g*wheel + b)*32]
     unsigned* bits;      // [(g*wheel/32 + k)*32]
+    double* wts;         // TTFT window stamps [k*32]
+    unsigned char* wtf;  // TTFT window flags (≤ SLO, < SLO) [k*32]
     int Wh, Wm, nwords;
     int tbusy, mk, mid, twh, twt, twl;
     double mte;
@@ -155,7 +159,7 @@ struct JReplay {
         for (int g = 1; g < kJG; g++) if (kp[g] < bl) { bl = kp[g]; best = g; }
         const int tin = T.in_tok[i];
         add_kp(best, tin);
-        const int o = best * kThreads;
+        const int o = best * TB;
         W.a0[o] += tin;
         LNK(i) = kNoIdx;
         const int qn = W.ql[o];
@@ -172,7 +176,7 @@ struct JReplay {
 #pragma unroll
         for (int g = 1; g < kJG; g++) if (kd[g] < bl) { bl = kd[g]; best = g; }
         add_kd(best, 1);
-        const int o = best * kThreads;
+        const int o = best * TB;
         LNK(i) = kNoIdx;
         const int qn = W.ql[o];
         if (qn == 0) W.qh[o] = i; else LNK(W.qt[o]) = i;
@@ -187,7 +191,7 @@ struct JReplay {
     }
 
     __device__ void batch_end(int g, double t) {
-        const int o = g * kThreads;
+        const int o = g * TB;
         int i = W.b0[o];
         const int n = W.b1[o];
         int dec = 0;
@@ -197,10 +201,12 @@ struct JReplay {
             dec += T.in_tok[i];
             if (DYN) {
                 const double ttft = t - arr(i);
-                X.ordt[(size_t)w_th * 32] = i;
+                const unsigned char f = (ttft <= P.ttft_slo ? 1 : 0) | (ttft < P.ttft_slo ? 2 : 0);
+                wts[(size_t)w_th * 32] = t;
+                wtf[(size_t)w_th * 32] = f;
                 w_th++;
-                w_tle += ttft <= P.ttft_slo ? 1 : 0;
-                w_tlt += ttft < P.ttft_slo ? 1 : 0;
+                w_tle += f & 1;
+                w_tlt += f >> 1;
             }
             if (tbusy < P.m.slots) {
                 const double te = t + T.kv[i];
@@ -226,7 +232,7 @@ struct JReplay {
     // a timing wheel: bucket (finish step mod Wh) chains its members through
     // link[]; an occupancy bitmap gives the next finish step.
     __device__ bool boundary(int g, double t) {
-        const int o = g * kThreads;
+        const int o = g * TB;
         const int s = W.b1[o];
         W.b0[o] = s;
         set_tnext(g, PAD_INF);
@@ -285,7 +291,7 @@ struct JReplay {
     }
 
     __device__ void dispatch_prefill(int g, double t) {
-        const int o = g * kThreads;
+        const int o = g * TB;
         const int qn = W.ql[o];
         if (get_tnext(g) != PAD_INF || qn == 0) return;
         const int h = W.qh[o];
@@ -307,7 +313,7 @@ struct JReplay {
     }
 
     __device__ void dispatch_decode(int g, double t, bool at_bnd, bool changed) {
-        const int o = g * kThreads;
+        const int o = g * TB;
         int n = W.a0[o];
         if (n > 0 && !at_bnd) {
             if (get_tnext(g) != t) return;      // mid-step
@@ -370,7 +376,7 @@ struct JReplay {
     // ---- dynamic ---------------------------------------------------------
     __device__ void settle(double t) {
         for (int g = 0; g < N; g++) {
-            const int o = g * kThreads;
+            const int o = g * TB;
             bool changed = false;
             int e = W.eff[o], c = W.cmd[o];
             const int r = W.rse[o];
@@ -390,7 +396,7 @@ struct JReplay {
     }
 
     __device__ void flip() {
-        const int g = flip_g, o = g * kThreads;
+        const int g = flip_g, o = g * TB;
         const bool to_p = ((dmask >> g) & 1u) != 0;
         pmask ^= 1u << g;
         dmask ^= 1u << g;
@@ -414,13 +420,10 @@ struct JReplay {
         if ((t - last_move) > pol.cooldown_s) {
             acted = 1;
             const double lo = t - pol.window_s;
-            while (w_tlo < w_th) {
-                const int id = X.ordt[(size_t)w_tlo * 32];
-                const double pe = PE(id);
-                if (!(pe < lo)) break;
-                const double ttft = pe - arr(id);
-                w_tle -= ttft <= P.ttft_slo ? 1 : 0;
-                w_tlt -= ttft < P.ttft_slo ? 1 : 0;
+            while (w_tlo < w_th && wts[(size_t)w_tlo * 32] < lo) {
+                const unsigned char f = wtf[(size_t)w_tlo * 32];
+                w_tle -= f & 1;
+                w_tlt -= f >> 1;
                 w_tlo++;
             }
             while (w_plo < w_ph && X.tst[(size_t)w_plo * 32] < lo) {
@@ -436,17 +439,17 @@ struct JReplay {
             sg.tpot_gt = (phase2 ? w_ple1 : w_ple0) < kq;
             sg.tpot_lt = (phase2 ? w_plt1 : w_plt0) >= kq;
             int qp = 0;
-            for (unsigned m = pmask; m; m &= m - 1) qp += W.ql[(__ffs(m) - 1) * kThreads];
+            for (unsigned m = pmask; m; m &= m - 1) qp += W.ql[(__ffs(m) - 1) * TB];
             sg.q_prefill = qp;
             int newcap[kJG];
             int gsel, dir;
-            JCtlView view{&W, pmask};
+            JCtlView<TB> view{&W, pmask};
             const int act = ctl_step(pol, P.m.min_w, P.m.max_w, P.B, N, view, drain_pending != 0,
                                      last_move, t, sg, newcap, &gsel, &dir);
             if (act == ACT_MOVE_POWER || act == ACT_MOVE_GPU) {
                 last_move = t;
                 if (act == ACT_MOVE_GPU) {
-                    const int g = gsel, o = g * kThreads;
+                    const int g = gsel, o = g * TB;
                     W.fl[o] |= JF_DRAIN;
                     drain_pending = 1;
                     flip_g = g;
@@ -473,7 +476,7 @@ struct JReplay {
                     }
                 }
                 for (int g = 0; g < N; g++) {
-                    const int o = g * kThreads;
+                    const int o = g * TB;
                     const int tg = newcap[g];
                     if (tg < W.cmd[o]) W.cmd[o] = tg;
                     else if (tg > W.cmd[o]) W.rse[o] = tg;
@@ -524,7 +527,7 @@ struct JReplay {
             k = cooldown_tick(k0);           // no tick before it can act, whatever happens
         } else {
             k = tick_at_or_after(next_event, k0);
-            if (w_tlo < w_th) k = min(k, expiry_tick(PE(X.ordt[(size_t)w_tlo * 32]), k0));
+            if (w_tlo < w_th) k = min(k, expiry_tick(wts[(size_t)w_tlo * 32], k0));
             if (w_plo < w_ph) k = min(k, expiry_tick(X.tst[(size_t)w_plo * 32], k0));
         }
         if (k > k0 && k != 0x7fffffffffffffffLL) {
@@ -544,7 +547,7 @@ struct JReplay {
         pmask = dmask = 0;
 #pragma unroll
         for (int g = 0; g < kJG; g++) {
-            const int o = g * kThreads;
+            const int o = g * TB;
             const bool on = g < N;
             const int r = on ? crole[g] : 2;
             if (r == 0) pmask |= 1u << g;
@@ -619,7 +622,7 @@ struct JReplay {
                 else dispatch_decode(g, t, (bd >> g) & 1u, (chg >> g) & 1u);
             }
             if (DYN && flip_g >= 0 && flip_t == PAD_INF) {
-                const int o = flip_g * kThreads;
+                const int o = flip_g * TB;
                 const bool empty = ((pmask >> flip_g) & 1u)
                                        ? (get_tnext(flip_g) == PAD_INF && W.ql[o] == 0)
                                        : (W.a0[o] == 0 && W.ql[o] == 0);
@@ -643,13 +646,13 @@ struct JReplay {
 };
 
 // CTAs bound to one trace (s = blockIdx.x mod S); warps pull 32-replay items.
-template <bool DYN>
-__global__ void __launch_bounds__(kThreads) joint8_kernel(const __grid_constant__ Plan P) {
+template <bool DYN, int TB>
+__global__ void __launch_bounds__(TB) joint8_kernel(const __grid_constant__ Plan P) {
     extern __shared__ __align__(128) unsigned char smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     JWork W;
     {
-        const int n = kJG * kThreads;
+        const int n = kJG * TB;
         unsigned char* p = smem;
         W.tseg = (double*)p + tid; p += n * sizeof(double);
         W.L = (double*)p + tid; p += n * sizeof(double);
@@ -661,12 +664,12 @@ __global__ void __launch_bounds__(kThreads) joint8_kernel(const __grid_constant_
         p += 13 * n * sizeof(int);
         W.fl = p + tid;
     }
-    char* wbase = P.scratch + ((size_t)blockIdx.x * kWarps + warp) * P.warp_bytes;
+    char* wbase = P.scratch + ((size_t)blockIdx.x * (TB / 32) + warp) * P.warp_bytes;
     Scratch X;
     X.link = (int*)(wbase + P.off_link) + lane;
     X.pe = (double*)(wbase + P.off_pe) + lane;
     X.mem = (int2*)(wbase + P.off_mem) + lane;
-    X.ordt = DYN ? (int*)(wbase + P.off_ordt) + lane : nullptr;
+    X.ordt = nullptr;
     X.tst = DYN ? (double*)(wbase + P.off_tst) + lane : nullptr;
     X.tfl = DYN ? (unsigned char*)(wbase + P.off_tfl) + lane : nullptr;
     double* tte = (double*)(wbase + P.off_tte) + lane;
@@ -688,11 +691,13 @@ __global__ void __launch_bounds__(kThreads) joint8_kernel(const __grid_constant_
         const int q = u / P.n_clist;
         const int c = P.clist[u - q * P.n_clist];
         const long long r = ((long long)c * P.Q + q) * P.S + s;
-        JReplay<DYN> rp(P, T, X, W);
+        JReplay<DYN, TB> rp(P, T, X, W);
         rp.tte = tte;
         rp.tti = tti;
         rp.heads = (int*)(wbase + P.off_heads) + lane;
         rp.bits = (unsigned*)(wbase + P.off_bits) + lane;
+        rp.wts = DYN ? (double*)(wbase + P.off_wts) + lane : nullptr;
+        rp.wtf = DYN ? (unsigned char*)(wbase + P.off_wtf) + lane : nullptr;
         const ReplayResult res = rp.run(c, q, P.rec_ttft ? r * P.Rmax : -1);
         P.rep_met[r] = res.met;
         P.rep_near[r] = res.near;

@@ -83,12 +83,14 @@ struct padsim_ctx {
     FPlan fplan{};
     int fA_grid = 0, fC_grid = 0;
     size_t fC_smem = 0, fA_smem = 0;
+    int fA_tb = kThreads;
+    int j_tb[2] = {kThreads, kThreads};
     long long* d_evA = nullptr;
     int n_evA = 0;
     unsigned* d_workC = nullptr;
     std::vector<int> max_out;   // per trace
-    bool j8 = false;            // dynamic candidates on the joint8 kernel (N <= 8)
-    unsigned* d_workJ = nullptr;
+    bool j8[2] = {false, false};   // [static, dynamic] list on the joint8 kernel (N <= 8)
+    unsigned* d_workJ[2] = {nullptr, nullptr};
 };
 
 static const char* kVersion = "padsim 0.1 (sm_100a)";
@@ -128,7 +130,7 @@ static void free_plan(padsim_ctx* ctx) {
     ctx->bufs.clear();
     ctx->planned = false;
     ctx->fact = false;
-    ctx->j8 = false;
+    ctx->j8[0] = ctx->j8[1] = false;
     ctx->static_list.clear();
     ctx->dyn_list.clear();
     for (auto& r : ctx->d_rec) r = nullptr;
@@ -398,18 +400,23 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
         F.a_off_tid = take((size_t)PADSIM_MAX_SLOTS * 32 * sizeof(int));
         F.a_off_tpe = take((size_t)PADSIM_MAX_SLOTS * 32 * sizeof(double));
         F.a_warp_bytes = off;
-        F.a_blocks_per_trace = (int)(((long long)Q * G + kThreads - 1) / kThreads);
+        // small stage-A workloads (e.g. cfg 2: 12k replays) use 32-thread CTAs so every SM
+        // gets some of the latency-bound replays; large ones use 128-thread CTAs
+        const int tb = GQS >= (long long)ctx->n_sm * 2 * kThreads ? kThreads : 32;
+        ctx->fA_tb = tb;
+        F.a_blocks_per_trace = (int)(((long long)Q * G + tb - 1) / tb);
         const long long ctas = (long long)F.a_blocks_per_trace * S;
         char* scr;
-        AL(scr, (size_t)ctas * kWarps * off);
+        AL(scr, (size_t)ctas * (tb / 32) * off);
         F.scrA = scr;
         ctx->fA_grid = (int)ctas;
         const size_t Rp = (Rm + 15) & ~(size_t)15;
-        const size_t tb = Rp * (8 + 8 + 4 + 4 + 1);
-        F.a_smem_trace = kAWorkBytes + tb <= 200 * 1024 ? 1 : 0;
-        ctx->fA_smem = kAWorkBytes + (F.a_smem_trace ? tb : 0);
-        CK(cudaFuncSetAttribute((const void*)stageA_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)ctx->fA_smem));
+        const size_t tb_bytes = Rp * (8 + 8 + 4 + 4 + 1);
+        const size_t wbytes = tb == kThreads ? a_work_bytes<kThreads>() : a_work_bytes<32>();
+        F.a_smem_trace = wbytes + tb_bytes <= 200 * 1024 ? 1 : 0;
+        ctx->fA_smem = wbytes + (F.a_smem_trace ? tb_bytes : 0);
+        const void* fa = tb == kThreads ? (const void*)stageA_kernel<kThreads> : (const void*)stageA_kernel<32>;
+        CK(cudaFuncSetAttribute(fa, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->fA_smem));
     }
     // stage C: CTAs bound to one trace each (staged in smem by TMA bulk copies),
     // warps pull 32-replay items from that trace's counter
@@ -690,7 +697,7 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
     CK(cudaGetLastError());
 
     // factorized static path (stage A prefill groups -> stage C decode) for N <= 8
-    ctx->fact = N <= 8 && !ctx->static_list.empty();
+    ctx->fact = N <= 8 && !ctx->static_list.empty() && !(flags & PADSIM_JOINT);
     if (ctx->fact) {
         int r_ = plan_factorized(ctx, model, slo, n_qps, n_traces, Rmax, tot, cands);
         if (r_) return r_;
@@ -732,12 +739,16 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
         auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~(size_t)255; return o; };
         P.off_link = take(R * 32 * sizeof(int));
         P.off_pe = take(R * 32 * sizeof(double));
-        const bool j8 = dyn && N <= 8;
+        const bool j8 = N <= 8;        // static here only with PADSIM_JOINT
         if (!j8) P.off_mem = take((size_t)N * model->max_decode_batch * 32 * sizeof(int2));
         if (dyn) {
-            P.off_ordt = take(R * 32 * sizeof(int));
+            if (!j8) P.off_ordt = take(R * 32 * sizeof(int));
             P.off_tst = take(R * 32 * sizeof(double));
             P.off_tfl = take(R * 32);
+            if (j8) {
+                P.off_wts = take(R * 32 * sizeof(double));
+                P.off_wtf = take(R * 32);
+            }
         }
         if (j8) {
             P.off_tte = take((size_t)PADSIM_MAX_SLOTS * 32 * sizeof(double));
@@ -753,31 +764,39 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
         P.warp_bytes = off;
         P.scratch_per_cta = off * kWarps;
         if (j8) {
-            ctx->j8 = true;
+            ctx->j8[dyn] = true;
             unsigned* d_wj;
             AL(d_wj, n_traces);
-            ctx->d_workJ = d_wj;
+            ctx->d_workJ[dyn] = d_wj;
             P.work = d_wj;
             P.smem_trace = 0;
-            P.smem_trace_bytes = kJWorkBytes;
-            const void* fnj = (const void*)joint8_kernel<true>;
-            CK(cudaFuncSetAttribute(fnj, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kJWorkBytes));
+            const long long UJ = (long long)n_traces * n_qps * P.n_clist;
+            const int tbj = UJ >= (long long)ctx->n_sm * 3 * kThreads ? kThreads : 32;
+            ctx->j_tb[dyn] = tbj;
+            const size_t jb = tbj == kThreads ? j_work_bytes<kThreads>() : j_work_bytes<32>();
+            P.smem_trace_bytes = jb;
+            const void* fnj = tbj == kThreads
+                ? (dyn ? (const void*)joint8_kernel<true, kThreads> : (const void*)joint8_kernel<false, kThreads>)
+                : (dyn ? (const void*)joint8_kernel<true, 32> : (const void*)joint8_kernel<false, 32>);
+            CK(cudaFuncSetAttribute(fnj, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jb));
             int occj = 0;
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occj, fnj, kThreads, kJWorkBytes));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occj, fnj, tbj, jb));
             occj = std::max(occj, 1);
             const long long items = ((long long)n_qps * P.n_clist + 31) / 32;
+            const int wpc = tbj / 32;
             long long per_trace = std::max<long long>(1, ((long long)ctx->n_sm * occj) / n_traces);
-            per_trace = std::min<long long>(per_trace, (items + kWarps - 1) / kWarps);
+            per_trace = std::min<long long>(per_trace, (items + wpc - 1) / wpc);
+            const size_t per_cta = P.warp_bytes * wpc;
             size_t frj = 0, tmj = 0;
             CK(cudaMemGetInfo(&frj, &tmj));
-            const long long cap_ctas = std::max<long long>(n_traces, (long long)((frj * 2 / 5) / P.scratch_per_cta));
+            const long long cap_ctas = std::max<long long>(n_traces, (long long)((frj * 2 / 5) / per_cta));
             long long gridj = std::min<long long>(per_trace * n_traces, (cap_ctas / n_traces) * n_traces);
             gridj = std::max<long long>(gridj, n_traces);
             char* scrj = nullptr;
-            AL(scrj, (size_t)gridj * P.scratch_per_cta);
+            AL(scrj, (size_t)gridj * per_cta);
             P.scratch = scrj;
-            ctx->grid_dyn = (int)gridj;
-            ctx->smem_dyn = kJWorkBytes;
+            (dyn ? ctx->grid_dyn : ctx->grid_static) = (int)gridj;
+            (dyn ? ctx->smem_dyn : ctx->smem_static) = jb;
             continue;
         }
         // trace staging in shared memory via TMA bulk copies when it fits
@@ -839,9 +858,15 @@ int padsim_run(padsim_ctx* ctx, void* stream) {
         if (P.n_clist == 0) continue;
         const int grid = dyn ? ctx->grid_dyn : ctx->grid_static;
         const size_t smem = dyn ? ctx->smem_dyn : ctx->smem_static;
-        if (dyn && ctx->j8) {
-            CK(cudaMemsetAsync(ctx->d_workJ, 0, (size_t)ctx->S * sizeof(unsigned), js));
-            joint8_kernel<true><<<grid, kThreads, smem, js>>>(P);
+        if (ctx->j8[dyn]) {
+            CK(cudaMemsetAsync(ctx->d_workJ[dyn], 0, (size_t)ctx->S * sizeof(unsigned), js));
+            if (ctx->j_tb[dyn] == kThreads) {
+                if (dyn) joint8_kernel<true, kThreads><<<grid, kThreads, smem, js>>>(P);
+                else joint8_kernel<false, kThreads><<<grid, kThreads, smem, js>>>(P);
+            } else {
+                if (dyn) joint8_kernel<true, 32><<<grid, 32, smem, js>>>(P);
+                else joint8_kernel<false, 32><<<grid, 32, smem, js>>>(P);
+            }
         } else if (ctx->N <= 8) {
             if (dyn) replay_kernel<8, true><<<grid, kThreads, smem, js>>>(P);
             else replay_kernel<8, false><<<grid, kThreads, smem, js>>>(P);
@@ -855,7 +880,8 @@ int padsim_run(padsim_ctx* ctx, void* stream) {
     if (ctx->fact) {
         const FPlan& F = ctx->fplan;
         CK(cudaMemsetAsync(ctx->d_workC, 0, (size_t)ctx->S * sizeof(unsigned), st));
-        stageA_kernel<<<ctx->fA_grid, kThreads, ctx->fA_smem, st>>>(F);
+        if (ctx->fA_tb == kThreads) stageA_kernel<kThreads><<<ctx->fA_grid, kThreads, ctx->fA_smem, st>>>(F);
+        else stageA_kernel<32><<<ctx->fA_grid, 32, ctx->fA_smem, st>>>(F);
         CK(cudaGetLastError());
         CK(cudaEventRecord(ctx->evA, st));
         if (ctx->model.decode_per_ctx_tok_s == 0.0)

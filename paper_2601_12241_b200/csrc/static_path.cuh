@@ -117,14 +117,16 @@ struct FPlan {
 // worker index, convergent lanes).  The ≤ 32 in-flight transfers live in
 // lane-interleaved scratch with the earliest (te, id) cached in registers.
 // ---------------------------------------------------------------------------
-constexpr size_t kAWorkBytes = (size_t)kNW * kThreads * (sizeof(double) + 5 * sizeof(int));
+template <int TB>
+__host__ __device__ constexpr size_t a_work_bytes() { return (size_t)kNW * TB * (sizeof(double) + 5 * sizeof(int)); }
 
-__global__ void __launch_bounds__(kThreads) stageA_kernel(const __grid_constant__ FPlan P) {
+template <int TB>
+__global__ void __launch_bounds__(TB) stageA_kernel(const __grid_constant__ FPlan P) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ unsigned long long bar;
     const int tid = threadIdx.x;
     const int s = blockIdx.x / P.a_blocks_per_trace;
-    const int local = (blockIdx.x - s * P.a_blocks_per_trace) * kThreads + tid;
+    const int local = (blockIdx.x - s * P.a_blocks_per_trace) * TB + tid;
     const long long off = P.toff[s];
     const int R = P.nreq[s];
     // the CTA's trace: staged once in shared memory by TMA bulk copies, read by
@@ -136,7 +138,7 @@ __global__ void __launch_bounds__(kThreads) stageA_kernel(const __grid_constant_
     const unsigned char* ph;
     if (P.a_smem_trace) {
         const int Rp = (R + 15) & ~15;
-        double* d_su = (double*)(smem + kAWorkBytes);
+        double* d_su = (double*)(smem + a_work_bytes<TB>());
         double* d_kv = d_su + Rp;
         int* d_in = (int*)(d_kv + Rp);
         int* d_ot = d_in + Rp;
@@ -161,8 +163,8 @@ __global__ void __launch_bounds__(kThreads) stageA_kernel(const __grid_constant_
     if (local >= P.Q * P.n_groups) return;
     const int q = local / P.n_groups;
     const int g = local - q * P.n_groups;
-    const long long u = (long long)blockIdx.x * kThreads + tid;    // scratch slot
-    const int n_sm = kNW * kThreads;
+    const long long u = (long long)blockIdx.x * TB + tid;    // scratch slot
+    const int n_sm = kNW * TB;
     double* Wsp = (double*)smem + tid;
     int* ib = (int*)(smem + (size_t)n_sm * sizeof(double));
     int* Wqh = ib + 0 * n_sm + tid;
@@ -187,7 +189,7 @@ __global__ void __launch_bounds__(kThreads) stageA_kernel(const __grid_constant_
     long long a0[kNW];              // outstanding tokens = routing key (A8)
 #pragma unroll
     for (int w = 0; w < kNW; w++) {
-        const int o = w * kThreads;
+        const int o = w * TB;
         tnext[w] = PAD_INF;
         a0[w] = w < x ? 0 : 0x7fffffffffffffffLL;
         Wqh[o] = kNoIdx; Wqt[o] = kNoIdx; Wql[o] = 0; Wbh[o] = 0; Wbn[o] = 0;
@@ -210,7 +212,7 @@ __global__ void __launch_bounds__(kThreads) stageA_kernel(const __grid_constant_
         // kind 2: prefill batch ends, worker order; members enter the KV buffer
         for (unsigned m = bm; m; m &= m - 1) {
             const int w = __ffs(m) - 1;
-            const int o = w * kThreads;
+            const int o = w * TB;
             int i = Wbh[o];
             const int n = Wbn[o];
             long long dec = 0;
@@ -281,7 +283,7 @@ __global__ void __launch_bounds__(kThreads) stageA_kernel(const __grid_constant_
             const int tin = it[i];
             radd<kNW, long long>(a0, best, (long long)tin);
             link[(size_t)i * 32] = kNoIdx;
-            const int o = best * kThreads;
+            const int o = best * TB;
             const int qn = Wql[o];
             if (qn == 0) Wqh[o] = i; else link[(size_t)Wqt[o] * 32] = i;
             Wqt[o] = i;
@@ -293,7 +295,7 @@ __global__ void __launch_bounds__(kThreads) stageA_kernel(const __grid_constant_
         // dispatch: idle prefill workers take a FIFO prefix (A9)
         for (unsigned m = bm | touched; m; m &= m - 1) {
             const int w = __ffs(m) - 1;
-            const int o = w * kThreads;
+            const int o = w * TB;
             const double tw = rget<kNW>(tnext, w);
             const int qn = Wql[o];
             if (tw != PAD_INF || qn == 0) continue;

@@ -222,3 +222,67 @@ def test_enumeration_on_gpu_build(pkg):
     for N, B in ((8, 4800), (64, 38400)):
         assert np.array_equal(pkg.enumerate_pool_uniform(N, B, 400, 750, 25),
                               oracle.enumerate_pool_uniform(N, B, 400, 750, 25))
+
+
+def test_joint_kernel_matches_factorized_path(pkg):
+    # the same static candidates through the factorized stages (default) and through
+    # the joint kernel (PADSIM_JOINT): identical per-request records, both = oracle
+    role, cap = static_candidates(8, XPD)
+    pols = [policy("static")] * len(XPD)
+    traces = [make_trace("lb", 40 + s, 400) for s in range(2)] + [make_trace("lb_bursty", 3, 300)]
+    qps = [0.5, 1.75, 3.5]
+    outs = []
+    for joint in (False, True):
+        ctx = pkg.Context(0)
+        try:
+            ctx.plan(traces, qps, DEFAULT_MODEL, role, cap, pols, DEFAULT_SLO, 4800, records=True,
+                     joint=joint)
+            ctx.run()
+            outs.append((ctx.fetch(), ctx.fetch_replays(), ctx.fetch_records()))
+        finally:
+            ctx.close()
+    (ra, pa, ca), (rb, pb, cb) = outs
+    for k in ra:
+        assert np.array_equal(ra[k], rb[k]), k
+    for k in ("met", "near_boundary", "duration", "goodput"):
+        assert np.array_equal(pa[k], pb[k]), k
+    for k in ca:
+        assert np.array_equal(ca[k], cb[k]), k
+    ref = oracle.evaluate(DEFAULT_MODEL, role, cap, pols, 4800, DEFAULT_SLO, traces, qps, n_threads=8)
+    assert np.array_equal(ra["met"], ref["met"]) and np.array_equal(ra["argmax"], ref["argmax"])
+
+
+def test_cfg1_full_exact(pkg):
+    # BASELINE cfg 1 in full: 4P4D on a 100 W grid (13 candidates), one 200-request trace
+    xpd = pkg.enumerate_pool_uniform(8, 4800, 400, 750, 100)
+    xpd = xpd[xpd[:, 0] == 4]
+    assert len(xpd) == 13
+    role, cap = static_candidates(8, xpd)
+    pols = [policy("static")] * 13
+    compare_records([make_trace("lb", 0, 200)], [1.5], DEFAULT_MODEL, role, cap, pols, DEFAULT_SLO, 4800)
+
+
+def test_cfg4_shape_sampled(pkg):
+    # cfg 4 shape: static + dynamic (3 policies x 7 splits at 600 W), R = 2000; sampled oracle
+    cands = pkg.enumerate_pool_uniform(8, 4800, 400, 750, 50)
+    role, cap = static_candidates(8, cands)
+    drole, dcap = static_candidates(8, [(x, 600, 600) for x in range(1, 8)] * 3)
+    role = np.concatenate([role, drole])
+    cap = np.concatenate([cap, dcap])
+    pols = [policy("static")] * len(cands) + [policy(k) for k in ("dyn-power", "dyn-gpu", "dyn-both")
+                                               for _ in range(7)]
+    traces = [make_trace("lb", s, 2000) for s in range(2)]
+    qps = [0.0625 * k for k in (4, 16, 24, 32, 48, 64)]
+    ctx = pkg.Context(0)
+    ctx.plan(traces, qps, DEFAULT_MODEL, role, cap, pols, DEFAULT_SLO, 4800)
+    ctx.run()
+    rep = ctx.fetch_replays()
+    ctx.close()
+    rng = np.random.default_rng(4)
+    picks = [(int(c), int(rng.integers(len(qps))), int(rng.integers(2)))
+             for c in list(rng.integers(len(cands), size=12)) + list(range(len(cands), len(pols)))]
+    for c, q, s in picks:
+        o = oracle.replay(DEFAULT_MODEL, role[c], cap[c], pols[c], 4800, DEFAULT_SLO, traces[s], qps[q])
+        assert rep["met"][c, q, s] == o["met"], (c, q, s)
+        assert rep["duration"][c, q, s] == o["duration"]
+        assert rep["goodput"][c, q, s] == o["goodput"]
