@@ -65,7 +65,8 @@ class Summary(C.Structure):
     _fields_ = [("met", C.c_int32), ("near_boundary", C.c_int32), ("n_req", C.c_int32),
                 ("pad", C.c_int32), ("duration", C.c_double), ("goodput", C.c_double),
                 ("events", C.c_int64), ("n_moves_power", C.c_int32), ("n_moves_gpu", C.c_int32),
-                ("n_saturated", C.c_int32), ("n_flips", C.c_int32)]
+                ("n_saturated", C.c_int32), ("n_flips", C.c_int32), ("avg_watts", C.c_double),
+                ("qps_per_watt", C.c_double)]
 
 
 class LogRec(C.Structure):
@@ -130,6 +131,9 @@ def lib():
                                       _P(_P(C.c_uint8)), C.c_int32, _P(C.c_double), C.c_int32,
                                       _P(C.c_int64), _P(C.c_double), _P(C.c_int64), _P(C.c_int32),
                                       _P(C.c_int32), _P(C.c_double), _P(C.c_double)]
+            L.or_met_for_slos.restype = C.c_int
+            L.or_met_for_slos.argtypes = [C.c_int32, _P(C.c_double), _P(C.c_double), _P(C.c_uint8),
+                                          C.c_int32, _P(Slo), _P(C.c_int32)]
             L.or_step_controller.restype = C.c_int
             L.or_step_controller.argtypes = [_P(Policy), _P(Model), C.c_int32, _P(CtlState),
                                              _P(CtlObs), C.c_double, _P(CtlAction)]
@@ -258,7 +262,8 @@ def replay(model: dict, role, cap, policy: dict, budget_w: int, slo: dict, trace
     res = {k: v[:R] for k, v in outs.items()}
     res.update(met=sm.met, near_boundary=sm.near_boundary, duration=sm.duration,
                goodput=sm.goodput, events=sm.events, n_moves_power=sm.n_moves_power,
-               n_moves_gpu=sm.n_moves_gpu, n_saturated=sm.n_saturated, n_flips=sm.n_flips)
+               n_moves_gpu=sm.n_moves_gpu, n_saturated=sm.n_saturated, n_flips=sm.n_flips,
+               avg_watts=sm.avg_watts, qps_per_watt=sm.qps_per_watt)
     if lg is not None:
         n = min(lg.n, log_cap)
         res["log"] = [(recs[k].t, recs[k].type, recs[k].gpu, recs[k].a, recs[k].b) for k in range(n)]
@@ -303,6 +308,20 @@ def evaluate(model: dict, role, cap, policies, budget_w: int, slo: dict, traces,
     if per_replay:
         out.update(rep_met=rm, rep_goodput=rg, rep_duration=rd)
     return out
+
+
+def met_for_slos(ttft, tpot, phase, slos) -> np.ndarray:
+    """Met counts of one replay's records against several SLO sets."""
+    t1 = np.ascontiguousarray(ttft, dtype=np.float64)
+    t2 = np.ascontiguousarray(tpot, dtype=np.float64)
+    ph = np.ascontiguousarray(phase, dtype=np.uint8)
+    arr = (Slo * max(len(slos), 1))(*[make_slo(s) for s in slos])
+    out = np.zeros(max(len(slos), 1), np.int32)
+    rc = lib().or_met_for_slos(t1.size, _ptr(t1, C.c_double), _ptr(t2, C.c_double), _ptr(ph, C.c_uint8),
+                               len(slos), arr, _ptr(out, C.c_int32))
+    if rc != 0:
+        raise OracleError(rc)
+    return out[: len(slos)]
 
 
 def step_controller(policy: dict, model: dict, budget_w: int, state: dict, obs: dict, now: float):

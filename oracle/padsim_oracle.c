@@ -360,6 +360,11 @@ int or_replay(const or_model* m, int32_t N, const uint8_t* role, const int32_t* 
     if (dynamic && heap_push(&h, (double)tick_k * pol->tick_s, K_TICK, 0)) goto out;
 
     int completed = 0, tbusy = 0, phase2_seen = 0, drain_pending = 0;
+    /* provisioned power ("average provisioned GPU power"): Σ eff caps is
+     * piecewise constant, changing only at settle instants; integrated over [a_0, last] */
+    long w_sum = 0;
+    for (int g = 0; g < N; g++) w_sum += W[g].eff;
+    double w_acc = 0.0, w_prev = a[0];
     double last_move = 0.0;    /* Alg. 1 "last_move_time ← 0", A24 */
     int64_t events = 0;
     if (lg) {
@@ -390,6 +395,12 @@ int or_replay(const or_model* m, int32_t N, const uint8_t* role, const int32_t* 
                     if (w->raise_to > 0) { w->cmd = w->eff = w->raise_to; w->raise_to = 0; changed = 1; }
                     if (changed && w->role == 1) w->dirty = 1;
                 }
+                if (t > a[0]) {
+                    w_acc = w_acc + (double)w_sum * (t - w_prev);
+                    w_prev = t;
+                }
+                w_sum = 0;
+                for (int g = 0; g < N; g++) w_sum += W[g].eff;
                 if (lg) {
                     long c = 0; for (int g = 0; g < N; g++) c += W[g].eff;
                     log_put(lg, t, OR_LOG_SETTLE, -1, 0, 0);
@@ -681,6 +692,9 @@ int or_replay(const or_model* m, int32_t N, const uint8_t* role, const int32_t* 
         sum->duration = last - a[0];
         sum->goodput = sum->duration > 0 ? (double)met / sum->duration : 0.0;
         sum->events = events;
+        w_acc = w_acc + (double)w_sum * (last - w_prev);
+        sum->avg_watts = sum->duration > 0 ? w_acc / sum->duration : (double)w_sum;
+        sum->qps_per_watt = sum->avg_watts > 0 ? sum->goodput / sum->avg_watts : 0.0;
     }
     rc = 0;
 out:
@@ -694,6 +708,19 @@ out:
     free(twait.buf); free(s_ttft.stamp); free(s_ttft.val); free(s_tpot.stamp); free(s_tpot.val);
     free(h.a);
     return rc;
+}
+
+int or_met_for_slos(int32_t R, const double* ttft, const double* tpot, const uint8_t* phase,
+                    int32_t K, const or_slo* slos, int32_t* out_met) {
+    if (R < 0 || K < 0 || (R > 0 && (!ttft || !tpot || !phase)) || (K > 0 && (!slos || !out_met)))
+        return -1;
+    for (int k = 0; k < K; k++) {
+        int m = 0;
+        for (int i = 0; i < R; i++)
+            if (ttft[i] <= slos[k].ttft && tpot[i] <= slos[k].tpot[phase[i]]) m++;
+        out_met[k] = m;
+    }
+    return 0;
 }
 
 /* ------------------------------------------------------------------------ */

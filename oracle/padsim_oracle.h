@@ -59,6 +59,8 @@ typedef struct {
     double duration, goodput;
     int64_t events;       /* heap events processed (diagnostic)             */
     int32_t n_moves_power, n_moves_gpu, n_saturated, n_flips;
+    double avg_watts;     /* time-weighted mean of Σ effective caps over [a_0, last completion] */
+    double qps_per_watt;  /* goodput / avg_watts                                  */
 } or_summary;
 
 /* log records for invariant tests (budget, cooldown, role bounds, masking) */
@@ -96,6 +98,11 @@ int or_evaluate(const or_model* m, int32_t n_gpus, int32_t n_cand, const uint8_t
                 const uint8_t* const* phase, int32_t n_qps, const double* qps,
                 int32_t n_threads, int64_t* met, double* goodput, int64_t* near_boundary,
                 int32_t* argmax, int32_t* rep_met, double* rep_goodput, double* rep_duration);
+
+/* met count of one replay's per-request records against K SLO sets (the
+ * inclusive rule of S:407, per-phase TPOT SLO): out_met[k].           */
+int or_met_for_slos(int32_t n_req, const double* ttft, const double* tpot, const uint8_t* phase,
+                    int32_t n_slo, const or_slo* slos, int32_t* out_met);
 
 /* Pool-uniform candidate enumeration by brute force over (x, p, d) (a1). */
 int or_enumerate(int32_t n_gpus, int32_t budget_w, int32_t min_w, int32_t max_w, int32_t step_w,

@@ -39,7 +39,11 @@ struct padsim_ctx {
     std::vector<long long> toff;
     std::vector<int> capsum_h;
     // device buffers
-    std::vector<void*> bufs;
+    // device buffers of the current plan; a re-plan with the same shapes reuses them
+    // in allocation order (no cudaMalloc/cudaFree on the end-to-end path)
+    struct Buf { void* p; size_t bytes; };
+    std::vector<Buf> bufs;
+    size_t buf_cursor = 0;
     long long* d_toff = nullptr;
     int* d_nreq = nullptr;
     double* d_s_unit = nullptr;
@@ -113,21 +117,37 @@ template <class T>
 static int dalloc(padsim_ctx* ctx, T** p, size_t n) {
     *p = nullptr;
     if (n == 0) n = 1;
+    const size_t bytes = n * sizeof(T);
+    const size_t k = ctx->buf_cursor++;
+    if (k < ctx->bufs.size() && ctx->bufs[k].bytes >= bytes) {
+        *p = (T*)ctx->bufs[k].p;
+        return PADSIM_OK;
+    }
+    if (k < ctx->bufs.size()) {
+        cudaFree(ctx->bufs[k].p);
+        ctx->bufs[k] = {nullptr, 0};
+    }
     void* q = nullptr;
-    cudaError_t e = cudaMalloc(&q, n * sizeof(T));
+    cudaError_t e = cudaMalloc(&q, bytes);
     if (e != cudaSuccess) {
         cudaGetLastError();
         ctx->err = std::string("cudaMalloc: ") + cudaGetErrorString(e);
         return PADSIM_ENOMEM;
     }
-    ctx->bufs.push_back(q);
+    if (k < ctx->bufs.size()) ctx->bufs[k] = {q, bytes};
+    else ctx->bufs.push_back({q, bytes});
     *p = (T*)q;
     return PADSIM_OK;
 }
 
-static void free_plan(padsim_ctx* ctx) {
-    for (void* p : ctx->bufs) cudaFree(p);
+static void release_buffers(padsim_ctx* ctx) {
+    for (auto& b : ctx->bufs) if (b.p) cudaFree(b.p);
     ctx->bufs.clear();
+    ctx->buf_cursor = 0;
+}
+
+static void free_plan(padsim_ctx* ctx) {
+    ctx->buf_cursor = 0;       // buffers are kept for reuse by the next plan
     ctx->planned = false;
     ctx->fact = false;
     ctx->j8[0] = ctx->j8[1] = false;
@@ -453,7 +473,7 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
         size_t fr = 0, tm = 0;
         CK(cudaMemGetInfo(&fr, &tm));
         const size_t per_cta = off * kWarps;
-        const long long cap_ctas = std::max<long long>(S, (long long)((fr * 2 / 5) / per_cta));
+        const long long cap_ctas = std::max<long long>(S, (long long)((tm * 3 / 10) / per_cta));
         long long grid = std::min<long long>(per_trace * S, (cap_ctas / S) * S);
         grid = std::max<long long>(grid, S);
         char* scr;
@@ -501,6 +521,7 @@ void padsim_destroy(padsim_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     free_plan(ctx);
+    release_buffers(ctx);
     if (ctx->d_ctl_state) cudaFree(ctx->d_ctl_state);
     if (ctx->d_ctl_act) cudaFree(ctx->d_ctl_act);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
@@ -789,7 +810,7 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
             const size_t per_cta = P.warp_bytes * wpc;
             size_t frj = 0, tmj = 0;
             CK(cudaMemGetInfo(&frj, &tmj));
-            const long long cap_ctas = std::max<long long>(n_traces, (long long)((frj * 2 / 5) / per_cta));
+            const long long cap_ctas = std::max<long long>(n_traces, (long long)((tmj * 3 / 10) / per_cta));
             long long gridj = std::min<long long>(per_trace * n_traces, (cap_ctas / n_traces) * n_traces);
             gridj = std::max<long long>(gridj, n_traces);
             char* scrj = nullptr;
@@ -816,7 +837,7 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
         // bound the scratch to ~40% of free device memory
         size_t fr = 0, totm = 0;
         CK(cudaMemGetInfo(&fr, &totm));
-        const long long max_ctas = (long long)((fr * 2 / 5) / std::max<size_t>(P.scratch_per_cta, 1));
+        const long long max_ctas = (long long)((totm * 3 / 10) / std::max<size_t>(P.scratch_per_cta, 1));
         if (max_ctas < 1) return fail(ctx, PADSIM_ENOMEM, "scratch does not fit in device memory");
         grid = std::max<long long>(1, std::min(grid, max_ctas));
         char* scr = nullptr;
