@@ -196,6 +196,27 @@ int padsim_replay_kernel_ms(padsim_ctx* ctx, float* ms);
  * a side stream concurrently with [0]+[1]; 0 if not run.                   */
 int padsim_kernel_times_ms(padsim_ctx* ctx, float* ms3);
 
+/* ---- SLO scaling, QPS/W, max QPS at 80 % ---------------
+ * Static trajectories do not depend on the SLOs, so extra SLO sets are scored
+ * on the same replays for the cost of a compare (Fig. 5b TPOT 25 ms, Fig. 8
+ * SLO scaling 0.5x–2x).  padsim_set_slo_sweep (after padsim_plan,
+ * before padsim_run): up to PADSIM_MAX_SLO_SWEEP extra SLO sets (all > 0).
+ * padsim_fetch_extras (synchronises), any pointer may be NULL:
+ *   met_sweep[(c*Q + q)*8 + k]  Σ over traces of requests meeting SLO set k
+ *   qps_per_watt[c*Q + q]       Σ over traces (ascending) of goodput / avg
+ *                               provisioned GPU W
+ *   avg_watts[c*Q + q]          Σ over traces of the time-weighted mean of the
+ *                               Σ of effective caps over [a_0, last completion]
+ *                               (static: Σ caps); divide by n_traces for a mean
+ *   max_qps80[c*9 + k]          k = 0: main SLO, k = 1..8: sweep set k−1 — the
+ *                               QPS index with the largest QPS among those with
+ *                               5·Σmet ≥ 4·Σ n_req (≥ 80 % attainment),
+ *                               −1 if none.                                      */
+#define PADSIM_MAX_SLO_SWEEP 8
+int padsim_set_slo_sweep(padsim_ctx* ctx, const padsim_slo* slos, int32_t n_slo);
+int padsim_fetch_extras(padsim_ctx* ctx, void* stream, int64_t* met_sweep, double* qps_per_watt,
+                        double* avg_watts, int32_t* max_qps80);
+
 /* Per-replay host copies (synchronises): arrays of C*Q*S, any may be NULL. */
 int padsim_fetch_replays(padsim_ctx* ctx, void* stream, int32_t* met, int32_t* near_boundary,
                          double* duration, double* goodput, int64_t* events);

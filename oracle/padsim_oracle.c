@@ -319,6 +319,7 @@ int or_replay(const or_model* m, int32_t N, const uint8_t* role, const int32_t* 
     }
     memset(sum, 0, sizeof(*sum));
     sum->n_req = R;
+    sum->avg_watts = (double)capsum;     /* nothing happens: the initial provisioning */
     if (R == 0) return 0;
 
     int rc = -8;

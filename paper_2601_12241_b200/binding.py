@@ -103,7 +103,8 @@ EXPORTS = ["padsim_create", "padsim_destroy", "padsim_last_error", "padsim_versi
            "padsim_evaluate_allocations", "padsim_plan", "padsim_run", "padsim_fetch",
            "padsim_get_device_results", "padsim_fetch_replays", "padsim_fetch_records",
            "padsim_argmax_device", "padsim_step_controller", "padsim_enumerate_pool_uniform",
-           "padsim_replay_kernel_ms", "padsim_kernel_times_ms"]
+           "padsim_replay_kernel_ms", "padsim_kernel_times_ms", "padsim_set_slo_sweep",
+           "padsim_fetch_extras"]
 
 _lib = None
 _P = C.POINTER
@@ -134,6 +135,9 @@ def load(path: str = LIB_PATH):
     L.padsim_get_device_results.argtypes = [vp, _P(DeviceResults)]
     L.padsim_replay_kernel_ms.argtypes = [vp, _P(C.c_float)]
     L.padsim_kernel_times_ms.argtypes = [vp, _P(C.c_float)]
+    L.padsim_set_slo_sweep.argtypes = [vp, _P(Slo), C.c_int32]
+    L.padsim_fetch_extras.argtypes = [vp, vp, _P(C.c_int64), _P(C.c_double), _P(C.c_double),
+                                      _P(C.c_int32)]
     L.padsim_fetch_replays.argtypes = [vp, vp, _P(C.c_int32), _P(C.c_int32), _P(C.c_double),
                                        _P(C.c_double), _P(C.c_int64)]
     L.padsim_fetch_records.argtypes = [vp, vp] + [_P(C.c_double)] * 5 + [_P(C.c_int32)]
@@ -292,6 +296,27 @@ class Context:
         ms = C.c_float(0.0)
         self._check(self.L.padsim_replay_kernel_ms(self.ptr, C.byref(ms)), "replay_kernel_ms")
         return float(ms.value)
+
+    def set_slo_sweep(self, slos):
+        """Score up to 8 extra SLO sets on the same replays (padsim_set_slo_sweep)."""
+        arr = (Slo * max(len(slos), 1))(*[make_slo(x) for x in slos])
+        self._check(self.L.padsim_set_slo_sweep(self.ptr, arr, len(slos)), "set_slo_sweep")
+        self.n_sweep = len(slos)
+
+    def fetch_extras(self, stream=None):
+        """SLO-sweep met counts, QPS/W, mean provisioned W, max QPS index at ≥80 %."""
+        Cn, Q, S, _ = self.shape
+        K = 8
+        metk = np.zeros((Cn, Q, K), np.int64)
+        qpw = np.zeros((Cn, Q), np.float64)
+        watts = np.zeros((Cn, Q), np.float64)
+        m80 = np.zeros((Cn, K + 1), np.int32)
+        self._check(self.L.padsim_fetch_extras(self.ptr, C.c_void_p(stream or 0), _p(metk, C.c_int64),
+                                               _p(qpw, C.c_double), _p(watts, C.c_double),
+                                               _p(m80, C.c_int32)), "fetch_extras")
+        n = getattr(self, "n_sweep", 0)
+        return {"met_sweep": metk[:, :, :n], "qps_per_watt": qpw, "watts_sum": watts,
+                "max_qps80": m80[:, : n + 1]}
 
     def kernel_times_ms(self):
         """[stage A, stage C, joint] device ms of the last run."""

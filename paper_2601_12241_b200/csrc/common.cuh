@@ -11,6 +11,17 @@
 
 namespace padsim {
 
+constexpr int kMaxSloSweep = 8;        // extra SLO sets scored per replay
+
+// Extra SLO sets scored on the same trajectories + per-replay extra outputs.
+struct SloSweep {
+    int n;
+    double ttft[kMaxSloSweep], tpot0[kMaxSloSweep], tpot1[kMaxSloSweep];
+    int* rep_met;          // [r * kMaxSloSweep + k]
+    double* rep_watts;     // [r] time-weighted mean of Σ effective caps
+    const int* capsum;     // [C] Σ initial caps
+};
+
 constexpr int kThreads = 128;          // replays per CTA (4 warps)
 constexpr int kWarps = kThreads / 32;
 constexpr int kNoIdx = -1;
@@ -58,6 +69,7 @@ struct Plan {
     long long* rep_events;
     // optional per-request records [r*Rmax + i]
     double *rec_ttft, *rec_tpot, *rec_pe, *rec_comp, *rec_te;
+    SloSweep sw;
     // scratch: per CTA slot, lane-interleaved
     char* scratch;
     size_t scratch_per_cta;

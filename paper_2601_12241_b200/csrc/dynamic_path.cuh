@@ -88,6 +88,11 @@ struct JReplay {
     int flip_g, drain_pending, phase2;
     int w_th, w_tlo, w_tle, w_tlt, w_ph, w_plo, w_ple0, w_plt0, w_ple1, w_plt1;
     unsigned touched;
+    // SLO sweep + provisioned power (time-weighted Σ effective caps)
+    int* metk;            // this replay's sweep counters (global, kMaxSloSweep)
+    int nk;
+    long long w_sum;
+    double w_acc, w_prev, a0t;
 
     __device__ JReplay(const Plan& p, const TraceView& t, const Scratch& x, const JWork& w)
         : P(p), T(t), X(x), W(w) {}
@@ -136,6 +141,10 @@ struct JReplay {
         met += (ttft <= P.ttft_slo && tpot <= ts) ? 1 : 0;
         near += (fabs(ttft - P.ttft_slo) <= 1e-9 * P.ttft_slo || fabs(tpot - ts) <= 1e-9 * ts) ? 1 : 0;
         maxcomp = fmax(maxcomp, t);
+        for (int z = 0; z < nk; z++) {
+            const double tz = T.phase[i] ? P.sw.tpot1[z] : P.sw.tpot0[z];
+            if (ttft <= P.sw.ttft[z] && tpot <= tz) metk[z]++;
+        }
         if (DYN) {
             const unsigned char f = (tpot <= P.tpot_slo0 ? 1 : 0) | (tpot < P.tpot_slo0 ? 2 : 0) |
                                     (tpot <= P.tpot_slo1 ? 4 : 0) | (tpot < P.tpot_slo1 ? 8 : 0);
@@ -393,6 +402,13 @@ struct JReplay {
             }
         }
         settle_t = PAD_INF;
+        if (t > a0t) {
+            w_acc = w_acc + (double)w_sum * (t - w_prev);
+            w_prev = t;
+        }
+        long long ws = 0;
+        for (int g = 0; g < N; g++) ws += W.eff[g * TB];
+        w_sum = ws;
     }
 
     __device__ void flip() {
@@ -579,6 +595,12 @@ struct JReplay {
         } else {
             tick_t = settle_t = flip_t = PAD_INF;
         }
+        nk = P.sw.n;
+        for (int z = 0; z < nk; z++) metk[z] = 0;
+        w_sum = P.sw.capsum[c];
+        a0t = R > 0 ? arr(0) : 0.0;
+        w_acc = 0.0;
+        w_prev = a0t;
         long long events = 0;
         int na = 0;
         double ta = R > 0 ? arr(0) : PAD_INF;
@@ -641,6 +663,8 @@ struct JReplay {
         res.duration = R > 0 ? maxcomp - arr(0) : 0.0;
         res.goodput = res.duration > 0 ? (double)met / res.duration : 0.0;
         res.events = events;
+        if (R > 0) w_acc = w_acc + (double)w_sum * (maxcomp - w_prev);
+        res.watts = res.duration > 0 ? w_acc / res.duration : (double)w_sum;
         return res;
     }
 };
@@ -692,6 +716,7 @@ __global__ void __launch_bounds__(TB) joint8_kernel(const __grid_constant__ Plan
         const int c = P.clist[u - q * P.n_clist];
         const long long r = ((long long)c * P.Q + q) * P.S + s;
         JReplay<DYN, TB> rp(P, T, X, W);
+        rp.metk = P.sw.rep_met + r * kMaxSloSweep;
         rp.tte = tte;
         rp.tti = tti;
         rp.heads = (int*)(wbase + P.off_heads) + lane;
@@ -704,6 +729,7 @@ __global__ void __launch_bounds__(TB) joint8_kernel(const __grid_constant__ Plan
         P.rep_dur[r] = res.duration;
         P.rep_good[r] = res.goodput;
         P.rep_events[r] = res.events;
+        P.sw.rep_watts[r] = res.watts;
     }
 }
 

@@ -68,6 +68,15 @@ struct padsim_ctx {
     double* d_good = nullptr;
     long long* d_near = nullptr;
     int* d_argmax = nullptr;
+    // SLO sweep / provisioned power outputs
+    int* d_rep_metk = nullptr;
+    double* d_rep_watts = nullptr;
+    long long* d_metk = nullptr;     // [C*Q*kMaxSloSweep]
+    double* d_qpw = nullptr;         // [C*Q] Σ_s goodput/avg_watts
+    double* d_watts = nullptr;       // [C*Q] Σ_s avg_watts
+    int* d_max80 = nullptr;          // [C*(1+kMaxSloSweep)]
+    long long n_req_total = 0;
+    SloSweep sweep{};
     double *d_rec[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     unsigned* d_work = nullptr;
     char* d_scratch_static = nullptr;
@@ -199,20 +208,50 @@ __global__ void tables_kernel(const padsim_model m, double* spre, double* sdec, 
 // row a8: seed reduction (ascending trace order) and per-QPS argmax
 // ---------------------------------------------------------------------------
 __global__ void reduce_kernel(const int* rep_met, const int* rep_near, const double* rep_good,
-                              int CQ, int S, long long* met, double* good, long long* near) {
+                              int CQ, int S, long long* met, double* good, long long* near,
+                              const int* rep_metk, const double* rep_watts, int nk,
+                              long long* metk, double* qpw, double* watts) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= CQ) return;
     long long m = 0, nn = 0;
-    double g = 0.0;
+    long long mk[kMaxSloSweep] = {0, 0, 0, 0, 0, 0, 0, 0};
+    double g = 0.0, qw = 0.0, ws = 0.0;
     const long long base = (long long)k * S;
-    for (int s = 0; s < S; s++) {
-        m += rep_met[base + s];
-        nn += rep_near[base + s];
-        g += rep_good[base + s];
+    for (int s = 0; s < S; s++) {      // ascending trace order (c.4)
+        const long long r = base + s;
+        m += rep_met[r];
+        nn += rep_near[r];
+        g += rep_good[r];
+        const double w = rep_watts[r];
+        qw += w > 0 ? rep_good[r] / w : 0.0;     // QPS/W = goodput / avg provisioned W
+        ws += w;
+        for (int z = 0; z < nk; z++) mk[z] += rep_metk[r * kMaxSloSweep + z];
     }
     met[k] = m;
     near[k] = nn;
     good[k] = g;
+    qpw[k] = qw;
+    watts[k] = ws;
+    for (int z = 0; z < kMaxSloSweep; z++) metk[(long long)k * kMaxSloSweep + z] = z < nk ? mk[z] : 0;
+}
+
+// Max QPS at >= 80% SLO attainment per candidate, for the main SLO
+// (column 0) and each sweep SLO (columns 1..nk): the QPS point with the largest
+// qps among those with 5·Σmet ≥ 4·Σ_s R_s (integer test), else -1.
+__global__ void max80_kernel(const long long* met, const long long* metk, const double* qps, int C, int Q,
+                             int nk, long long n_req_total, int* out) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= C) return;
+    for (int z = 0; z <= nk; z++) {
+        int best = -1;
+        for (int q = 0; q < Q; q++) {
+            const long long m = z == 0 ? met[(long long)c * Q + q]
+                                       : metk[((long long)c * Q + q) * kMaxSloSweep + (z - 1)];
+            if (5 * m >= 4 * n_req_total && (best < 0 || qps[q] > qps[best])) best = q;
+        }
+        out[(long long)c * (1 + kMaxSloSweep) + z] = best;
+    }
+    for (int z = nk + 1; z <= kMaxSloSweep; z++) out[(long long)c * (1 + kMaxSloSweep) + z] = -1;
 }
 
 struct Key { long long met; int capsum; int idx; };
@@ -692,6 +731,18 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
     AL(ctx->d_good, CQ);
     AL(ctx->d_near, CQ);
     AL(ctx->d_argmax, n_qps);
+    AL(ctx->d_rep_metk, R_all * kMaxSloSweep);
+    AL(ctx->d_rep_watts, R_all);
+    AL(ctx->d_metk, CQ * kMaxSloSweep);
+    AL(ctx->d_qpw, CQ);
+    AL(ctx->d_watts, CQ);
+    AL(ctx->d_max80, (long long)C * (1 + kMaxSloSweep));
+    ctx->sweep = SloSweep{};
+    ctx->sweep.rep_met = ctx->d_rep_metk;
+    ctx->sweep.rep_watts = ctx->d_rep_watts;
+    ctx->sweep.capsum = ctx->d_capsum;
+    ctx->n_req_total = 0;
+    for (int s2 = 0; s2 < n_traces; s2++) ctx->n_req_total += traces[s2].n_req;
     AL(ctx->d_work, 4);
     if (flags & PADSIM_RECORDS) {
         for (auto& r : ctx->d_rec) AL(r, (size_t)R_all * std::max(Rmax, 1));
@@ -847,6 +898,9 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
         (dyn ? ctx->smem_dyn : ctx->smem_static) = P.smem_trace_bytes;
     }
 #undef AL
+    ctx->plan_static.sw = ctx->sweep;
+    ctx->plan_dyn.sw = ctx->sweep;
+    ctx->fplan.sw = ctx->sweep;
     CK(cudaDeviceSynchronize());
     ctx->planned = true;
     return PADSIM_OK;
@@ -919,7 +973,12 @@ int padsim_run(padsim_ctx* ctx, void* stream) {
     ctx->ev_recorded = true;
     const int CQ = ctx->C * ctx->Q;
     reduce_kernel<<<(CQ + 255) / 256, 256, 0, st>>>(ctx->d_rep_met, ctx->d_rep_near, ctx->d_rep_good,
-                                                    CQ, ctx->S, ctx->d_met, ctx->d_good, ctx->d_near);
+                                                    CQ, ctx->S, ctx->d_met, ctx->d_good, ctx->d_near,
+                                                    ctx->d_rep_metk, ctx->d_rep_watts, ctx->sweep.n,
+                                                    ctx->d_metk, ctx->d_qpw, ctx->d_watts);
+    CK(cudaGetLastError());
+    max80_kernel<<<(ctx->C + 127) / 128, 128, 0, st>>>(ctx->d_met, ctx->d_metk, ctx->d_qps, ctx->C, ctx->Q,
+                                                       ctx->sweep.n, ctx->n_req_total, ctx->d_max80);
     CK(cudaGetLastError());
     argmax_kernel<<<ctx->Q, 256, 0, st>>>(ctx->d_met, ctx->d_capsum, ctx->C, ctx->Q, ctx->d_argmax);
     CK(cudaGetLastError());
@@ -962,6 +1021,42 @@ int padsim_replay_kernel_ms(padsim_ctx* ctx, float* ms) {
     CK(cudaSetDevice(ctx->device));
     CK(cudaEventSynchronize(ctx->ev1));
     CK(cudaEventElapsedTime(ms, ctx->ev0, ctx->ev1));
+    return PADSIM_OK;
+}
+
+int padsim_set_slo_sweep(padsim_ctx* ctx, const padsim_slo* slos, int32_t n_slo) {
+    if (!ctx || n_slo < 0 || n_slo > kMaxSloSweep || (n_slo > 0 && !slos)) return PADSIM_EINVAL;
+    if (!ctx->planned) return fail(ctx, PADSIM_EINVAL, "set_slo_sweep before padsim_plan");
+    for (int k = 0; k < n_slo; k++)
+        if (!(slos[k].ttft_s > 0 && slos[k].tpot_s[0] > 0 && slos[k].tpot_s[1] > 0))
+            return fail(ctx, PADSIM_EINVAL, "SLOs must be > 0");
+    ctx->sweep.n = n_slo;
+    for (int k = 0; k < kMaxSloSweep; k++) {
+        ctx->sweep.ttft[k] = k < n_slo ? slos[k].ttft_s : 0.0;
+        ctx->sweep.tpot0[k] = k < n_slo ? slos[k].tpot_s[0] : 0.0;
+        ctx->sweep.tpot1[k] = k < n_slo ? slos[k].tpot_s[1] : 0.0;
+    }
+    ctx->plan_static.sw = ctx->sweep;
+    ctx->plan_dyn.sw = ctx->sweep;
+    ctx->fplan.sw = ctx->sweep;
+    return PADSIM_OK;
+}
+
+int padsim_fetch_extras(padsim_ctx* ctx, void* stream, int64_t* met_sweep, double* qps_per_watt,
+                        double* avg_watts, int32_t* max_qps80) {
+    if (!ctx) return PADSIM_EINVAL;
+    if (!ctx->planned) return fail(ctx, PADSIM_EINVAL, "no plan");
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t CQ = (size_t)ctx->C * ctx->Q;
+    if (met_sweep)
+        CK(cudaMemcpyAsync(met_sweep, ctx->d_metk, CQ * kMaxSloSweep * 8, cudaMemcpyDeviceToHost, st));
+    if (qps_per_watt) CK(cudaMemcpyAsync(qps_per_watt, ctx->d_qpw, CQ * 8, cudaMemcpyDeviceToHost, st));
+    if (avg_watts) CK(cudaMemcpyAsync(avg_watts, ctx->d_watts, CQ * 8, cudaMemcpyDeviceToHost, st));
+    if (max_qps80)
+        CK(cudaMemcpyAsync(max_qps80, ctx->d_max80, (size_t)ctx->C * (1 + kMaxSloSweep) * 4,
+                           cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
     return PADSIM_OK;
 }
 

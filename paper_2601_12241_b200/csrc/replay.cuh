@@ -84,6 +84,7 @@ struct ReplayResult {
     int met, near;
     double duration, goodput;
     long long events;
+    double watts;                  // time-weighted mean of Σ effective caps
 };
 
 template <int NMAX, bool DYN>
@@ -110,6 +111,10 @@ struct Replay {
     int flip_g, drain_pending, phase2;
     int w_th, w_tlo, w_tle, w_tlt;                       // TTFT window
     int w_ph, w_plo, w_ple0, w_plt0, w_ple1, w_plt1;     // TPOT window
+    int* metk;            // this replay's sweep counters (global, kMaxSloSweep)
+    int nk;
+    long long w_sum;
+    double w_acc, w_prev, a0t;
 
     __device__ Replay(const Plan& p, const TraceView& t, const Scratch& x) : P(p), T(t), X(x) {}
 
@@ -154,6 +159,10 @@ struct Replay {
         met += (ttft <= P.ttft_slo && tpot <= ts) ? 1 : 0;
         near += (fabs(ttft - P.ttft_slo) <= 1e-9 * P.ttft_slo || fabs(tpot - ts) <= 1e-9 * ts) ? 1 : 0;
         maxcomp = fmax(maxcomp, t);
+        for (int z = 0; z < nk; z++) {
+            const double tz = T.phase[i] ? P.sw.tpot1[z] : P.sw.tpot0[z];
+            if (ttft <= P.sw.ttft[z] && tpot <= tz) metk[z]++;
+        }
         if (DYN) {
             unsigned char f = (tpot <= P.tpot_slo0 ? 1 : 0) | (tpot < P.tpot_slo0 ? 2 : 0) |
                               (tpot <= P.tpot_slo1 ? 4 : 0) | (tpot < P.tpot_slo1 ? 8 : 0);
@@ -376,6 +385,13 @@ struct Replay {
             }
         }
         settle_t = PAD_INF;
+        if (t > a0t) {
+            w_acc = w_acc + (double)w_sum * (t - w_prev);
+            w_prev = t;
+        }
+        long long ws = 0;
+        for (int g = 0; g < N; g++) ws += G.eff[g];
+        w_sum = ws;
     }
 
     __device__ void flip(double) {
@@ -511,6 +527,12 @@ struct Replay {
             w_th = w_tlo = w_tle = w_tlt = 0;
             w_ph = w_plo = w_ple0 = w_plt0 = w_ple1 = w_plt1 = 0;
         }
+        nk = P.sw.n;
+        for (int z = 0; z < nk; z++) metk[z] = 0;
+        w_sum = P.sw.capsum[c];
+        a0t = R > 0 ? arr(0) : 0.0;
+        w_acc = 0.0;
+        w_prev = a0t;
         long long events = 0;
         int na = 0;
         double ta = R > 0 ? arr(0) : PAD_INF;
@@ -547,6 +569,8 @@ struct Replay {
         res.duration = R > 0 ? maxcomp - arr(0) : 0.0;
         res.goodput = res.duration > 0 ? (double)met / res.duration : 0.0;
         res.events = events;
+        if (R > 0) w_acc = w_acc + (double)w_sum * (maxcomp - w_prev);
+        res.watts = res.duration > 0 ? w_acc / res.duration : (double)w_sum;
         return res;
     }
 };
@@ -653,12 +677,14 @@ __global__ void __launch_bounds__(kThreads) replay_kernel(const __grid_constant_
             const int c = P.clist[u - q * P.n_clist];
             const long long r = ((long long)c * P.Q + q) * P.S + s;
             Replay<NMAX, DYN> rp(P, T, X);
+            rp.metk = P.sw.rep_met + r * kMaxSloSweep;
             const ReplayResult res = rp.run(c, q, P.rec_ttft ? r * P.Rmax : -1);
             P.rep_met[r] = res.met;
             P.rep_near[r] = res.near;
             P.rep_dur[r] = res.duration;
             P.rep_good[r] = res.goodput;
             P.rep_events[r] = res.events;
+            P.sw.rep_watts[r] = res.watts;
         }
         __syncthreads();   // every replay of the item done before the trace is replaced
     }

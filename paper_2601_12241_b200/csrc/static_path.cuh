@@ -106,6 +106,7 @@ struct FPlan {
     double* rep_good;
     long long* rep_events;
     double *rec_ttft, *rec_tpot, *rec_pe, *rec_comp, *rec_te;
+    SloSweep sw;
 };
 
 // ---------------------------------------------------------------------------
@@ -425,10 +426,21 @@ __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant_
         double tk = R > 0 ? recs[0].te : PAD_INF;
         long long inst = 0;
         auto set_tnext = [&](int wd, double v) { rset<kNW>(tnext, wd, v); };
+        int metk[kMaxSloSweep];
+#pragma unroll
+        for (int z = 0; z < kMaxSloSweep; z++) metk[z] = 0;
+        const int nk = P.sw.n;
         auto complete = [&](const SRec& rc, double t, double tpot) {
             completed++;
             const double ts = (rc.meta < 0) ? P.tpot_slo1 : P.tpot_slo0;
             met += (rc.ttft <= P.ttft_slo && tpot <= ts) ? 1 : 0;
+#pragma unroll
+            for (int z = 0; z < kMaxSloSweep; z++) {
+                if (z < nk) {
+                    const double tz = (rc.meta < 0) ? P.sw.tpot1[z] : P.sw.tpot0[z];
+                    metk[z] += (rc.ttft <= P.sw.ttft[z] && tpot <= tz) ? 1 : 0;
+                }
+            }
             near += (fabs(rc.ttft - P.ttft_slo) <= 1e-9 * P.ttft_slo || fabs(tpot - ts) <= 1e-9 * ts) ? 1 : 0;
             maxcomp = fmax(maxcomp, t);
             if (rb >= 0) {
@@ -591,6 +603,14 @@ __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant_
         P.rep_dur[r] = dur;
         P.rep_good[r] = dur > 0 ? (double)met / dur : 0.0;
         P.rep_events[r] = inst;
+        {   // static caps: provisioned power is Σ caps over [a_0, last completion]
+            const double cs = (double)P.sw.capsum[c];
+            const double acc = R > 0 ? cs * dur : 0.0;
+            P.sw.rep_watts[r] = dur > 0 ? acc / dur : cs;
+#pragma unroll
+            for (int z = 0; z < kMaxSloSweep; z++)
+                if (z < nk) P.sw.rep_met[r * kMaxSloSweep + z] = metk[z];
+        }
     }
 }
 

@@ -286,3 +286,45 @@ def test_cfg4_shape_sampled(pkg):
         assert rep["met"][c, q, s] == o["met"], (c, q, s)
         assert rep["duration"][c, q, s] == o["duration"]
         assert rep["goodput"][c, q, s] == o["goodput"]
+
+
+def test_slo_sweep_qps_per_watt_max80(pkg):
+    # Fig. 8 SLO scaling (0.5x-2x), Fig. 5b TPOT 25 ms, QPS/W,
+    # max QPS at >= 80 % attainment — static and dynamic candidates
+    xpd = [(4, 600, 600), (4, 750, 450), (4, 675, 525), (5, 600, 600), (3, 700, 550)]
+    role, cap = static_candidates(8, xpd + [(4, 600, 600), (4, 600, 600)])
+    pols = [policy("static")] * 5 + [policy("dyn-power", cooldown_s=2.0), policy("dyn-both")]
+    traces = [make_trace("lb", s, 600) for s in range(2)]
+    qps = [0.5, 1.0, 1.5, 2.0]
+    slos = [{"ttft": f * 1.0, "tpot": (f * 0.04, f * 0.04)} for f in (0.5, 2.0)] + \
+           [{"ttft": 1.0, "tpot": (0.025, 0.025)}]
+    ctx = pkg.Context(0)
+    try:
+        ctx.plan(traces, qps, DEFAULT_MODEL, role, cap, pols, DEFAULT_SLO, 4800)
+        ctx.set_slo_sweep(slos)
+        ctx.run()
+        res = ctx.fetch()
+        ex = ctx.fetch_extras()
+    finally:
+        ctx.close()
+    C, Q = role.shape[0], len(qps)
+    metk = np.zeros((C, Q, len(slos)), np.int64)
+    qpw = np.zeros((C, Q))
+    watts = np.zeros((C, Q))
+    for c in range(C):
+        for q in range(Q):
+            for s in range(2):
+                o = oracle.replay(DEFAULT_MODEL, role[c], cap[c], pols[c], 4800, DEFAULT_SLO, traces[s], qps[q])
+                metk[c, q] += oracle.met_for_slos(o["ttft"], o["tpot"], traces[s]["phase"], slos)
+                qpw[c, q] += o["qps_per_watt"]
+                watts[c, q] += o["avg_watts"]
+    assert np.array_equal(ex["met_sweep"], metk)
+    assert np.array_equal(ex["qps_per_watt"], qpw)
+    assert np.array_equal(ex["watts_sum"], watts)
+    nreq = sum(t["s_unit"].size for t in traces)
+    for c in range(C):
+        for k in range(len(slos) + 1):
+            m = res["met"][c] if k == 0 else metk[c, :, k - 1]
+            ok = [q for q in range(Q) if 5 * m[q] >= 4 * nreq]
+            want = max(ok, key=lambda q: qps[q]) if ok else -1
+            assert ex["max_qps80"][c, k] == want, (c, k)

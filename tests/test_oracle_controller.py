@@ -199,3 +199,45 @@ def test_dynamic_beats_static_on_phase_trace(model):
     base = _dyn_run(model, policy("static"), tr, 2.0, PHASE_SLO)["met"]
     both = _dyn_run(model, policy("dyn-both"), tr, 2.0, PHASE_SLO)["met"]
     assert both >= base
+
+
+def test_provisioned_power_integral(model):
+    # time-weighted mean of Σ effective caps; recompute from the budget log
+    tr = make_trace("phase", 7, 1500)
+    pol = policy("dyn-both", cooldown_s=2.0)
+    r = _dyn_run(model, pol, tr, 2.0, PHASE_SLO)
+    a0 = tr["s_unit"][0] * (1.0 / (2.0 * 8.0))
+    last = r["completion"].max()
+    pts = [(t, a) for t, typ, g, a, b in r["log"] if typ == oracle.LOG_BUDGET]
+    # budget records: (time, Σ eff) at t = 0 and after every settle
+    acc, prev, cur = 0.0, a0, pts[0][1]
+    for t, v in pts[1:]:
+        if t in [x[0] for x in r["log"] if x[1] == oracle.LOG_SETTLE]:
+            if t > a0:
+                acc += cur * (t - prev)
+                prev = t
+            cur = v
+    acc += cur * (last - prev)
+    assert r["avg_watts"] == pytest.approx(acc / (last - a0), rel=1e-12)
+    assert 8 * 400 <= r["avg_watts"] <= 4800
+    assert r["qps_per_watt"] == pytest.approx(r["goodput"] / r["avg_watts"], rel=1e-15)
+
+
+def test_static_provisioned_power_is_capsum(model):
+    role, cap = static_candidates(8, [(3, 700, 500)])
+    r = oracle.replay(model, role[0], cap[0], policy("static"), 4800, DEFAULT_SLO,
+                      make_trace("lb", 3, 300), 1.0)
+    assert r["avg_watts"] == pytest.approx(3 * 700 + 5 * 500, rel=1e-15)
+
+
+def test_met_for_slos_recount(model):
+    role, cap = static_candidates(8, [(4, 700, 500)])
+    tr = make_trace("lb", 8, 600)
+    r = oracle.replay(model, role[0], cap[0], policy("static"), 4800, DEFAULT_SLO, tr, 1.5)
+    slos = [{"ttft": f * 1.0, "tpot": (f * 0.04, f * 0.04)} for f in (0.5, 1.0, 2.0)] + \
+           [{"ttft": 1.0, "tpot": (0.025, 0.025)}]
+    got = oracle.met_for_slos(r["ttft"], r["tpot"], tr["phase"], slos)
+    for k, s in enumerate(slos):
+        assert got[k] == int(((r["ttft"] <= s["ttft"]) & (r["tpot"] <= s["tpot"][0])).sum())
+    assert got[1] == r["met"]
+    assert got[0] <= got[1] <= got[2]                       # monotone in SLO slack
