@@ -97,6 +97,7 @@ struct padsim_ctx {
     int fA_grid = 0, fC_grid = 0;
     size_t fC_smem = 0, fA_smem = 0;
     int fA_tb = kThreads;
+    bool fC_idx16 = false;
     int j_tb[2] = {kThreads, kThreads};
     long long* d_evA = nullptr;
     int n_evA = 0;
@@ -433,13 +434,14 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
     int *d_gx, *d_gcap, *d_ccc, *d_ccg, *d_ccy, *d_ccd;
     double* d_pe;
     SRec* d_rec;
+    SHot* d_hot;
     long long* d_evA;
     const long long GQS = (long long)G * Q * S;
     const size_t Rm = (size_t)F.Rmax;
 #define AL(p, n) do { int r_ = dalloc(ctx, &(p), (size_t)(n)); if (r_) return r_; } while (0)
     AL(d_gx, G); AL(d_gcap, (size_t)G * kNW); AL(d_ccc, NC); AL(d_ccg, NC); AL(d_ccy, NC);
     AL(d_ccd, (size_t)NC * kNW);
-    AL(d_rec, GQS * Rm); AL(d_pe, GQS * Rm); AL(d_evA, GQS);
+    AL(d_rec, GQS * Rm); AL(d_hot, GQS * Rm); AL(d_pe, GQS * Rm); AL(d_evA, GQS);
     CK(cudaMemcpy(d_gx, gx.data(), sizeof(int) * G, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(d_gcap, gcap.data(), sizeof(int) * G * kNW, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(d_ccc, cc_cand.data(), sizeof(int) * NC, cudaMemcpyHostToDevice));
@@ -447,7 +449,7 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
     CK(cudaMemcpy(d_ccy, cc_y.data(), sizeof(int) * NC, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(d_ccd, cc_dcap.data(), sizeof(int) * NC * kNW, cudaMemcpyHostToDevice));
     F.gx = d_gx; F.gcap = d_gcap; F.cc_cand = d_ccc; F.cc_group = d_ccg; F.cc_y = d_ccy; F.cc_dcap = d_ccd;
-    F.st_rec = d_rec; F.st_pe = d_pe; F.evA = d_evA;
+    F.st_rec = d_rec; F.st_hot = d_hot; F.st_pe = d_pe; F.evA = d_evA;
     ctx->d_evA = d_evA;
     ctx->n_evA = (int)GQS;
     // stage A scratch: one lane-interleaved slot per thread
@@ -482,13 +484,16 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
     {
         size_t off = 0;
         auto take = [&](size_t b) { size_t o = off; off += (b + 255) & ~(size_t)255; return o; };
-        take(Rm * 32 * sizeof(int));
+        const bool idx16 = Rm <= 32767;
+        ctx->fC_idx16 = idx16;
+        const size_t isz = idx16 ? 2 : 4;
+        take(Rm * 32 * isz);
         int maxo = 2;
         for (int s2 = 0; s2 < S; s2++) maxo = std::max(maxo, ctx->max_out[s2]);
         int wheel = 32;
         while (wheel < maxo) wheel <<= 1;        // finish steps lie in (step, step + out − 1]
         F.wheel = wheel;
-        F.c_off_heads = take((size_t)32 * kNW * wheel * sizeof(unsigned));
+        F.c_off_heads = take((size_t)32 * kNW * wheel * isz);
         F.c_off_bits = take((size_t)kNW * (wheel / 32) * 32 * sizeof(unsigned));
         F.c_warp_bytes = off;
         unsigned* d_wc;
@@ -501,7 +506,10 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
         F.bits_in_smem = wheel <= 256 ? 1 : 0;
         F.smem_trace = 0;
         ctx->fC_smem = wbytes + (F.bits_in_smem ? bbytes : 0);
-        const void* fn = ctxm ? (const void*)stageC_kernel<true> : (const void*)stageC_kernel<false>;
+        const void* fn = ctxm ? (idx16 ? (const void*)stageC_kernel<true, unsigned short>
+                                       : (const void*)stageC_kernel<true, unsigned>)
+                              : (idx16 ? (const void*)stageC_kernel<false, unsigned short>
+                                       : (const void*)stageC_kernel<false, unsigned>);
         CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->fC_smem));
         int occ = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, ctx->fC_smem));
@@ -959,10 +967,14 @@ int padsim_run(padsim_ctx* ctx, void* stream) {
         else stageA_kernel<32><<<ctx->fA_grid, 32, ctx->fA_smem, st>>>(F);
         CK(cudaGetLastError());
         CK(cudaEventRecord(ctx->evA, st));
-        if (ctx->model.decode_per_ctx_tok_s == 0.0)
-            stageC_kernel<false><<<ctx->fC_grid, kThreads, ctx->fC_smem, st>>>(F);
-        else
-            stageC_kernel<true><<<ctx->fC_grid, kThreads, ctx->fC_smem, st>>>(F);
+        const bool cm = ctx->model.decode_per_ctx_tok_s != 0.0;
+        if (ctx->fC_idx16) {
+            if (cm) stageC_kernel<true, unsigned short><<<ctx->fC_grid, kThreads, ctx->fC_smem, st>>>(F);
+            else stageC_kernel<false, unsigned short><<<ctx->fC_grid, kThreads, ctx->fC_smem, st>>>(F);
+        } else {
+            if (cm) stageC_kernel<true, unsigned><<<ctx->fC_grid, kThreads, ctx->fC_smem, st>>>(F);
+            else stageC_kernel<false, unsigned><<<ctx->fC_grid, kThreads, ctx->fC_smem, st>>>(F);
+        }
         CK(cudaGetLastError());
     } else {
         CK(cudaEventRecord(ctx->evA, st));

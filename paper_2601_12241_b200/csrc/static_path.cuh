@@ -53,7 +53,15 @@ __device__ __forceinline__ void radd(T (&a)[N], int i, T d) {
     for (int w = 0; w < N; w++) a[w] += (w == i) ? d : (T)0;
 }
 
-// One transfer-end record of the stage A → stage C stream (32 B).
+// Hot part of a transfer-end record (16 B): read sequentially at transfer ends.
+struct __align__(16) SHot {
+    double te;      // transfer end
+    int meta;       // out_tok | phase << 31
+    int id;         // request id
+};
+
+// One transfer-end record of the stage A → stage C stream (32 B), read when the
+// request completes.
 struct __align__(16) SRec {
     double te;      // transfer end (event time in stage C)
     double pe;      // prefill end (first token)
@@ -80,6 +88,7 @@ struct FPlan {
     const int* gcap;        // [G][kNW] their caps, P-id order
     // stage A → C stream, per (g, q, s) block of Rmax records in (te, id) order
     struct SRec* st_rec;
+    struct SHot* st_hot;    // same stream, hot 16-B part
     double* st_pe;          // prefill end, indexed by request id (stage A scratch)
     long long* evA;         // [G*Q*S] stage-A instants
     char* scrA;
@@ -181,6 +190,7 @@ __global__ void __launch_bounds__(TB) stageA_kernel(const __grid_constant__ FPla
     double* tpe = (double*)(wb + P.a_off_tpe) + lane;
     const long long sb = ((long long)(g * P.Q + q) * P.S + s) * P.Rmax;
     SRec* orec = P.st_rec + sb;
+    SHot* ohot = P.st_hot + sb;
     double* ope = P.st_pe + sb;
     const double inv_lam = 1.0 / (P.qps[q] * (double)P.N);
     const int x = P.gx[g];
@@ -249,6 +259,11 @@ __global__ void __launch_bounds__(TB) stageA_kernel(const __grid_constant__ FPla
                 rc.id = mid;
                 rc.meta = ot[mid] | ((int)ph[mid] << 31);
                 orec[k] = rc;
+                SHot hc;
+                hc.te = t;
+                hc.meta = rc.meta;
+                hc.id = mid;
+                ohot[k] = hc;
             }
             k++;
             tbusy--;
@@ -353,16 +368,18 @@ struct CWork {            // per-thread shared-memory SoA views (stride kThreads
 
 constexpr size_t kCWorkBytes = (size_t)kNW * kThreads * (2 * sizeof(double) + 8 * sizeof(int));
 constexpr size_t kCWorkCtxBytes = (size_t)kNW * kThreads * sizeof(long long);
-constexpr unsigned kMulti = 0x80000000u;
-
-template <bool CTX>
+// IDX: stream-index type of link[] and the wheel heads — uint16_t when
+// n_req ≤ 32767 (halves the scratch footprint and its DRAM/L2 traffic),
+// else uint32_t; the top bit flags "more members chained through link[]".
+template <bool CTX, typename IDX>
 __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant__ FPlan P) {
+    constexpr unsigned kMulti = sizeof(IDX) == 2 ? 0x8000u : 0x80000000u;
     extern __shared__ __align__(128) unsigned char smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     char* wb = P.scrC + ((size_t)blockIdx.x * kWarps + warp) * P.c_warp_bytes;
-    int* link = (int*)wb + lane;                                       // [k*32]
+    IDX* link = (IDX*)wb + lane;                                       // [k*32]
     const int Wh = P.wheel, Wm = P.wheel - 1, nwords = P.wheel >> 5;
-    unsigned* heads = (unsigned*)(wb + P.c_off_heads) + (size_t)lane * kNW * Wh;   // per lane
+    IDX* heads = (IDX*)(wb + P.c_off_heads) + (size_t)lane * kNW * Wh;   // per lane
     const int max_db = P.m.max_db;
     CWork W;
     unsigned* bits;
@@ -407,6 +424,7 @@ __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant_
         const long long r = ((long long)c * P.Q + q) * P.S + s;
         const long long sb = ((long long)(g * P.Q + q) * P.S + s) * P.Rmax;
         const SRec* recs = P.st_rec + sb;
+        const SHot* hots = P.st_hot + sb;
         const long long rb = P.rec_ttft ? r * P.Rmax : -1;
         double tnext[kNW];
         int ld[kNW];                       // routing load: active + pending (A13)
@@ -423,7 +441,9 @@ __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant_
         for (int z = 0; z < y * nwords; z++) bits[(size_t)z * bstride] = 0u;
         int completed = 0, met = 0, near = 0, k = 0;
         double maxcomp = -PAD_INF;
-        double tk = R > 0 ? recs[0].te : PAD_INF;
+        SHot nxt;                          // the next transfer end of the stream
+        if (R > 0) nxt = hots[0]; else { nxt.te = PAD_INF; nxt.meta = 0; nxt.id = 0; }
+        double tk = nxt.te;
         long long inst = 0;
         auto set_tnext = [&](int wd, double v) { rset<kNW>(tnext, wd, v); };
         int metk[kMaxSloSweep];
@@ -466,7 +486,7 @@ __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant_
                 W.stm[o] = sN;               // tnext[w] is rewritten by this instant's dispatch
                 if (sN == W.mfin[o]) {
                     const int b = sN & Wm;
-                    unsigned cur = heads[(size_t)w * Wh + b];
+                    unsigned cur = (unsigned)heads[(size_t)w * Wh + b];
                     int left = 0;
                     for (;;) {
                         const int kk = (int)(cur & ~kMulti);
@@ -476,7 +496,7 @@ __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant_
                         if (CTX) W.ctx[o] -= itk[rc.id];
                         left++;
                         if (!(cur & kMulti)) break;
-                        cur = (unsigned)link[(size_t)kk * 32];
+                        cur = (unsigned)link[(size_t)kk * 32];   // IDX → unsigned keeps the flag bit
                     }
                     unsigned* bw = bits + (size_t)w * nwords * bstride;
                     bw[(size_t)(b >> 5) * bstride] &= ~(1u << (b & 31));
@@ -501,18 +521,19 @@ __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant_
             // kind 4: transfer ends from the stream, (te, id) order
             while (tk == t) {
                 const int kk = k;
-                const SRec rc = recs[kk];
+                const SHot hc = nxt;
                 k++;
-                tk = k < R ? recs[k].te : PAD_INF;
-                if (rb >= 0) P.rec_te[rb + rc.id] = t;
-                if ((rc.meta & 0x7fffffff) == 1) { complete(rc, t, 0.0); continue; }   // S:280 D4
+                if (k < R) nxt = hots[k]; else nxt.te = PAD_INF;
+                tk = nxt.te;
+                if (rb >= 0) P.rec_te[rb + hc.id] = t;
+                if ((hc.meta & 0x7fffffff) == 1) { complete(recs[kk], t, 0.0); continue; }   // S:280 D4
                 int best = 0, bl = ld[0];
 #pragma unroll
                 for (int w = 1; w < kNW; w++) if (ld[w] < bl) { bl = ld[w]; best = w; }
                 radd<kNW, int>(ld, best, 1);
                 const int o = best * kThreads;
                 const int qn = W.ql[o];
-                if (qn == 0) W.qh[o] = kk; else link[(size_t)W.qt[o] * 32] = kk;
+                if (qn == 0) W.qh[o] = kk; else link[(size_t)W.qt[o] * 32] = (IDX)kk;
                 W.qt[o] = kk;
                 W.ql[o] = qn + 1;
                 touched |= 1u << best;
@@ -545,27 +566,27 @@ __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant_
                 const int step = W.stm[o];
                 int mf = W.mfin[o];
                 int h = W.qh[o];
-                unsigned* hw = heads + (size_t)w * Wh;
+                IDX* hw = heads + (size_t)w * Wh;
                 unsigned* bw = bits + (size_t)w * nwords * bstride;
                 while (n < max_db && qn > 0) {
                     const int kk = h;
                     qn--;
-                    if (qn > 0) h = link[(size_t)kk * 32];
-                    const int out = recs[kk].meta & 0x7fffffff;
+                    if (qn > 0) h = (int)link[(size_t)kk * 32];
+                    const int out = hots[kk].meta & 0x7fffffff;
                     const int fin = step + (out - 1);
                     const int b = fin & Wm;
                     unsigned* wp = bw + (size_t)(b >> 5) * bstride;
                     const unsigned bit = 1u << (b & 31);
                     const unsigned old = *wp;
                     if (old & bit) {                     // bucket occupied: chain
-                        link[(size_t)kk * 32] = (int)hw[b];
-                        hw[b] = (unsigned)kk | kMulti;
+                        link[(size_t)kk * 32] = hw[b];
+                        hw[b] = (IDX)((unsigned)kk | kMulti);
                     } else {
-                        hw[b] = (unsigned)kk;
+                        hw[b] = (IDX)kk;
                         *wp = old | bit;
                     }
                     n++;
-                    if (CTX) W.ctx[o] += itk[recs[kk].id];
+                    if (CTX) W.ctx[o] += itk[hots[kk].id];
                     mf = fin < mf ? fin : mf;
                     joined = true;
                 }

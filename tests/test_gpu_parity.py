@@ -328,3 +328,18 @@ def test_slo_sweep_qps_per_watt_max80(pkg):
             ok = [q for q in range(Q) if 5 * m[q] >= 4 * nreq]
             want = max(ok, key=lambda q: qps[q]) if ok else -1
             assert ex["max_qps80"][c, k] == want, (c, k)
+
+
+def test_long_trace_wide_index(pkg):
+    # n_req > 32767 switches stage C to 32-bit stream indices: same results as the oracle
+    role, cap = static_candidates(8, [(4, 700, 500), (3, 750, 475)])
+    pols = [policy("static")] * 2
+    traces = [make_trace("lb", 77, 40000)]
+    qps = [1.25, 2.5]
+    res, rep, rec = gpu_records(traces, qps, DEFAULT_MODEL, role, cap, pols, DEFAULT_SLO, 4800)
+    for c in range(2):
+        for q in range(2):
+            o = oracle.replay(DEFAULT_MODEL, role[c], cap[c], pols[c], 4800, DEFAULT_SLO, traces[0], qps[q])
+            assert rep["met"][c, q, 0] == o["met"]
+            assert np.array_equal(rec["completion"][c, q, 0], o["completion"])
+            assert np.array_equal(rec["tpot"][c, q, 0], o["tpot"])
