@@ -291,7 +291,7 @@ def test_cfg4_shape_sampled(pkg):
 def test_slo_sweep_qps_per_watt_max80(pkg):
     # Fig. 8 SLO scaling (0.5x-2x), Fig. 5b TPOT 25 ms, QPS/W,
     # max QPS at >= 80 % attainment — static and dynamic candidates
-    xpd = [(4, 600, 600), (4, 750, 450), (4, 675, 525), (5, 600, 600), (3, 700, 550)]
+    xpd = [(4, 600, 600), (4, 750, 450), (4, 675, 525), (5, 600, 600), (3, 700, 540)]
     role, cap = static_candidates(8, xpd + [(4, 600, 600), (4, 600, 600)])
     pols = [policy("static")] * 5 + [policy("dyn-power", cooldown_s=2.0), policy("dyn-both")]
     traces = [make_trace("lb", s, 600) for s in range(2)]
