@@ -343,3 +343,18 @@ def test_long_trace_wide_index(pkg):
             assert rep["met"][c, q, 0] == o["met"]
             assert np.array_equal(rec["completion"][c, q, 0], o["completion"])
             assert np.array_equal(rec["tpot"][c, q, 0], o["tpot"])
+
+
+def test_non_uniform_caps_within_pools(pkg):
+    # per-GPU cap vectors that are not pool-uniform ("as long as the
+    # aggregate GPU power adheres to its power limit, the power allocated to each GPU can vary")
+    # and interleaved role layouts: the ABI takes full vectors; both GPU paths = oracle
+    role = np.array([[0, 1, 0, 1, 0, 1, 1, 1], [1, 1, 0, 0, 0, 1, 0, 1], [0, 0, 0, 1, 1, 1, 1, 1]],
+                    np.uint8)
+    cap = np.array([[750, 450, 700, 500, 650, 400, 600, 550], [600, 400, 725, 700, 675, 500, 650, 450],
+                    [750, 725, 700, 400, 425, 450, 500, 550]], np.int32)
+    pols = [policy("static")] * 3
+    traces = [make_trace("lb", 90 + s, 300) for s in range(2)]
+    compare_records(traces, [0.75, 2.0], DEFAULT_MODEL, role, cap, pols, DEFAULT_SLO, 4800)
+    compare_records(traces[:1], [1.5], DEFAULT_MODEL, role, cap,
+                    [policy("dyn-both", cooldown_s=2.0)] * 3, DEFAULT_SLO, 4800)
