@@ -452,11 +452,13 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
     F.st_rec = d_rec; F.st_hot = d_hot; F.st_pe = d_pe; F.evA = d_evA;
     ctx->d_evA = d_evA;
     ctx->n_evA = (int)GQS;
-    // stage A scratch: one lane-interleaved slot per thread
+    // stage A scratch per warp: per-lane prompt rings (kNW workers + the KV-wait
+    // FIFO, R entries each) and lane-interleaved KV slots (128-thread CTAs)
     {
         size_t off = 0;
         auto take = [&](size_t b) { size_t o = off; off += (b + 255) & ~(size_t)255; return o; };
-        take(Rm * 32 * sizeof(int));
+        F.a_ring_lane = (size_t)(kNW + 1) * Rm;
+        F.a_off_ring = take((size_t)32 * F.a_ring_lane * sizeof(int));
         F.a_off_tte = take((size_t)PADSIM_MAX_SLOTS * 32 * sizeof(double));
         F.a_off_tid = take((size_t)PADSIM_MAX_SLOTS * 32 * sizeof(int));
         F.a_off_tpe = take((size_t)PADSIM_MAX_SLOTS * 32 * sizeof(double));
@@ -472,8 +474,9 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
         F.scrA = scr;
         ctx->fA_grid = (int)ctas;
         const size_t Rp = (Rm + 15) & ~(size_t)15;
-        const size_t tb_bytes = Rp * (8 + 8 + 4 + 4 + 1);
-        const size_t wbytes = tb == kThreads ? a_work_bytes<kThreads>() : a_work_bytes<32>();
+        const size_t tb_bytes = Rp * (8 + 8 + 4);
+        const size_t wbytes = tb == kThreads ? a_work_bytes<kThreads>() + a_slot_bytes<kThreads>()
+                                             : a_work_bytes<32>() + a_slot_bytes<32>();
         F.a_smem_trace = wbytes + tb_bytes <= 200 * 1024 ? 1 : 0;
         ctx->fA_smem = wbytes + (F.a_smem_trace ? tb_bytes : 0);
         const void* fa = tb == kThreads ? (const void*)stageA_kernel<kThreads> : (const void*)stageA_kernel<32>;

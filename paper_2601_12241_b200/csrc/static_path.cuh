@@ -92,7 +92,7 @@ struct FPlan {
     double* st_pe;          // prefill end, indexed by request id (stage A scratch)
     long long* evA;         // [G*Q*S] stage-A instants
     char* scrA;
-    size_t a_warp_bytes, a_off_tte, a_off_tid, a_off_tpe;
+    size_t a_warp_bytes, a_off_tte, a_off_tid, a_off_tpe, a_off_ring, a_ring_lane;
     int a_blocks_per_trace;   // stage A grid = S × this; a CTA never straddles traces
     int a_smem_trace;         // stage A stages its trace in shared memory (TMA bulk)
     // stage C
@@ -124,11 +124,19 @@ struct FPlan {
 // Next event time and routing key (outstanding tokens) per prefill worker are
 // register arrays; queue / batch / speedup state is a [field][worker][thread]
 // shared-memory SoA so handler bodies are shared across workers (run-time
-// worker index, convergent lanes).  The ≤ 32 in-flight transfers live in
-// lane-interleaved scratch with the earliest (te, id) cached in registers.
+// worker index, convergent lanes).  Prompt queues are per-worker ring arrays
+// of request ids (per-lane contiguous scratch), so forming a batch and ending
+// it read the next ≤ max_pb ids with independent loads instead of chasing a
+// linked list.  The ≤ 32 in-flight transfers are a small slot array (shared
+// memory for 32-thread CTAs) with the earliest (te, id) cached in registers.
 // ---------------------------------------------------------------------------
 template <int TB>
-__host__ __device__ constexpr size_t a_work_bytes() { return (size_t)kNW * TB * (sizeof(double) + 5 * sizeof(int)); }
+__host__ __device__ constexpr size_t a_work_bytes() { return (size_t)kNW * TB * (sizeof(double) + 4 * sizeof(int)); }
+template <int TB>
+__host__ __device__ constexpr size_t a_slot_bytes() {   // KV slots kept in smem for small CTAs
+    return TB == 32 ? (size_t)PADSIM_MAX_SLOTS * TB * (2 * sizeof(double) + sizeof(int)) : 0;
+}
+constexpr int kPre = 8;    // ids fetched per batch of independent loads
 
 template <int TB>
 __global__ void __launch_bounds__(TB) stageA_kernel(const __grid_constant__ FPlan P) {
@@ -139,36 +147,31 @@ __global__ void __launch_bounds__(TB) stageA_kernel(const __grid_constant__ FPla
     const int local = (blockIdx.x - s * P.a_blocks_per_trace) * TB + tid;
     const long long off = P.toff[s];
     const int R = P.nreq[s];
-    // the CTA's trace: staged once in shared memory by TMA bulk copies, read by
-    // every prefill group × QPS replay of the CTA
+    // the CTA's trace (arrival, kv, prompt tokens): staged once in shared memory
+    // by TMA bulk copies, read by every prefill group × QPS replay of the CTA
     const double* su;
     const double* kv;
     const int* it;
-    const int* ot;
-    const unsigned char* ph;
+    const int* ot = P.out_tok + off;
+    const unsigned char* ph = P.phase + off;
     if (P.a_smem_trace) {
         const int Rp = (R + 15) & ~15;
-        double* d_su = (double*)(smem + a_work_bytes<TB>());
+        double* d_su = (double*)(smem + a_work_bytes<TB>() + a_slot_bytes<TB>());
         double* d_kv = d_su + Rp;
         int* d_in = (int*)(d_kv + Rp);
-        int* d_ot = d_in + Rp;
-        unsigned char* d_ph = (unsigned char*)(d_ot + Rp);
         if (tid == 0) mbar_init(&bar, 1);
         __syncthreads();
         if (tid == 0 && Rp > 0) {
-            const unsigned b8 = (unsigned)Rp * 8u, b4 = (unsigned)Rp * 4u, b1 = (unsigned)Rp;
-            mbar_expect_tx(&bar, 2 * b8 + 2 * b4 + b1);
+            const unsigned b8 = (unsigned)Rp * 8u, b4 = (unsigned)Rp * 4u;
+            mbar_expect_tx(&bar, 2 * b8 + b4);
             bulk_g2s(d_su, P.s_unit + off, b8, &bar);
             bulk_g2s(d_kv, P.kv + off, b8, &bar);
             bulk_g2s(d_in, P.in_tok + off, b4, &bar);
-            bulk_g2s(d_ot, P.out_tok + off, b4, &bar);
-            bulk_g2s(d_ph, P.phase + off, b1, &bar);
         }
         if (Rp > 0) mbar_wait(&bar, 0);
-        su = d_su; kv = d_kv; it = d_in; ot = d_ot; ph = d_ph;
+        su = d_su; kv = d_kv; it = d_in;
     } else {
         su = P.s_unit + off; kv = P.kv + off; it = P.in_tok + off;
-        ot = P.out_tok + off; ph = P.phase + off;
     }
     if (local >= P.Q * P.n_groups) return;
     const int q = local / P.n_groups;
@@ -177,21 +180,33 @@ __global__ void __launch_bounds__(TB) stageA_kernel(const __grid_constant__ FPla
     const int n_sm = kNW * TB;
     double* Wsp = (double*)smem + tid;
     int* ib = (int*)(smem + (size_t)n_sm * sizeof(double));
-    int* Wqh = ib + 0 * n_sm + tid;
-    int* Wqt = ib + 1 * n_sm + tid;
-    int* Wql = ib + 2 * n_sm + tid;
-    int* Wbh = ib + 3 * n_sm + tid;
-    int* Wbn = ib + 4 * n_sm + tid;
+    int* Wqh = ib + 0 * n_sm + tid;     // ring index of the queue head
+    int* Wql = ib + 1 * n_sm + tid;     // queue length
+    int* Wbh = ib + 2 * n_sm + tid;     // ring index of the batch in service
+    int* Wbn = ib + 3 * n_sm + tid;     // its size
     const int lane = threadIdx.x & 31;
     char* wb = P.scrA + (size_t)(u >> 5) * P.a_warp_bytes;
-    int* link = (int*)wb + lane;
-    double* tte = (double*)(wb + P.a_off_tte) + lane;
-    int* tidb = (int*)(wb + P.a_off_tid) + lane;
-    double* tpe = (double*)(wb + P.a_off_tpe) + lane;
+    int* ring = (int*)(wb + P.a_off_ring) + (size_t)lane * P.a_ring_lane;   // [w*R + j], per lane
+    int* wring = ring + (size_t)kNW * R;                                     // KV-wait FIFO [j]
+    double* tte;
+    double* tpe;
+    int* tidb;
+    int ss;
+    if (TB == 32) {
+        unsigned char* sp = smem + a_work_bytes<TB>();
+        tte = (double*)sp + tid;
+        tpe = (double*)sp + PADSIM_MAX_SLOTS * TB + tid;
+        tidb = (int*)(sp + 2 * PADSIM_MAX_SLOTS * TB * sizeof(double)) + tid;
+        ss = TB;
+    } else {
+        tte = (double*)(wb + P.a_off_tte) + lane;
+        tidb = (int*)(wb + P.a_off_tid) + lane;
+        tpe = (double*)(wb + P.a_off_tpe) + lane;
+        ss = 32;
+    }
     const long long sb = ((long long)(g * P.Q + q) * P.S + s) * P.Rmax;
     SRec* orec = P.st_rec + sb;
     SHot* ohot = P.st_hot + sb;
-    double* ope = P.st_pe + sb;
     const double inv_lam = 1.0 / (P.qps[q] * (double)P.N);
     const int x = P.gx[g];
     const int slots = P.m.slots, max_pb = P.m.max_pb, pb_tokens = P.m.pb_tokens;
@@ -203,11 +218,11 @@ __global__ void __launch_bounds__(TB) stageA_kernel(const __grid_constant__ FPla
         const int o = w * TB;
         tnext[w] = PAD_INF;
         a0[w] = w < x ? 0 : 0x7fffffffffffffffLL;
-        Wqh[o] = kNoIdx; Wqt[o] = kNoIdx; Wql[o] = 0; Wbh[o] = 0; Wbn[o] = 0;
+        Wqh[o] = 0; Wql[o] = 0; Wbh[o] = 0; Wbn[o] = 0;
         Wsp[o] = w < x ? P.m.spre[P.gcap[g * kNW + w] - P.m.min_w] : 1.0;
     }
     auto set_tnext = [&](int wd, double v) { rset<kNW>(tnext, wd, v); };
-    int tbusy = 0, mk = 0, mid = 0, twh = kNoIdx, twt = kNoIdx, twl = 0;
+    int tbusy = 0, mk = 0, mid = 0, twh = 0, twl = 0;
     double mte = PAD_INF;
     int na = 0, k = 0;
     double ta = R > 0 ? su[0] * inv_lam : PAD_INF;
@@ -224,27 +239,40 @@ __global__ void __launch_bounds__(TB) stageA_kernel(const __grid_constant__ FPla
         for (unsigned m = bm; m; m &= m - 1) {
             const int w = __ffs(m) - 1;
             const int o = w * TB;
-            int i = Wbh[o];
+            const int* rw = ring + (size_t)w * R;
+            int j = Wbh[o];
             const int n = Wbn[o];
             long long dec = 0;
-            for (int z = 0; z < n; z++) {
-                const int nx = link[(size_t)i * 32];
-                dec += it[i];
-                if (tbusy < slots) {
-                    const double te = t + kv[i];
-                    tte[tbusy * 32] = te;
-                    tidb[tbusy * 32] = i;
-                    tpe[tbusy * 32] = t;
-                    if (tbusy == 0 || te < mte || (te == mte && i < mid)) { mte = te; mid = i; mk = tbusy; }
-                    tbusy++;
-                } else {
-                    ope[i] = t;                       // waits for a KV slot
-                    link[(size_t)i * 32] = kNoIdx;
-                    if (twl == 0) twh = i; else link[(size_t)twt * 32] = i;
-                    twt = i;
-                    twl++;
+            for (int z0 = 0; z0 < n; z0 += kPre) {
+                int ids[kPre];
+#pragma unroll
+                for (int z = 0; z < kPre; z++) {           // independent loads
+                    int jj = j + z;
+                    jj = jj >= R ? jj - R : jj;
+                    ids[z] = z0 + z < n ? rw[jj] : 0;
                 }
-                i = nx;
+#pragma unroll
+                for (int z = 0; z < kPre; z++) {
+                    if (z0 + z >= n) break;
+                    const int i = ids[z];
+                    dec += it[i];
+                    if (tbusy < slots) {
+                        const double te = t + kv[i];
+                        tte[tbusy * ss] = te;
+                        tidb[tbusy * ss] = i;
+                        tpe[tbusy * ss] = t;
+                        if (tbusy == 0 || te < mte || (te == mte && i < mid)) { mte = te; mid = i; mk = tbusy; }
+                        tbusy++;
+                    } else {                                  // waits for a KV slot (FIFO)
+                        int wj = twh + twl;
+                        wj = wj >= R ? wj - R : wj;
+                        wring[wj] = i;
+                        P.st_pe[sb + i] = t;
+                        twl++;
+                    }
+                }
+                j += kPre;
+                j = j >= R ? j - R : j;
             }
             radd<kNW, long long>(a0, w, -dec);
             set_tnext(w, PAD_INF);
@@ -254,7 +282,7 @@ __global__ void __launch_bounds__(TB) stageA_kernel(const __grid_constant__ FPla
             {
                 SRec rc;
                 rc.te = t;
-                rc.pe = tpe[mk * 32];
+                rc.pe = tpe[mk * ss];
                 rc.ttft = rc.pe - su[mid] * inv_lam;
                 rc.id = mid;
                 rc.meta = ot[mid] | ((int)ph[mid] << 31);
@@ -268,23 +296,23 @@ __global__ void __launch_bounds__(TB) stageA_kernel(const __grid_constant__ FPla
             k++;
             tbusy--;
             if (mk != tbusy) {
-                tte[mk * 32] = tte[tbusy * 32];
-                tidb[mk * 32] = tidb[tbusy * 32];
-                tpe[mk * 32] = tpe[tbusy * 32];
+                tte[mk * ss] = tte[tbusy * ss];
+                tidb[mk * ss] = tidb[tbusy * ss];
+                tpe[mk * ss] = tpe[tbusy * ss];
             }
             if (twl > 0) {
-                const int j = twh;
-                twh = link[(size_t)j * 32];
+                const int j = wring[twh];
+                twh = twh + 1 >= R ? 0 : twh + 1;
                 twl--;
-                tte[tbusy * 32] = t + kv[j];
-                tidb[tbusy * 32] = j;
-                tpe[tbusy * 32] = ope[j];
+                tte[tbusy * ss] = t + kv[j];
+                tidb[tbusy * ss] = j;
+                tpe[tbusy * ss] = P.st_pe[sb + j];
                 tbusy++;
             }
             mte = PAD_INF;
             for (int z = 0; z < tbusy; z++) {
-                const double e = tte[z * 32];
-                const int d = tidb[z * 32];
+                const double e = tte[z * ss];
+                const int d = tidb[z * ss];
                 if (e < mte || (e == mte && d < mid)) { mte = e; mid = d; mk = z; }
             }
         }
@@ -298,11 +326,11 @@ __global__ void __launch_bounds__(TB) stageA_kernel(const __grid_constant__ FPla
                 if (a0[w] < bl) { bl = a0[w]; best = w; }
             const int tin = it[i];
             radd<kNW, long long>(a0, best, (long long)tin);
-            link[(size_t)i * 32] = kNoIdx;
             const int o = best * TB;
             const int qn = Wql[o];
-            if (qn == 0) Wqh[o] = i; else link[(size_t)Wqt[o] * 32] = i;
-            Wqt[o] = i;
+            int jt = Wqh[o] + qn;
+            jt = jt >= R ? jt - R : jt;
+            ring[(size_t)best * R + jt] = i;
             Wql[o] = qn + 1;
             touched |= 1u << best;
             na++;
@@ -315,21 +343,36 @@ __global__ void __launch_bounds__(TB) stageA_kernel(const __grid_constant__ FPla
             const double tw = rget<kNW>(tnext, w);
             const int qn = Wql[o];
             if (tw != PAD_INF || qn == 0) continue;
+            const int* rw = ring + (size_t)w * R;
             const int h = Wqh[o];
-            long long tok = it[h];
-            int b = 1, j = h;
-            while (b < max_pb && b < qn) {
-                const int nx = link[(size_t)j * 32];
-                const long long tt = tok + it[nx];
-                if (tt > pb_tokens) break;
-                tok = tt;
-                j = nx;
-                b++;
+            long long tok = 0;
+            int b = 0;
+            bool stop = false;
+            int j = h;
+            while (!stop && b < qn && b < max_pb) {
+                int ids[kPre];
+#pragma unroll
+                for (int z = 0; z < kPre; z++) {           // independent loads
+                    int jj = j + z;
+                    jj = jj >= R ? jj - R : jj;
+                    ids[z] = b + z < qn ? rw[jj] : 0;
+                }
+#pragma unroll
+                for (int z = 0; z < kPre; z++) {
+                    if (stop || b >= qn || b >= max_pb) { stop = true; break; }
+                    const long long tt = tok + it[ids[z]];
+                    if (b > 0 && tt > pb_tokens) { stop = true; break; }   // head always admitted
+                    tok = tt;
+                    b++;
+                }
+                j += kPre;
+                j = j >= R ? j - R : j;
             }
             Wbh[o] = h;
             Wbn[o] = b;
             Wql[o] = qn - b;
-            if (qn > b) Wqh[o] = link[(size_t)j * 32];
+            int nh = h + b;
+            Wqh[o] = nh >= R ? nh - R : nh;
             set_tnext(w, t + ((double)tok / P.m.den[b]) / Wsp[o]);
         }
     }
