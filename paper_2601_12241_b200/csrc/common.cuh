@@ -76,7 +76,8 @@ struct Plan {
     size_t off_link, off_pe, off_mem, off_ordt, off_tst, off_tfl;   // per-warp offsets
     size_t off_tte, off_tti;           // KV-buffer slots (joint8 kernel)
     size_t off_heads, off_bits;        // decode timing wheel (joint8 kernel)
-    size_t off_wts, off_wtf;           // TTFT window: stamps + flags (joint8 kernel)
+    size_t off_wts, off_wtf;           // TTFT window: stamps + flags (joint kernel)
+    size_t off_jw;                     // per-GPU SoA in global scratch (joint kernel, NG = 64)
     int wheel;                         // wheel size: power of 2 ≥ max out_tok, ≥ 32
     size_t warp_bytes;
     int smem_trace;                    // stage the trace in shared memory (TMA bulk)

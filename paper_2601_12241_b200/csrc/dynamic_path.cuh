@@ -1,6 +1,10 @@
-// dynamic_path.cuh — joint replay for nodes of up to 8 simulated GPUs (rows
-// a4–a7, and a6 for dynamic candidates): prefill, KV buffer, decode and the
-// Algorithm 1 controller in one event loop per replay (one thread per replay).
+// dynamic_path.cuh — joint replay (rows a4–a7, and a6 for dynamic candidates):
+// prefill, KV buffer, decode and the Algorithm 1 controller in one event loop
+// per replay (one thread per replay).  NG = 8 (nodes of up to 8 simulated
+// GPUs, per-GPU next-event/routing keys in registers, per-GPU state in shared
+// memory) or NG = 64 (cfg 5: keys in shared memory with per-group-of-8 minima
+// in registers, refreshed lazily; per-GPU state in lane-interleaved global
+// scratch).
 //
 // Same semantics as replay.cuh (DESIGN.md §3 c.2/c.3), different storage:
 //  * per-GPU next event time and the two routing keys (prefill: outstanding
@@ -23,10 +27,148 @@
 
 namespace padsim {
 
-constexpr int kJG = 8;     // GPU slots (N ≤ 8)
+constexpr int kJG = 8;     // GPU slots of the small-node variant (N ≤ 8)
 constexpr int kIntMax = 0x7fffffff;
 
-// smem SoA, stride TB (threads per CTA)
+template <int NG> struct MaskT { using type = unsigned; };
+template <> struct MaskT<64> { using type = unsigned long long; };
+__device__ __forceinline__ int mffs(unsigned m) { return __ffs(m) - 1; }
+__device__ __forceinline__ int mffs(unsigned long long m) { return __ffsll((long long)m) - 1; }
+
+// Per-GPU next event time + routing keys (kp: prefill outstanding tokens, kd:
+// decode active+pending; INT_MAX = not eligible).
+template <int NG> struct WTab;
+
+template <> struct WTab<8> {                // register arrays, predicated selects
+    double tn[8];
+    int kp[8], kd[8];
+    __device__ __forceinline__ void init(int g, int role) {
+#pragma unroll
+        for (int v = 0; v < 8; v++) if (v == g) { tn[v] = PAD_INF; kp[v] = role == 0 ? 0 : kIntMax; kd[v] = role == 1 ? 0 : kIntMax; }
+    }
+    __device__ __forceinline__ double tmin(double cur) {
+#pragma unroll
+        for (int g = 0; g < 8; g++) cur = tn[g] < cur ? tn[g] : cur;
+        return cur;
+    }
+    __device__ __forceinline__ unsigned eq(double t) {
+        unsigned m = 0;
+#pragma unroll
+        for (int g = 0; g < 8; g++) if (tn[g] == t) m |= 1u << g;
+        return m;
+    }
+    __device__ __forceinline__ void set_t(int gd, double v) {
+#pragma unroll
+        for (int g = 0; g < 8; g++) tn[g] = (g == gd) ? v : tn[g];
+    }
+    __device__ __forceinline__ double get_t(int gd) const {
+        double v = tn[0];
+#pragma unroll
+        for (int g = 1; g < 8; g++) v = (g == gd) ? tn[g] : v;
+        return v;
+    }
+    __device__ __forceinline__ int arg_p() {
+        int best = 0, bl = kp[0];
+#pragma unroll
+        for (int g = 1; g < 8; g++) if (kp[g] < bl) { bl = kp[g]; best = g; }
+        return best;
+    }
+    __device__ __forceinline__ int arg_d() {
+        int best = 0, bl = kd[0];
+#pragma unroll
+        for (int g = 1; g < 8; g++) if (kd[g] < bl) { bl = kd[g]; best = g; }
+        return best;
+    }
+    __device__ __forceinline__ void add_p(int gd, int d) {
+#pragma unroll
+        for (int g = 0; g < 8; g++) kp[g] += (g == gd) ? d : 0;
+    }
+    __device__ __forceinline__ void add_d(int gd, int d) {
+#pragma unroll
+        for (int g = 0; g < 8; g++) kd[g] += (g == gd) ? d : 0;
+    }
+    __device__ __forceinline__ void set_p(int gd, int v) {
+#pragma unroll
+        for (int g = 0; g < 8; g++) kp[g] = (g == gd) ? v : kp[g];
+    }
+    __device__ __forceinline__ void set_d(int gd, int v) {
+#pragma unroll
+        for (int g = 0; g < 8; g++) kd[g] = (g == gd) ? v : kd[g];
+    }
+};
+
+template <> struct WTab<64> {               // memory arrays + lazily refreshed group minima
+    double* tn; int* kp; int* kd; int st;   // [g*st]
+    double gt[8];
+    int gpv[8], gpi[8], gdv[8], gdi[8];
+    unsigned dt, dp, dd;                    // dirty groups
+    __device__ __forceinline__ void init(int g, int role) {
+        tn[g * st] = PAD_INF;
+        kp[g * st] = role == 0 ? 0 : kIntMax;
+        kd[g * st] = role == 1 ? 0 : kIntMax;
+        dt = dp = dd = 0xffu;
+    }
+    __device__ __forceinline__ void refresh_t() {
+        for (unsigned m = dt; m; m &= m - 1) {
+            const int gi = __ffs(m) - 1;
+            double v = PAD_INF;
+            for (int j = 0; j < 8; j++) { const double x = tn[(gi * 8 + j) * st]; v = x < v ? x : v; }
+#pragma unroll
+            for (int z = 0; z < 8; z++) gt[z] = (z == gi) ? v : gt[z];
+        }
+        dt = 0;
+    }
+    __device__ __forceinline__ double tmin(double cur) {
+        refresh_t();
+#pragma unroll
+        for (int z = 0; z < 8; z++) cur = gt[z] < cur ? gt[z] : cur;
+        return cur;
+    }
+    __device__ __forceinline__ unsigned long long eq(double t) {
+        unsigned long long m = 0;
+#pragma unroll
+        for (int z = 0; z < 8; z++) {
+            if (gt[z] == t) {
+                for (int j = 0; j < 8; j++)
+                    if (tn[(z * 8 + j) * st] == t) m |= 1ull << (z * 8 + j);
+            }
+        }
+        return m;
+    }
+    __device__ __forceinline__ void set_t(int g, double v) { tn[g * st] = v; dt |= 1u << (g >> 3); }
+    __device__ __forceinline__ double get_t(int g) const { return tn[g * st]; }
+    __device__ __forceinline__ void refresh_k(int* k, unsigned& dirty, int (&gv)[8], int (&gi)[8]) {
+        for (unsigned m = dirty; m; m &= m - 1) {
+            const int z = __ffs(m) - 1;
+            int bv = k[(z * 8) * st], bi = z * 8;
+            for (int j = 1; j < 8; j++) { const int x = k[(z * 8 + j) * st]; if (x < bv) { bv = x; bi = z * 8 + j; } }
+#pragma unroll
+            for (int y = 0; y < 8; y++) { gv[y] = (y == z) ? bv : gv[y]; gi[y] = (y == z) ? bi : gi[y]; }
+        }
+        dirty = 0;
+    }
+    __device__ __forceinline__ int arg_p() {
+        refresh_k(kp, dp, gpv, gpi);
+        int best = gpi[0], bl = gpv[0];
+#pragma unroll
+        for (int z = 1; z < 8; z++) if (gpv[z] < bl) { bl = gpv[z]; best = gpi[z]; }
+        return best;
+    }
+    __device__ __forceinline__ int arg_d() {
+        refresh_k(kd, dd, gdv, gdi);
+        int best = gdi[0], bl = gdv[0];
+#pragma unroll
+        for (int z = 1; z < 8; z++) if (gdv[z] < bl) { bl = gdv[z]; best = gdi[z]; }
+        return best;
+    }
+    __device__ __forceinline__ void add_p(int g, int d) { kp[g * st] += d; dp |= 1u << (g >> 3); }
+    __device__ __forceinline__ void add_d(int g, int d) { kd[g * st] += d; dd |= 1u << (g >> 3); }
+    __device__ __forceinline__ void set_p(int g, int v) { kp[g * st] = v; dp |= 1u << (g >> 3); }
+    __device__ __forceinline__ void set_d(int g, int v) { kd[g * st] = v; dd |= 1u << (g >> 3); }
+};
+
+// per-GPU SoA: shared memory with stride TB (NG = 8) or lane-interleaved
+// global scratch with stride 32 (NG = 64); field[g * ws]
 struct JWork {
     double* tseg; double* L;
     int* a0;    // P: outstanding tokens | D: active count
@@ -41,33 +183,35 @@ __host__ __device__ constexpr size_t j_work_bytes() { return (size_t)kJG * TB * 
 
 enum : unsigned char { JF_DRAIN = 1, JF_DIRTY = 2 };
 
-template <int TB>
+template <typename Mask>
 struct JCtlView {
     const JWork* W;
-    unsigned pmask;
+    Mask pmask;
+    int ws;
     __device__ int role(int g) const { return ((pmask >> g) & 1u) ? 0 : 1; }
-    __device__ bool draining(int g) const { return (W->fl[g * TB] & JF_DRAIN) != 0; }
+    __device__ bool draining(int g) const { return (W->fl[g * ws] & JF_DRAIN) != 0; }
     __device__ int target(int g) const {
-        const int r = W->rse[g * TB];
-        return r > 0 ? r : W->cmd[g * TB];
+        const int r = W->rse[g * ws];
+        return r > 0 ? r : W->cmd[g * ws];
     }
     __device__ long long load(int g) const {
-        const int o = g * TB;
+        const int o = g * ws;
         return ((pmask >> g) & 1u) ? (long long)W->a0[o] : (long long)W->a0[o] + W->ql[o];
     }
 };
 
-template <bool DYN, int TB>
+template <bool DYN, int TB, int NG>
 struct JReplay {
+    using Mask = typename MaskT<NG>::type;
     const Plan& P;
     const TraceView& T;
     const Scratch& X;
     const JWork& W;
+    int ws;              // stride of the per-GPU SoA
     int N, R, max_db;
     double inv_lam;
-    double tnext[kJG];
-    int kp[kJG], kd[kJG];
-    unsigned pmask, dmask;
+    WTab<NG> tab;
+    Mask pmask, dmask;
     // KV buffer: slots in lane-interleaved scratch
     double* tte;
     int* tti;
@@ -87,7 +231,7 @@ struct JReplay {
     long long tick_k;
     int flip_g, drain_pending, phase2;
     int w_th, w_tlo, w_tle, w_tlt, w_ph, w_plo, w_ple0, w_plt0, w_ple1, w_plt1;
-    unsigned touched;
+    Mask touched;
     // SLO sweep + provisioned power (time-weighted Σ effective caps)
     int* metk;            // this replay's sweep counters (global, kMaxSloSweep)
     int nk;
@@ -100,25 +244,10 @@ struct JReplay {
     __device__ __forceinline__ int& LNK(int i) { return X.link[(size_t)i * 32]; }
     __device__ __forceinline__ double& PE(int i) { return X.pe[(size_t)i * 32]; }
     __device__ __forceinline__ double arr(int i) const { return T.s_unit[i] * inv_lam; }
-    // register arrays, run-time index: predicated selects only
-    __device__ __forceinline__ void set_tnext(int gd, double v) {
-#pragma unroll
-        for (int g = 0; g < kJG; g++) tnext[g] = (g == gd) ? v : tnext[g];
-    }
-    __device__ __forceinline__ double get_tnext(int gd) const {
-        double v = tnext[0];
-#pragma unroll
-        for (int g = 1; g < kJG; g++) v = (g == gd) ? tnext[g] : v;
-        return v;
-    }
-    __device__ __forceinline__ void add_kp(int gd, int d) {
-#pragma unroll
-        for (int g = 0; g < kJG; g++) kp[g] += (g == gd) ? d : 0;
-    }
-    __device__ __forceinline__ void add_kd(int gd, int d) {
-#pragma unroll
-        for (int g = 0; g < kJG; g++) kd[g] += (g == gd) ? d : 0;
-    }
+    __device__ __forceinline__ void set_tnext(int g, double v) { tab.set_t(g, v); }
+    __device__ __forceinline__ double get_tnext(int g) const { return tab.get_t(g); }
+    __device__ __forceinline__ void add_kp(int g, int d) { tab.add_p(g, d); }
+    __device__ __forceinline__ void add_kd(int g, int d) { tab.add_d(g, d); }
     __device__ __forceinline__ double bnd(int o, int s) const {
         return W.tseg[o] + (double)(s - W.st0[o]) * W.L[o];
     }
@@ -163,35 +292,31 @@ struct JReplay {
 
     // A8: least outstanding non-draining prefill GPU, lowest id
     __device__ void route_prompt(int i) {
-        int best = 0, bl = kp[0];
-#pragma unroll
-        for (int g = 1; g < kJG; g++) if (kp[g] < bl) { bl = kp[g]; best = g; }
+        const int best = tab.arg_p();
         const int tin = T.in_tok[i];
         add_kp(best, tin);
-        const int o = best * TB;
+        const int o = best * ws;
         W.a0[o] += tin;
         LNK(i) = kNoIdx;
         const int qn = W.ql[o];
         if (qn == 0) W.qh[o] = i; else LNK(W.qt[o]) = i;
         W.qt[o] = i;
         W.ql[o] = qn + 1;
-        touched |= 1u << best;
+        touched |= ((Mask)1) << best;
     }
 
     // A13/A14: fewest active+pending non-draining decode GPU, lowest id; joins
     // at the first step boundary at or after t
-    __device__ void route_decode(int i, double t, unsigned bm_now) {
-        int best = 0, bl = kd[0];
-#pragma unroll
-        for (int g = 1; g < kJG; g++) if (kd[g] < bl) { bl = kd[g]; best = g; }
+    __device__ void route_decode(int i, double t, Mask bm_now) {
+        const int best = tab.arg_d();
         add_kd(best, 1);
-        const int o = best * TB;
+        const int o = best * ws;
         LNK(i) = kNoIdx;
         const int qn = W.ql[o];
         if (qn == 0) W.qh[o] = i; else LNK(W.qt[o]) = i;
         W.qt[o] = i;
         W.ql[o] = qn + 1;
-        touched |= 1u << best;
+        touched |= ((Mask)1) << best;
         const int na = W.a0[o];
         if (na > 0 && !((bm_now >> best) & 1u) && na < max_db && qn == 0) {
             const int s = first_bnd_ge(o, t);
@@ -200,7 +325,7 @@ struct JReplay {
     }
 
     __device__ void batch_end(int g, double t) {
-        const int o = g * TB;
+        const int o = g * ws;
         int i = W.b0[o];
         const int n = W.b1[o];
         int dec = 0;
@@ -241,7 +366,7 @@ struct JReplay {
     // a timing wheel: bucket (finish step mod Wh) chains its members through
     // link[]; an occupancy bitmap gives the next finish step.
     __device__ bool boundary(int g, double t) {
-        const int o = g * TB;
+        const int o = g * ws;
         const int s = W.b1[o];
         W.b0[o] = s;
         set_tnext(g, PAD_INF);
@@ -276,7 +401,7 @@ struct JReplay {
         return true;
     }
 
-    __device__ void transfer_end(double t, unsigned bm_now) {
+    __device__ void transfer_end(double t, Mask bm_now) {
         const int i = mid;
         tbusy--;
         if (mk != tbusy) { tte[mk * 32] = tte[tbusy * 32]; tti[mk * 32] = tti[tbusy * 32]; }
@@ -300,7 +425,7 @@ struct JReplay {
     }
 
     __device__ void dispatch_prefill(int g, double t) {
-        const int o = g * TB;
+        const int o = g * ws;
         const int qn = W.ql[o];
         if (get_tnext(g) != PAD_INF || qn == 0) return;
         const int h = W.qh[o];
@@ -322,7 +447,7 @@ struct JReplay {
     }
 
     __device__ void dispatch_decode(int g, double t, bool at_bnd, bool changed) {
-        const int o = g * TB;
+        const int o = g * ws;
         int n = W.a0[o];
         if (n > 0 && !at_bnd) {
             if (get_tnext(g) != t) return;      // mid-step
@@ -385,7 +510,7 @@ struct JReplay {
     // ---- dynamic ---------------------------------------------------------
     __device__ void settle(double t) {
         for (int g = 0; g < N; g++) {
-            const int o = g * TB;
+            const int o = g * ws;
             bool changed = false;
             int e = W.eff[o], c = W.cmd[o];
             const int r = W.rse[o];
@@ -406,24 +531,22 @@ struct JReplay {
             w_acc = w_acc + (double)w_sum * (t - w_prev);
             w_prev = t;
         }
-        long long ws = 0;
-        for (int g = 0; g < N; g++) ws += W.eff[g * TB];
-        w_sum = ws;
+        long long wsum_ = 0;
+        for (int g = 0; g < N; g++) wsum_ += W.eff[g * ws];
+        w_sum = wsum_;
     }
 
     __device__ void flip() {
-        const int g = flip_g, o = g * TB;
+        const int g = flip_g, o = g * ws;
         const bool to_p = ((dmask >> g) & 1u) != 0;
-        pmask ^= 1u << g;
-        dmask ^= 1u << g;
+        pmask ^= ((Mask)1) << g;
+        dmask ^= ((Mask)1) << g;
         W.fl[o] = 0;
         W.a0[o] = 0; W.ql[o] = 0; W.b0[o] = 0; W.b1[o] = 0; W.st0[o] = 0;
         W.mfin[o] = kIntMax; W.ctx[o] = 0;
         set_tnext(g, PAD_INF);
-#pragma unroll
-        for (int v = 0; v < kJG; v++) {
-            if (v == g) { kp[v] = to_p ? 0 : kIntMax; kd[v] = to_p ? kIntMax : 0; }
-        }
+        tab.set_p(g, to_p ? 0 : kIntMax);
+        tab.set_d(g, to_p ? kIntMax : 0);
         drain_pending = 0;
         flip_g = -1;
         flip_t = PAD_INF;
@@ -431,7 +554,7 @@ struct JReplay {
 
     // returns 0: cooldown not elapsed (guards not evaluated), 1: evaluated, no
     // move (none or saturated), 2: a move was made
-    __device__ int tick(double t, unsigned bm_now) {
+    __device__ int tick(double t, Mask bm_now) {
         int acted = 0;
         if ((t - last_move) > pol.cooldown_s) {
             acted = 1;
@@ -455,17 +578,17 @@ struct JReplay {
             sg.tpot_gt = (phase2 ? w_ple1 : w_ple0) < kq;
             sg.tpot_lt = (phase2 ? w_plt1 : w_plt0) >= kq;
             int qp = 0;
-            for (unsigned m = pmask; m; m &= m - 1) qp += W.ql[(__ffs(m) - 1) * TB];
+            for (Mask m = pmask; m; m &= m - 1) qp += W.ql[mffs(m) * ws];
             sg.q_prefill = qp;
-            int newcap[kJG];
+            int newcap[NG];
             int gsel, dir;
-            JCtlView<TB> view{&W, pmask};
+            JCtlView<Mask> view{&W, pmask, ws};
             const int act = ctl_step(pol, P.m.min_w, P.m.max_w, P.B, N, view, drain_pending != 0,
                                      last_move, t, sg, newcap, &gsel, &dir);
             if (act == ACT_MOVE_POWER || act == ACT_MOVE_GPU) {
                 last_move = t;
                 if (act == ACT_MOVE_GPU) {
-                    const int g = gsel, o = g * TB;
+                    const int g = gsel, o = g * ws;
                     W.fl[o] |= JF_DRAIN;
                     drain_pending = 1;
                     flip_g = g;
@@ -473,8 +596,7 @@ struct JReplay {
                     const int n = W.ql[o];
                     W.ql[o] = 0;
                     if ((pmask >> g) & 1u) {
-#pragma unroll
-                        for (int v = 0; v < kJG; v++) if (v == g) kp[v] = kIntMax;
+                        tab.set_p(g, kIntMax);
                         for (int z = 0; z < n; z++) {
                             const int nx = LNK(i);
                             W.a0[o] -= T.in_tok[i];
@@ -482,8 +604,7 @@ struct JReplay {
                             i = nx;
                         }
                     } else {
-#pragma unroll
-                        for (int v = 0; v < kJG; v++) if (v == g) kd[v] = kIntMax;
+                        tab.set_d(g, kIntMax);
                         for (int z = 0; z < n; z++) {
                             const int nx = LNK(i);
                             route_decode(i, t, bm_now);
@@ -492,7 +613,7 @@ struct JReplay {
                     }
                 }
                 for (int g = 0; g < N; g++) {
-                    const int o = g * TB;
+                    const int o = g * ws;
                     const int tg = newcap[g];
                     if (tg < W.cmd[o]) W.cmd[o] = tg;
                     else if (tg > W.cmd[o]) W.rse[o] = tg;
@@ -562,15 +683,13 @@ struct JReplay {
         const int* ccap = P.cap + (size_t)c * N;
         pmask = dmask = 0;
 #pragma unroll
-        for (int g = 0; g < kJG; g++) {
-            const int o = g * TB;
+        for (int g = 0; g < NG; g++) {
+            const int o = g * ws;
             const bool on = g < N;
             const int r = on ? crole[g] : 2;
-            if (r == 0) pmask |= 1u << g;
-            if (r == 1) dmask |= 1u << g;
-            tnext[g] = PAD_INF;
-            kp[g] = r == 0 ? 0 : kIntMax;
-            kd[g] = r == 1 ? 0 : kIntMax;
+            if (r == 0) pmask |= ((Mask)1) << g;
+            if (r == 1) dmask |= ((Mask)1) << g;
+            tab.init(g, r);
             W.tseg[o] = 0.0; W.L[o] = 1.0;
             W.a0[o] = 0; W.qh[o] = kNoIdx; W.qt[o] = kNoIdx; W.ql[o] = 0;
             W.b0[o] = 0; W.b1[o] = 0; W.st0[o] = 0; W.mfin[o] = kIntMax;
@@ -578,7 +697,7 @@ struct JReplay {
             W.rse[o] = 0; W.ctx[o] = 0; W.fl[o] = 0;
         }
         Wh = P.wheel; Wm = Wh - 1; nwords = Wh >> 5;
-        for (int z = 0; z < kJG * nwords; z++) bits[(size_t)z * 32] = 0u;
+        for (int z = 0; z < N * nwords; z++) bits[(size_t)z * 32] = 0u;
         tbusy = 0; mk = 0; mid = 0; twh = twt = kNoIdx; twl = 0;
         mte = PAD_INF;
         completed = 0; met = 0; near = 0;
@@ -605,9 +724,7 @@ struct JReplay {
         int na = 0;
         double ta = R > 0 ? arr(0) : PAD_INF;
         while (completed < R) {
-            double t = ta < mte ? ta : mte;
-#pragma unroll
-            for (int g = 0; g < kJG; g++) t = tnext[g] < t ? tnext[g] : t;
+            double t = tab.tmin(ta < mte ? ta : mte);
             if (DYN) {
                 t = tick_t < t ? tick_t : t;
                 t = settle_t < t ? settle_t : t;
@@ -619,15 +736,13 @@ struct JReplay {
                 if (settle_t == t) settle(t);
                 if (flip_t == t) flip();
             }
-            unsigned bm = 0;
-#pragma unroll
-            for (int g = 0; g < kJG; g++) if (tnext[g] == t) bm |= 1u << g;
-            const unsigned bp = bm & pmask, bd = bm & dmask;
-            for (unsigned m = bp; m; m &= m - 1) batch_end(__ffs(m) - 1, t);
-            unsigned chg = 0;
-            for (unsigned m = bd; m; m &= m - 1) {
-                const int g = __ffs(m) - 1;
-                if (boundary(g, t)) chg |= 1u << g;
+            const Mask bm = tab.eq(t);
+            const Mask bp = bm & pmask, bd = bm & dmask;
+            for (Mask m = bp; m; m &= m - 1) batch_end(mffs(m), t);
+            Mask chg = 0;
+            for (Mask m = bd; m; m &= m - 1) {
+                const int g = mffs(m);
+                if (boundary(g, t)) chg |= ((Mask)1) << g;
             }
             while (tbusy > 0 && mte == t) transfer_end(t, bd);
             while (ta == t) {
@@ -638,23 +753,23 @@ struct JReplay {
             }
             int tick_outcome = 2;
             if (DYN && tick_t == t) tick_outcome = tick(t, bd);
-            for (unsigned m = bm | touched; m; m &= m - 1) {
-                const int g = __ffs(m) - 1;
+            for (Mask m = bm | touched; m; m &= m - 1) {
+                const int g = mffs(m);
                 if ((pmask >> g) & 1u) dispatch_prefill(g, t);
                 else dispatch_decode(g, t, (bd >> g) & 1u, (chg >> g) & 1u);
             }
             if (DYN && flip_g >= 0 && flip_t == PAD_INF) {
-                const int o = flip_g * TB;
+                const int o = flip_g * ws;
                 const bool empty = ((pmask >> flip_g) & 1u)
                                        ? (get_tnext(flip_g) == PAD_INF && W.ql[o] == 0)
                                        : (W.a0[o] == 0 && W.ql[o] == 0);
                 if (empty) flip_t = t + pol.reassign_s;
             }
             if (DYN && tick_outcome < 2) {
-                double ne = fmin(fmin(ta, mte), fmin(settle_t, flip_t));
-#pragma unroll
-                for (int g = 0; g < kJG; g++) ne = fmin(ne, tnext[g]);
-                skip_ticks(tick_outcome, ne);
+                double ne = ta < mte ? ta : mte;
+                ne = settle_t < ne ? settle_t : ne;
+                ne = flip_t < ne ? flip_t : ne;
+                skip_ticks(tick_outcome, tab.tmin(ne));
             }
         }
         ReplayResult res;
@@ -670,12 +785,14 @@ struct JReplay {
 };
 
 // CTAs bound to one trace (s = blockIdx.x mod S); warps pull 32-replay items.
-template <bool DYN, int TB>
-__global__ void __launch_bounds__(TB) joint8_kernel(const __grid_constant__ Plan P) {
+template <bool DYN, int TB, int NG>
+__global__ void __launch_bounds__(TB) joint_kernel(const __grid_constant__ Plan P) {
     extern __shared__ __align__(128) unsigned char smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    char* wbase = P.scratch + ((size_t)blockIdx.x * (TB / 32) + warp) * P.warp_bytes;
     JWork W;
-    {
+    int ws;
+    if (NG == 8) {           // per-GPU SoA in shared memory
         const int n = kJG * TB;
         unsigned char* p = smem;
         W.tseg = (double*)p + tid; p += n * sizeof(double);
@@ -687,12 +804,25 @@ __global__ void __launch_bounds__(TB) joint8_kernel(const __grid_constant__ Plan
         W.cmd = ib + 9 * n + tid; W.rse = ib + 10 * n + tid; W.ctx = ib + 11 * n + tid;
         p += 13 * n * sizeof(int);
         W.fl = p + tid;
+        ws = TB;
+    } else {                 // per-GPU SoA in lane-interleaved global scratch
+        const int n = NG * 32;
+        char* p = wbase + P.off_jw;
+        W.tseg = (double*)p + lane; p += n * sizeof(double);
+        W.L = (double*)p + lane; p += n * sizeof(double);
+        int* ib = (int*)p;
+        W.a0 = ib + 0 * n + lane; W.qh = ib + 1 * n + lane; W.qt = ib + 2 * n + lane;
+        W.ql = ib + 3 * n + lane; W.b0 = ib + 4 * n + lane; W.b1 = ib + 5 * n + lane;
+        W.st0 = ib + 6 * n + lane; W.mfin = ib + 7 * n + lane; W.eff = ib + 8 * n + lane;
+        W.cmd = ib + 9 * n + lane; W.rse = ib + 10 * n + lane; W.ctx = ib + 11 * n + lane;
+        p += 13 * n * sizeof(int);
+        W.fl = (unsigned char*)p + lane;
+        ws = 32;
     }
-    char* wbase = P.scratch + ((size_t)blockIdx.x * (TB / 32) + warp) * P.warp_bytes;
     Scratch X;
     X.link = (int*)(wbase + P.off_link) + lane;
     X.pe = (double*)(wbase + P.off_pe) + lane;
-    X.mem = (int2*)(wbase + P.off_mem) + lane;
+    X.mem = nullptr;
     X.ordt = nullptr;
     X.tst = DYN ? (double*)(wbase + P.off_tst) + lane : nullptr;
     X.tfl = DYN ? (unsigned char*)(wbase + P.off_tfl) + lane : nullptr;
@@ -715,7 +845,14 @@ __global__ void __launch_bounds__(TB) joint8_kernel(const __grid_constant__ Plan
         const int q = u / P.n_clist;
         const int c = P.clist[u - q * P.n_clist];
         const long long r = ((long long)c * P.Q + q) * P.S + s;
-        JReplay<DYN, TB> rp(P, T, X, W);
+        JReplay<DYN, TB, NG> rp(P, T, X, W);
+        rp.ws = ws;
+        if constexpr (NG == 64) {        // next-event / routing keys: shared memory
+            rp.tab.tn = (double*)smem + tid;
+            rp.tab.kp = (int*)(smem + (size_t)NG * TB * sizeof(double)) + tid;
+            rp.tab.kd = rp.tab.kp + NG * TB;
+            rp.tab.st = TB;
+        }
         rp.metk = P.sw.rep_met + r * kMaxSloSweep;
         rp.tte = tte;
         rp.tti = tti;
@@ -731,6 +868,14 @@ __global__ void __launch_bounds__(TB) joint8_kernel(const __grid_constant__ Plan
         P.rep_events[r] = res.events;
         P.sw.rep_watts[r] = res.watts;
     }
+}
+
+template <int NG, int TB>
+__host__ __device__ constexpr size_t joint_smem_bytes() {
+    return NG == 8 ? j_work_bytes<TB>() : (size_t)NG * TB * (sizeof(double) + 2 * sizeof(int));
+}
+constexpr size_t joint_global_bytes_per_warp(int NG) {   // per-GPU SoA for NG = 64
+    return NG == 8 ? 0 : (size_t)NG * 32 * (2 * sizeof(double) + 13 * sizeof(int) + 1);
 }
 
 }  // namespace padsim

@@ -103,7 +103,8 @@ struct padsim_ctx {
     int n_evA = 0;
     unsigned* d_workC = nullptr;
     std::vector<int> max_out;   // per trace
-    bool j8[2] = {false, false};   // [static, dynamic] list on the joint8 kernel (N <= 8)
+    bool j8[2] = {false, false};   // [static, dynamic] list planned on the joint kernel
+    int j_ng = 8;                  // its GPU-slot width (8 or 64)
     unsigned* d_workJ[2] = {nullptr, nullptr};
 };
 
@@ -818,95 +819,70 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
         }
         // scratch layout per warp (lane-interleaved, 32 lanes)
         const size_t R = (size_t)std::max(Rmax, 1);
+        const int NG = N <= 8 ? 8 : 64;
         size_t off = 0;
         auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~(size_t)255; return o; };
         P.off_link = take(R * 32 * sizeof(int));
         P.off_pe = take(R * 32 * sizeof(double));
-        const bool j8 = N <= 8;        // static here only with PADSIM_JOINT
-        if (!j8) P.off_mem = take((size_t)N * model->max_decode_batch * 32 * sizeof(int2));
         if (dyn) {
-            if (!j8) P.off_ordt = take(R * 32 * sizeof(int));
             P.off_tst = take(R * 32 * sizeof(double));
             P.off_tfl = take(R * 32);
-            if (j8) {
-                P.off_wts = take(R * 32 * sizeof(double));
-                P.off_wtf = take(R * 32);
-            }
+            P.off_wts = take(R * 32 * sizeof(double));
+            P.off_wtf = take(R * 32);
         }
-        if (j8) {
-            P.off_tte = take((size_t)PADSIM_MAX_SLOTS * 32 * sizeof(double));
-            P.off_tti = take((size_t)PADSIM_MAX_SLOTS * 32 * sizeof(int));
-            int maxo = 2;
-            for (int s2 = 0; s2 < n_traces; s2++) maxo = std::max(maxo, ctx->max_out[s2]);
-            int wheel = 32;
-            while (wheel < maxo) wheel <<= 1;
-            P.wheel = wheel;
-            P.off_heads = take((size_t)kJG * wheel * 32 * sizeof(int));
-            P.off_bits = take((size_t)kJG * (wheel / 32) * 32 * sizeof(unsigned));
-        }
+        P.off_tte = take((size_t)PADSIM_MAX_SLOTS * 32 * sizeof(double));
+        P.off_tti = take((size_t)PADSIM_MAX_SLOTS * 32 * sizeof(int));
+        int maxo = 2;
+        for (int s2 = 0; s2 < n_traces; s2++) maxo = std::max(maxo, ctx->max_out[s2]);
+        int wheel = 32;
+        while (wheel < maxo) wheel <<= 1;
+        P.wheel = wheel;
+        P.off_heads = take((size_t)NG * wheel * 32 * sizeof(int));
+        P.off_bits = take((size_t)NG * (wheel / 32) * 32 * sizeof(unsigned));
+        if (NG == 64) P.off_jw = take(joint_global_bytes_per_warp(64));
         P.warp_bytes = off;
-        P.scratch_per_cta = off * kWarps;
-        if (j8) {
-            ctx->j8[dyn] = true;
-            unsigned* d_wj;
-            AL(d_wj, n_traces);
-            ctx->d_workJ[dyn] = d_wj;
-            P.work = d_wj;
-            P.smem_trace = 0;
-            const long long UJ = (long long)n_traces * n_qps * P.n_clist;
-            const int tbj = UJ >= (long long)ctx->n_sm * 3 * kThreads ? kThreads : 32;
-            ctx->j_tb[dyn] = tbj;
-            const size_t jb = tbj == kThreads ? j_work_bytes<kThreads>() : j_work_bytes<32>();
-            P.smem_trace_bytes = jb;
-            const void* fnj = tbj == kThreads
-                ? (dyn ? (const void*)joint8_kernel<true, kThreads> : (const void*)joint8_kernel<false, kThreads>)
-                : (dyn ? (const void*)joint8_kernel<true, 32> : (const void*)joint8_kernel<false, 32>);
-            CK(cudaFuncSetAttribute(fnj, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jb));
-            int occj = 0;
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occj, fnj, tbj, jb));
-            occj = std::max(occj, 1);
-            const long long items = ((long long)n_qps * P.n_clist + 31) / 32;
-            const int wpc = tbj / 32;
-            long long per_trace = std::max<long long>(1, ((long long)ctx->n_sm * occj) / n_traces);
-            per_trace = std::min<long long>(per_trace, (items + wpc - 1) / wpc);
-            const size_t per_cta = P.warp_bytes * wpc;
-            size_t frj = 0, tmj = 0;
-            CK(cudaMemGetInfo(&frj, &tmj));
-            const long long cap_ctas = std::max<long long>(n_traces, (long long)((tmj * 3 / 10) / per_cta));
-            long long gridj = std::min<long long>(per_trace * n_traces, (cap_ctas / n_traces) * n_traces);
-            gridj = std::max<long long>(gridj, n_traces);
-            char* scrj = nullptr;
-            AL(scrj, (size_t)gridj * per_cta);
-            P.scratch = scrj;
-            (dyn ? ctx->grid_dyn : ctx->grid_static) = (int)gridj;
-            (dyn ? ctx->smem_dyn : ctx->smem_static) = jb;
-            continue;
+        ctx->j8[dyn] = true;
+        ctx->j_ng = NG;
+        unsigned* d_wj;
+        AL(d_wj, n_traces);
+        ctx->d_workJ[dyn] = d_wj;
+        P.work = d_wj;
+        P.smem_trace = 0;
+        const long long UJ = (long long)n_traces * n_qps * P.n_clist;
+        const int tbj = (NG == 8 && UJ >= (long long)ctx->n_sm * 3 * kThreads) ? kThreads : 32;
+        ctx->j_tb[dyn] = tbj;
+        const void* fnj;
+        size_t jb;
+        if (NG == 8) {
+            jb = tbj == kThreads ? joint_smem_bytes<8, kThreads>() : joint_smem_bytes<8, 32>();
+            fnj = tbj == kThreads
+                ? (dyn ? (const void*)joint_kernel<true, kThreads, 8> : (const void*)joint_kernel<false, kThreads, 8>)
+                : (dyn ? (const void*)joint_kernel<true, 32, 8> : (const void*)joint_kernel<false, 32, 8>);
+        } else {
+            jb = joint_smem_bytes<64, 32>();
+            fnj = dyn ? (const void*)joint_kernel<true, 32, 64> : (const void*)joint_kernel<false, 32, 64>;
         }
-        // trace staging in shared memory via TMA bulk copies when it fits
-        const size_t Rp = ((size_t)Rmax + 15) & ~(size_t)15;
-        const size_t tbytes = Rp * (8 + 8 + 4 + 4 + 1);
-        P.smem_trace = tbytes <= 96 * 1024 ? 1 : 0;
-        P.smem_trace_bytes = P.smem_trace ? tbytes : 0;
-        const void* fn;
-        if (N <= 8) fn = dyn ? (const void*)replay_kernel<8, true> : (const void*)replay_kernel<8, false>;
-        else fn = dyn ? (const void*)replay_kernel<64, true> : (const void*)replay_kernel<64, false>;
-        CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem_trace_bytes));
-        int occ = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, P.smem_trace_bytes));
-        occ = std::max(occ, 1);
-        long long grid = (long long)ctx->n_sm * occ;
-        grid = std::min<long long>(grid, P.n_items);
-        // bound the scratch to ~40% of free device memory
-        size_t fr = 0, totm = 0;
-        CK(cudaMemGetInfo(&fr, &totm));
-        const long long max_ctas = (long long)((totm * 3 / 10) / std::max<size_t>(P.scratch_per_cta, 1));
-        if (max_ctas < 1) return fail(ctx, PADSIM_ENOMEM, "scratch does not fit in device memory");
-        grid = std::max<long long>(1, std::min(grid, max_ctas));
-        char* scr = nullptr;
-        AL(scr, (size_t)grid * P.scratch_per_cta);
-        P.scratch = scr;
-        (dyn ? ctx->grid_dyn : ctx->grid_static) = (int)grid;
-        (dyn ? ctx->smem_dyn : ctx->smem_static) = P.smem_trace_bytes;
+        P.smem_trace_bytes = jb;
+        CK(cudaFuncSetAttribute(fnj, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jb));
+        int occj = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occj, fnj, tbj, jb));
+        occj = std::max(occj, 1);
+        const long long items = ((long long)n_qps * P.n_clist + 31) / 32;
+        const int wpc = tbj / 32;
+        long long per_trace = std::max<long long>(1, ((long long)ctx->n_sm * occj) / n_traces);
+        per_trace = std::min<long long>(per_trace, (items + wpc - 1) / wpc);
+        const size_t per_cta = P.warp_bytes * wpc;
+        P.scratch_per_cta = per_cta;
+        size_t frj = 0, tmj = 0;
+        CK(cudaMemGetInfo(&frj, &tmj));
+        const long long cap_ctas = std::max<long long>(n_traces, (long long)((tmj * 3 / 10) / per_cta));
+        long long gridj = std::min<long long>(per_trace * n_traces, (cap_ctas / n_traces) * n_traces);
+        gridj = std::max<long long>(gridj, n_traces);
+        char* scrj = nullptr;
+        AL(scrj, (size_t)gridj * per_cta);
+        P.scratch = scrj;
+        (dyn ? ctx->grid_dyn : ctx->grid_static) = (int)gridj;
+        (dyn ? ctx->smem_dyn : ctx->smem_static) = jb;
     }
 #undef AL
     ctx->plan_static.sw = ctx->sweep;
@@ -944,21 +920,16 @@ int padsim_run(padsim_ctx* ctx, void* stream) {
         if (P.n_clist == 0) continue;
         const int grid = dyn ? ctx->grid_dyn : ctx->grid_static;
         const size_t smem = dyn ? ctx->smem_dyn : ctx->smem_static;
-        if (ctx->j8[dyn]) {
-            CK(cudaMemsetAsync(ctx->d_workJ[dyn], 0, (size_t)ctx->S * sizeof(unsigned), js));
-            if (ctx->j_tb[dyn] == kThreads) {
-                if (dyn) joint8_kernel<true, kThreads><<<grid, kThreads, smem, js>>>(P);
-                else joint8_kernel<false, kThreads><<<grid, kThreads, smem, js>>>(P);
-            } else {
-                if (dyn) joint8_kernel<true, 32><<<grid, 32, smem, js>>>(P);
-                else joint8_kernel<false, 32><<<grid, 32, smem, js>>>(P);
-            }
-        } else if (ctx->N <= 8) {
-            if (dyn) replay_kernel<8, true><<<grid, kThreads, smem, js>>>(P);
-            else replay_kernel<8, false><<<grid, kThreads, smem, js>>>(P);
+        CK(cudaMemsetAsync(ctx->d_workJ[dyn], 0, (size_t)ctx->S * sizeof(unsigned), js));
+        if (ctx->j_ng == 64) {
+            if (dyn) joint_kernel<true, 32, 64><<<grid, 32, smem, js>>>(P);
+            else joint_kernel<false, 32, 64><<<grid, 32, smem, js>>>(P);
+        } else if (ctx->j_tb[dyn] == kThreads) {
+            if (dyn) joint_kernel<true, kThreads, 8><<<grid, kThreads, smem, js>>>(P);
+            else joint_kernel<false, kThreads, 8><<<grid, kThreads, smem, js>>>(P);
         } else {
-            if (dyn) replay_kernel<64, true><<<grid, kThreads, smem, js>>>(P);
-            else replay_kernel<64, false><<<grid, kThreads, smem, js>>>(P);
+            if (dyn) joint_kernel<true, 32, 8><<<grid, 32, smem, js>>>(P);
+            else joint_kernel<false, 32, 8><<<grid, 32, smem, js>>>(P);
         }
         CK(cudaGetLastError());
     }
