@@ -40,6 +40,7 @@ from workloads import (DEFAULT_MODEL, get_config, make_trace, policy,  # noqa: E
 from workloads.configs import dynamic_candidates  # noqa: E402
 
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+TRAFFIC_PATH = os.path.join(ROOT, "profiles", "ncu_traffic.json")   # dram bytes/launch per kernel
 OPS_PER_EVENT = 32          # algorithmic ALU ops of one DES event handler
 LANES_PER_SM = 128          # INT32/FP32 lanes per SM (4 SMSP x 32)
 
@@ -111,6 +112,15 @@ class ClockSampler:
                           if len(r) > 3 + k and r[3 + k].lower().startswith("active")})
         return {"sm_mhz": float(np.median(sm)) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+
+
+def ncu_traffic(workload: str, kernel: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one launch of `kernel` on
+    `workload`, from the committed ncu --set full capture (profiles/), or None."""
+    try:
+        return json.load(open(TRAFFIC_PATH)).get(workload, {}).get(kernel, {}).get("bytes")
+    except Exception:
+        return None
 
 
 def peaks():
@@ -316,7 +326,7 @@ def main():
         f_mhz = clocks.get("sm_mhz") or pk.get("sm_max_mhz") or 1965.0
         r_ms = float(np.mean(replay_ms)) if replay_ms else float("nan")
         km = np.mean(np.array(kern_ms), axis=0) if kern_ms else np.zeros(3)
-        names = ["stageA_kernel", "stageC_kernel", "joint8_kernel/replay_kernel"]
+        names = ["stageA_kernel", "stageC_kernel", "joint_kernel"]
         evs = [ev_a, ev_static, ev_dyn]
         dom = int(np.argmax(km))
         achieved = evs[dom] * OPS_PER_EVENT / (km[dom] / 1e3) / 1e12 if km[dom] > 0 else float("nan")
@@ -336,7 +346,7 @@ def main():
                     "d2h_bytes_per_step": int(d2h), "api": "padsim_evaluate_allocations"},
             "gpu_launches": launches,
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tops/s",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak, "traffic": ncu_traffic(cfg["name"], names[dom]),
                          "kernel": names[dom], "kernel_ms": float(km[dom]),
                          "events_per_launch": evs[dom], "ops_per_event": OPS_PER_EVENT,
                          "peak_basis": f"148 SM x 128 lanes x {f_mhz:.0f} MHz (sampled clock)",
