@@ -90,6 +90,11 @@ struct padsim_ctx {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, evA = nullptr, evC = nullptr;
     cudaEvent_t evJ0 = nullptr, evJ1 = nullptr;
     cudaStream_t side = nullptr;     // joint kernel runs concurrently with stages A/C
+    cudaStream_t sideA = nullptr;    // stage A chunks run ahead of stage C chunks
+    cudaEvent_t evAc[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t evC0 = nullptr;
+    int fC_per_trace = 1;
+    int n_chunks = 1;
     bool ev_recorded = false;
     // factorized static path (N <= 8)
     bool fact = false;
@@ -432,6 +437,8 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
     F.ttft_slo = slo->ttft_s; F.tpot_slo0 = slo->tpot_s[0]; F.tpot_slo1 = slo->tpot_s[1];
     F.n_groups = G;
     F.n_cc = NC;
+    F.s_begin = 0;
+    F.s_count = S;
     int *d_gx, *d_gcap, *d_ccc, *d_ccg, *d_ccy, *d_ccd;
     double* d_pe;
     SRec* d_rec;
@@ -531,6 +538,11 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
         AL(scr, (size_t)grid * per_cta);
         F.scrC = scr;
         ctx->fC_grid = (int)grid;
+        ctx->fC_per_trace = (int)(grid / S);
+        // pipeline stage A ahead of stage C in trace chunks when stage A alone has
+        // enough replays to fill the GPU (else it is latency-bound and splitting
+        // only serialises it)
+        ctx->n_chunks = GQS >= 8LL * ctx->n_sm * kThreads ? std::min(S, 4) : 1;
     }
     F.rep_met = ctx->d_rep_met; F.rep_near = ctx->d_rep_near; F.rep_dur = ctx->d_rep_dur;
     F.rep_good = ctx->d_rep_good; F.rep_events = ctx->d_rep_events;
@@ -582,6 +594,9 @@ void padsim_destroy(padsim_ctx* ctx) {
     if (ctx->evJ0) cudaEventDestroy(ctx->evJ0);
     if (ctx->evJ1) cudaEventDestroy(ctx->evJ1);
     if (ctx->side) cudaStreamDestroy(ctx->side);
+    if (ctx->sideA) cudaStreamDestroy(ctx->sideA);
+    for (auto& e : ctx->evAc) if (e) cudaEventDestroy(e);
+    if (ctx->evC0) cudaEventDestroy(ctx->evC0);
     delete ctx;
 }
 
@@ -907,6 +922,9 @@ int padsim_run(padsim_ctx* ctx, void* stream) {
         CK(cudaEventCreate(&ctx->evJ0));
         CK(cudaEventCreate(&ctx->evJ1));
         CK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&ctx->sideA, cudaStreamNonBlocking));
+        for (auto& e : ctx->evAc) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        CK(cudaEventCreate(&ctx->evC0));
     }
     CK(cudaEventRecord(ctx->ev0, st));
     // fork: the joint replay (dynamic candidates, or static when N > 8) runs on a
@@ -935,23 +953,44 @@ int padsim_run(padsim_ctx* ctx, void* stream) {
     }
     CK(cudaEventRecord(ctx->evJ1, js));
     if (ctx->fact) {
-        const FPlan& F = ctx->fplan;
+        // stage A chunk j runs on sideA while stage C consumes chunk j-1 on st
         CK(cudaMemsetAsync(ctx->d_workC, 0, (size_t)ctx->S * sizeof(unsigned), st));
-        if (ctx->fA_tb == kThreads) stageA_kernel<kThreads><<<ctx->fA_grid, kThreads, ctx->fA_smem, st>>>(F);
-        else stageA_kernel<32><<<ctx->fA_grid, 32, ctx->fA_smem, st>>>(F);
-        CK(cudaGetLastError());
-        CK(cudaEventRecord(ctx->evA, st));
+        CK(cudaStreamWaitEvent(ctx->sideA, ctx->ev0, 0));
+        const int nch = ctx->n_chunks;
+        const int per = (ctx->S + nch - 1) / nch;
         const bool cm = ctx->model.decode_per_ctx_tok_s != 0.0;
-        if (ctx->fC_idx16) {
-            if (cm) stageC_kernel<true, unsigned short><<<ctx->fC_grid, kThreads, ctx->fC_smem, st>>>(F);
-            else stageC_kernel<false, unsigned short><<<ctx->fC_grid, kThreads, ctx->fC_smem, st>>>(F);
-        } else {
-            if (cm) stageC_kernel<true, unsigned><<<ctx->fC_grid, kThreads, ctx->fC_smem, st>>>(F);
-            else stageC_kernel<false, unsigned><<<ctx->fC_grid, kThreads, ctx->fC_smem, st>>>(F);
+        for (int j = 0; j < nch; j++) {
+            FPlan F = ctx->fplan;
+            F.s_begin = j * per;
+            F.s_count = std::min(per, ctx->S - F.s_begin);
+            if (F.s_count <= 0) break;
+            const int ga = F.a_blocks_per_trace * F.s_count;
+            if (ctx->fA_tb == kThreads) stageA_kernel<kThreads><<<ga, kThreads, ctx->fA_smem, ctx->sideA>>>(F);
+            else stageA_kernel<32><<<ga, 32, ctx->fA_smem, ctx->sideA>>>(F);
+            CK(cudaGetLastError());
+            CK(cudaEventRecord(ctx->evAc[j], ctx->sideA));
         }
-        CK(cudaGetLastError());
+        CK(cudaEventRecord(ctx->evA, ctx->sideA));
+        for (int j = 0; j < nch; j++) {
+            FPlan F = ctx->fplan;
+            F.s_begin = j * per;
+            F.s_count = std::min(per, ctx->S - F.s_begin);
+            if (F.s_count <= 0) break;
+            CK(cudaStreamWaitEvent(st, ctx->evAc[j], 0));
+            if (j == 0) CK(cudaEventRecord(ctx->evC0, st));
+            const int gc = ctx->fC_per_trace * F.s_count;
+            if (ctx->fC_idx16) {
+                if (cm) stageC_kernel<true, unsigned short><<<gc, kThreads, ctx->fC_smem, st>>>(F);
+                else stageC_kernel<false, unsigned short><<<gc, kThreads, ctx->fC_smem, st>>>(F);
+            } else {
+                if (cm) stageC_kernel<true, unsigned><<<gc, kThreads, ctx->fC_smem, st>>>(F);
+                else stageC_kernel<false, unsigned><<<gc, kThreads, ctx->fC_smem, st>>>(F);
+            }
+            CK(cudaGetLastError());
+        }
     } else {
         CK(cudaEventRecord(ctx->evA, st));
+        CK(cudaEventRecord(ctx->evC0, st));
     }
     CK(cudaEventRecord(ctx->evC, st));
     if (js != st) CK(cudaStreamWaitEvent(st, ctx->evJ1, 0));   // join
@@ -1051,8 +1090,8 @@ int padsim_kernel_times_ms(padsim_ctx* ctx, float* ms3) {
     if (!ctx->ev_recorded) return fail(ctx, PADSIM_EINVAL, "no run recorded");
     CK(cudaSetDevice(ctx->device));
     CK(cudaEventSynchronize(ctx->ev1));
-    CK(cudaEventElapsedTime(&ms3[0], ctx->ev0, ctx->evA));   // includes the counter memset
-    CK(cudaEventElapsedTime(&ms3[1], ctx->evA, ctx->evC));
+    CK(cudaEventElapsedTime(&ms3[0], ctx->ev0, ctx->evA));   // stage A span (its own stream)
+    CK(cudaEventElapsedTime(&ms3[1], ctx->evC0, ctx->evC));
     CK(cudaEventElapsedTime(&ms3[2], ctx->evJ0, ctx->evJ1));
     return PADSIM_OK;
 }

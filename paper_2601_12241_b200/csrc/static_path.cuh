@@ -94,6 +94,7 @@ struct FPlan {
     char* scrA;
     size_t a_warp_bytes, a_off_tte, a_off_tid, a_off_tpe, a_off_ring, a_ring_lane;
     int a_blocks_per_trace;   // stage A grid = S × this; a CTA never straddles traces
+    int s_begin, s_count;     // traces [s_begin, s_begin + s_count) of this launch (pipelined chunks)
     int a_smem_trace;         // stage A stages its trace in shared memory (TMA bulk)
     // stage C
     int n_cc;
@@ -143,8 +144,9 @@ __global__ void __launch_bounds__(TB) stageA_kernel(const __grid_constant__ FPla
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ unsigned long long bar;
     const int tid = threadIdx.x;
-    const int s = blockIdx.x / P.a_blocks_per_trace;
-    const int local = (blockIdx.x - s * P.a_blocks_per_trace) * TB + tid;
+    const int sl = blockIdx.x / P.a_blocks_per_trace;
+    const int s = P.s_begin + sl;
+    const int local = (blockIdx.x - sl * P.a_blocks_per_trace) * TB + tid;
     const long long off = P.toff[s];
     const int R = P.nreq[s];
     // the CTA's trace (arrival, kv, prompt tokens): staged once in shared memory
@@ -447,7 +449,7 @@ __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant_
             bstride = 32;
         }
     }
-    const int s = blockIdx.x % P.S;
+    const int s = P.s_begin + blockIdx.x % P.s_count;
     const long long off = P.toff[s];
     const int R = P.nreq[s];
     const int* itk = P.in_tok + off;
