@@ -66,7 +66,7 @@ class Summary(C.Structure):
                 ("pad", C.c_int32), ("duration", C.c_double), ("goodput", C.c_double),
                 ("events", C.c_int64), ("n_moves_power", C.c_int32), ("n_moves_gpu", C.c_int32),
                 ("n_saturated", C.c_int32), ("n_flips", C.c_int32), ("avg_watts", C.c_double),
-                ("qps_per_watt", C.c_double)]
+                ("qps_per_watt", C.c_double), ("sum_queue", C.c_double), ("sum_exec", C.c_double)]
 
 
 class LogRec(C.Structure):
@@ -116,6 +116,8 @@ def lib():
             L.or_kv_lat.argtypes = [_P(Model), C.c_int32]
             L.or_p90.restype = C.c_double
             L.or_p90.argtypes = [_P(C.c_double), C.c_int32]
+            L.or_percentile.restype = C.c_double
+            L.or_percentile.argtypes = [_P(C.c_double), C.c_int32, C.c_int32]
             L.or_enumerate.restype = C.c_int
             L.or_enumerate.argtypes = [C.c_int32] * 6 + [_P(C.c_int32), C.c_int32, _P(C.c_int32)]
             L.or_replay.restype = C.c_int
@@ -123,7 +125,7 @@ def lib():
                                     C.c_int32, _P(Slo), C.c_int32, _P(C.c_double), _P(C.c_int32),
                                     _P(C.c_int32), _P(C.c_uint8), C.c_double, _P(C.c_double),
                                     _P(C.c_double), _P(C.c_double), _P(C.c_double), _P(C.c_double),
-                                    _P(Summary), _P(Log)]
+                                    _P(C.c_double), _P(Summary), _P(Log)]
             L.or_evaluate.restype = C.c_int
             L.or_evaluate.argtypes = [_P(Model), C.c_int32, C.c_int32, _P(C.c_uint8), _P(C.c_int32),
                                       _P(Policy), C.c_int32, _P(Slo), C.c_int32, _P(C.c_int32),
@@ -208,6 +210,11 @@ def p90(values) -> float:
     return lib().or_p90(_ptr(v, C.c_double), int(v.size))
 
 
+def percentile(values, p: int) -> float:
+    v = np.ascontiguousarray(values, dtype=np.float64)
+    return lib().or_percentile(_ptr(v, C.c_double), int(v.size), int(p))
+
+
 def enumerate_pool_uniform(n_gpus, budget_w, min_w, max_w, step_w, exact=False) -> np.ndarray:
     n = C.c_int32(0)
     rc = lib().or_enumerate(n_gpus, budget_w, min_w, max_w, step_w, int(exact), None, 0, C.byref(n))
@@ -241,7 +248,7 @@ def replay(model: dict, role, cap, policy: dict, budget_w: int, slo: dict, trace
     s, i, o, p = _trace_arrays(trace)
     R = s.size
     outs = {k: np.zeros(max(R, 1), dtype=np.float64)
-            for k in ("ttft", "tpot", "prefill_end", "completion", "transfer_end")}
+            for k in ("ttft", "tpot", "prefill_end", "completion", "transfer_end", "prefill_start")}
     sm = Summary()
     lg = None
     recs = None
@@ -255,7 +262,8 @@ def replay(model: dict, role, cap, policy: dict, budget_w: int, slo: dict, trace
                          float(qps_per_gpu), _ptr(outs["ttft"], C.c_double),
                          _ptr(outs["tpot"], C.c_double), _ptr(outs["prefill_end"], C.c_double),
                          _ptr(outs["completion"], C.c_double),
-                         _ptr(outs["transfer_end"], C.c_double), C.byref(sm),
+                         _ptr(outs["transfer_end"], C.c_double), _ptr(outs["prefill_start"], C.c_double),
+                         C.byref(sm),
                          C.byref(lg) if lg is not None else None)
     if rc != 0:
         raise OracleError(rc)
@@ -263,7 +271,8 @@ def replay(model: dict, role, cap, policy: dict, budget_w: int, slo: dict, trace
     res.update(met=sm.met, near_boundary=sm.near_boundary, duration=sm.duration,
                goodput=sm.goodput, events=sm.events, n_moves_power=sm.n_moves_power,
                n_moves_gpu=sm.n_moves_gpu, n_saturated=sm.n_saturated, n_flips=sm.n_flips,
-               avg_watts=sm.avg_watts, qps_per_watt=sm.qps_per_watt)
+               avg_watts=sm.avg_watts, qps_per_watt=sm.qps_per_watt, sum_queue=sm.sum_queue,
+               sum_exec=sm.sum_exec)
     if lg is not None:
         n = min(lg.n, log_cap)
         res["log"] = [(recs[k].t, recs[k].type, recs[k].gpu, recs[k].a, recs[k].b) for k in range(n)]

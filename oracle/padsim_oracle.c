@@ -64,6 +64,20 @@ static int cmp_double(const void* a, const void* b) {
     return (x > y) - (x < y);
 }
 
+/* nearest-rank percentile: value at 1-based rank ceil(p/100 · n)
+ * = (p·n + 99)/100 of the sorted samples, p integer in [1, 100]; n ≥ 1.        */
+double or_percentile(const double* v, int32_t n, int32_t p) {
+    if (n <= 0 || p < 1 || p > 100) return NAN;
+    double* tmp = (double*)malloc(sizeof(double) * (size_t)n);
+    if (!tmp) return NAN;
+    memcpy(tmp, v, sizeof(double) * (size_t)n);
+    qsort(tmp, (size_t)n, sizeof(double), cmp_double);
+    int k = (p * n + 99) / 100;
+    double r = tmp[k - 1];
+    free(tmp);
+    return r;
+}
+
 /* p90 nearest rank: 1-based rank ceil(0.9 n) = (90n+99)/100,
  * empty → 0 which counts as "SLO met".                       */
 double or_p90(const double* v, int32_t n) {
@@ -289,7 +303,7 @@ int or_replay(const or_model* m, int32_t N, const uint8_t* role, const int32_t* 
               int32_t R, const double* s_unit, const int32_t* in_tok,
               const int32_t* out_tok, const uint8_t* phase, double qps,
               double* o_ttft, double* o_tpot, double* o_pe, double* o_comp, double* o_te,
-              or_summary* sum, or_log* lg) {
+              double* o_ps, or_summary* sum, or_log* lg) {
     if (!m || !role || !cap || !pol || !slo || !sum || N < 2 || N > OR_MAX_GPUS || R < 0) return -1;
     if (!valid_model(m)) return -5;
     if (!(qps > 0) || !(slo->ttft > 0 && slo->tpot[0] > 0 && slo->tpot[1] > 0)) return -1;
@@ -328,12 +342,13 @@ int or_replay(const or_model* m, int32_t N, const uint8_t* role, const int32_t* 
     double* comp = (double*)malloc(sizeof(double) * (size_t)R);
     double* tpot = (double*)malloc(sizeof(double) * (size_t)R);
     double* te = (double*)malloc(sizeof(double) * (size_t)R);
+    double* ps = (double*)malloc(sizeof(double) * (size_t)R);   /* prefill (batch) start */
     int* done = (int*)calloc((size_t)R, sizeof(int));
     wk_t* W = (wk_t*)calloc((size_t)N, sizeof(wk_t));
     ring_t twait = {0};
     samples_t s_ttft = {0}, s_tpot = {0};
     heap_t h = {0};
-    if (!a || !pe || !comp || !tpot || !te || !done || !W) goto out;
+    if (!a || !pe || !comp || !tpot || !te || !ps || !done || !W) goto out;
     twait.buf = (int*)malloc(sizeof(int) * (size_t)R); twait.cap = R;
     s_ttft.stamp = (double*)malloc(sizeof(double) * (size_t)R);
     s_ttft.val = (double*)malloc(sizeof(double) * (size_t)R);
@@ -622,7 +637,10 @@ int or_replay(const or_model* m, int32_t N, const uint8_t* role, const int32_t* 
                 tok += in_tok[nx];
                 b++;
             }
-            for (int k = 0; k < b; k++) w->batch[k] = ring_pop(&w->q);
+            for (int k = 0; k < b; k++) {
+                w->batch[k] = ring_pop(&w->q);
+                ps[w->batch[k]] = t;
+            }
             w->bn = b;
             w->busy = 1;
             double end = t + or_prefill_lat(m, tok, b, w->eff);
@@ -675,8 +693,12 @@ int or_replay(const or_model* m, int32_t N, const uint8_t* role, const int32_t* 
     /* c.2 step 5–6, metrics (D11 inclusive ≤). */
     {
         int met = 0, near = 0;
-        double last = 0.0;
+        double last = 0.0, sq = 0.0, se = 0.0;
         for (int i = 0; i < R; i++) {
+            /* Fig. 6 decomposition: TTFT = queueing + prefill exec */
+            sq = sq + (ps[i] - a[i]);
+            se = se + (pe[i] - ps[i]);
+            if (o_ps) o_ps[i] = ps[i];
             double tt = pe[i] - a[i];
             double ts = slo->tpot[phase[i]];
             if (tt <= slo->ttft && tpot[i] <= ts) met++;
@@ -695,6 +717,8 @@ int or_replay(const or_model* m, int32_t N, const uint8_t* role, const int32_t* 
         sum->events = events;
         w_acc = w_acc + (double)w_sum * (last - w_prev);
         sum->avg_watts = sum->duration > 0 ? w_acc / sum->duration : (double)w_sum;
+        sum->sum_queue = sq;
+        sum->sum_exec = se;
         sum->qps_per_watt = sum->avg_watts > 0 ? sum->goodput / sum->avg_watts : 0.0;
     }
     rc = 0;
@@ -705,7 +729,7 @@ out:
             free(W[g].act_id); free(W[g].act_fin);
         }
     }
-    free(W); free(a); free(pe); free(comp); free(tpot); free(te); free(done);
+    free(W); free(a); free(pe); free(comp); free(tpot); free(te); free(ps); free(done);
     free(twait.buf); free(s_ttft.stamp); free(s_ttft.val); free(s_tpot.stamp); free(s_tpot.val);
     free(h.a);
     return rc;
@@ -751,7 +775,7 @@ static void* worker_main(void* arg) {
         int rc = or_replay(J->m, J->N, J->role + (size_t)c * J->N, J->cap + (size_t)c * J->N,
                            &J->pol[c], J->B, J->slo, J->n_req[s], J->s_unit[s], J->in_tok[s],
                            J->out_tok[s], J->phase[s], J->qps[q], NULL, NULL, NULL, NULL, NULL,
-                           &sm, NULL);
+                           NULL, &sm, NULL);
         if (rc) { J->err = rc; continue; }
         J->r_met[r] = sm.met;
         J->r_near[r] = sm.near_boundary;

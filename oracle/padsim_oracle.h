@@ -61,6 +61,8 @@ typedef struct {
     int32_t n_moves_power, n_moves_gpu, n_saturated, n_flips;
     double avg_watts;     /* time-weighted mean of Σ effective caps over [a_0, last completion] */
     double qps_per_watt;  /* goodput / avg_watts                                  */
+    double sum_queue;     /* Σ_i (prefill start − arrival), request-id order (Fig. 6)    */
+    double sum_exec;      /* Σ_i (prefill end − prefill start), request-id order               */
 } or_summary;
 
 /* log records for invariant tests (budget, cooldown, role bounds, masking) */
@@ -76,6 +78,7 @@ double or_prefill_lat(const or_model* m, int64_t tokens, int32_t b, int32_t w);
 double or_decode_lat(const or_model* m, int32_t n, int64_t ctx, int32_t w);
 double or_kv_lat(const or_model* m, int32_t tokens);
 double or_p90(const double* v, int32_t n); /* nearest rank, copies + sorts  */
+double or_percentile(const double* v, int32_t n, int32_t p);   /* nearest rank, p in 1..100 */
 
 /* One replay: one candidate (role[N], cap[N], policy) x one trace x one QPS.
  * Outputs per request (nullable arrays of n_req).  Returns 0 or <0 on bad
@@ -85,7 +88,7 @@ int or_replay(const or_model* m, int32_t n_gpus, const uint8_t* role, const int3
               int32_t n_req, const double* s_unit, const int32_t* in_tok,
               const int32_t* out_tok, const uint8_t* phase, double qps_per_gpu,
               double* ttft, double* tpot, double* prefill_end, double* completion,
-              double* transfer_end, or_summary* sum, or_log* log);
+              double* transfer_end, double* prefill_start, or_summary* sum, or_log* log);
 
 /* Whole evaluation: n_cand x n_qps x n_traces replays over n_threads host
  * threads; Σ over traces in ascending trace order; argmax per QPS with key

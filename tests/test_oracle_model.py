@@ -130,3 +130,15 @@ def test_enumeration_per_x_and_cfg1():
     assert per_x == GOLD["enumeration"]["per_x_8_4800_25"]
     g1 = oracle.enumerate_pool_uniform(8, 4800, 400, 750, 100)
     assert int((g1[:, 0] == 4).sum()) == GOLD["enumeration"]["cfg1_4p4d_100w"]
+
+
+def test_percentile_nearest_rank():
+    # nearest rank = value at 1-based index ceil(p/100 * n)
+    assert oracle.percentile(list(range(1, 11)), 90) == 9.0
+    assert oracle.percentile([7.5], 50) == 7.5
+    rng = np.random.default_rng(3)
+    for n in (1, 2, 3, 10, 99, 100, 101, 2000):
+        v = rng.random(n)
+        for p in (50, 90, 99, 100):
+            k = int(np.ceil(p / 100 * n))
+            assert oracle.percentile(v, p) == np.sort(v)[k - 1]
