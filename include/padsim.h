@@ -228,6 +228,27 @@ int padsim_fetch_records(padsim_ctx* ctx, void* stream, double* ttft, double* tp
                          double* prefill_end, double* completion, double* transfer_end,
                          int32_t* r_max);
 
+/* ---- Fig. 6 TTFT decomposition, percentiles ----------
+ * padsim_fetch_decomposition (synchronises; any pointer may be NULL):
+ *   rep_queue[r], rep_exec[r]   r = (c*Q + q)*S + s: Σ over the replay's
+ *       requests of (prefill batch start − arrival) and (prefill end − batch
+ *       start) — the queueing-delay / prefill-execution split of TTFT that
+ *       Fig. 6 reports (TTFT = queue + exec + KV transfer)
+ *   sum_queue[c*Q + q], sum_exec[c*Q + q]   Σ over traces (ascending) of the
+ *       per-replay sums; divide by Σ_s n_req for per-request means.
+ * Summation order inside a replay is batch-completion order (the oracle sums
+ * in request-id order): FP64 agreement is to rounding (≤ 1e-9 relative).
+ * padsim_fetch_percentiles (plan flag PADSIM_RECORDS, after padsim_run;
+ * synchronises): nearest-rank percentiles (S:426–432, 1-based rank
+ * ⌈p·n/100⌉) of each replay's TTFT and TPOT records, pcts[k] ∈ [1, 100],
+ * 1 ≤ n_pct ≤ PADSIM_MAX_PCT, out[(r*2 + m)*n_pct + k] (m = 0 TTFT, 1 TPOT),
+ * NaN for an empty trace. Exact (a sort; no arithmetic). EINVAL otherwise.  */
+#define PADSIM_MAX_PCT 16
+int padsim_fetch_decomposition(padsim_ctx* ctx, void* stream, double* rep_queue, double* rep_exec,
+                               double* sum_queue, double* sum_exec);
+int padsim_fetch_percentiles(padsim_ctx* ctx, void* stream, const int32_t* pcts, int32_t n_pct,
+                             double* out);
+
 /* a8 across ranks: argmax over a device met array (e.g. after an NCCL
  * all-reduce of d_met) using the planned candidates' Σcaps; asynchronous.   */
 int padsim_argmax_device(padsim_ctx* ctx, void* stream, const int64_t* d_met, int32_t n_cand,

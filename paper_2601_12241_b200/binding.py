@@ -16,6 +16,7 @@ LIB_PATH = os.path.join(HERE, "libpadsim.so")
 
 MAX_GPUS = 64
 MAX_ANCHORS = 8
+MAX_PCT = 16
 RECORDS = 1
 JOINT = 2
 
@@ -104,7 +105,7 @@ EXPORTS = ["padsim_create", "padsim_destroy", "padsim_last_error", "padsim_versi
            "padsim_get_device_results", "padsim_fetch_replays", "padsim_fetch_records",
            "padsim_argmax_device", "padsim_step_controller", "padsim_enumerate_pool_uniform",
            "padsim_replay_kernel_ms", "padsim_kernel_times_ms", "padsim_set_slo_sweep",
-           "padsim_fetch_extras"]
+           "padsim_fetch_extras", "padsim_fetch_decomposition", "padsim_fetch_percentiles"]
 
 _lib = None
 _P = C.POINTER
@@ -141,6 +142,8 @@ def load(path: str = LIB_PATH):
     L.padsim_fetch_replays.argtypes = [vp, vp, _P(C.c_int32), _P(C.c_int32), _P(C.c_double),
                                        _P(C.c_double), _P(C.c_int64)]
     L.padsim_fetch_records.argtypes = [vp, vp] + [_P(C.c_double)] * 5 + [_P(C.c_int32)]
+    L.padsim_fetch_decomposition.argtypes = [vp, vp] + [_P(C.c_double)] * 4
+    L.padsim_fetch_percentiles.argtypes = [vp, vp, _P(C.c_int32), C.c_int32, _P(C.c_double)]
     L.padsim_argmax_device.argtypes = [vp, vp, vp, C.c_int32, C.c_int32, vp]
     L.padsim_step_controller.argtypes = [vp, _P(Policy), _P(Budget), _P(Model), _P(CtrlState),
                                          _P(WindowStats), C.c_double, _P(Action)]
@@ -345,6 +348,29 @@ class Context:
                                                 *[_p(out[k], C.c_double) for k in names],
                                                 C.byref(rmax)), "fetch_records")
         return out
+
+    def fetch_decomposition(self, stream=None):
+        """Fig. 6 split of TTFT: per-replay Σ queueing delay / Σ prefill
+        execution time [C,Q,S] and their Σ over traces [C,Q]."""
+        Cn, Q, S, _ = self.shape
+        rq = np.zeros((Cn, Q, S), np.float64)
+        re = np.zeros((Cn, Q, S), np.float64)
+        sq = np.zeros((Cn, Q), np.float64)
+        se = np.zeros((Cn, Q), np.float64)
+        self._check(self.L.padsim_fetch_decomposition(self.ptr, C.c_void_p(stream or 0), _p(rq, C.c_double),
+                                                      _p(re, C.c_double), _p(sq, C.c_double),
+                                                      _p(se, C.c_double)), "fetch_decomposition")
+        return {"rep_queue": rq, "rep_exec": re, "sum_queue": sq, "sum_exec": se}
+
+    def fetch_percentiles(self, pcts, stream=None):
+        """Nearest-rank TTFT/TPOT percentiles per replay (records mode):
+        returns {"ttft": [C,Q,S,n_pct], "tpot": [C,Q,S,n_pct]}."""
+        Cn, Q, S, _ = self.shape
+        p = np.ascontiguousarray(np.asarray(pcts, np.int32))
+        out = np.zeros((Cn, Q, S, 2, max(p.size, 1)), np.float64)
+        self._check(self.L.padsim_fetch_percentiles(self.ptr, C.c_void_p(stream or 0), _p(p, C.c_int32),
+                                                    int(p.size), _p(out, C.c_double)), "fetch_percentiles")
+        return {"ttft": out[..., 0, :], "tpot": out[..., 1, :]}
 
     def device_results(self):
         d = DeviceResults()

@@ -12,6 +12,8 @@
 namespace padsim {
 
 constexpr int kMaxSloSweep = 8;        // extra SLO sets scored per replay
+constexpr int kMaxPct = 16;             // percentiles per padsim_fetch_percentiles call (PADSIM_MAX_PCT)
+constexpr size_t kPctSmemMax = 128 * 1024;   // bitonic buffer in shared memory up to 16384 values
 
 // Extra SLO sets scored on the same trajectories + per-replay extra outputs.
 struct SloSweep {
@@ -20,6 +22,8 @@ struct SloSweep {
     int* rep_met;          // [r * kMaxSloSweep + k]
     double* rep_watts;     // [r] time-weighted mean of Σ effective caps
     const int* capsum;     // [C] Σ initial caps
+    double* rep_sq;        // [r] Σ_i (prefill start − arrival)   (Fig. 6)
+    double* rep_se;        // [r] Σ_i (prefill end − prefill start)
 };
 
 constexpr int kThreads = 128;          // replays per CTA (4 warps)

@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -75,6 +76,16 @@ struct padsim_ctx {
     double* d_qpw = nullptr;         // [C*Q] Σ_s goodput/avg_watts
     double* d_watts = nullptr;       // [C*Q] Σ_s avg_watts
     int* d_max80 = nullptr;          // [C*(1+kMaxSloSweep)]
+    // Fig. 6 decomposition and percentiles
+    double* d_rep_sq = nullptr;      // [r] Σ_i queueing delay
+    double* d_rep_se = nullptr;      // [r] Σ_i prefill exec time
+    double* d_qsum = nullptr;        // [C*Q] Σ_s rep_sq
+    double* d_esum = nullptr;        // [C*Q] Σ_s rep_se
+    int* d_pct = nullptr;            // [kMaxPct] requested percentiles (records mode)
+    double* d_pct_out = nullptr;     // [r][2][kMaxPct]
+    double* d_pct_scratch = nullptr; // global sort buffers when a trace exceeds shared memory
+    int pct_n2 = 0, pct_grid = 0;
+    size_t pct_smem = 0;
     long long n_req_total = 0;
     SloSweep sweep{};
     double *d_rec[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -93,7 +104,6 @@ struct padsim_ctx {
     cudaStream_t sideA = nullptr;    // stage A chunks run ahead of stage C chunks
     cudaEvent_t evAc[4] = {nullptr, nullptr, nullptr, nullptr};
     cudaEvent_t evC0 = nullptr;
-    int fC_per_trace = 1;
     int n_chunks = 1;
     bool ev_recorded = false;
     // factorized static path (N <= 8)
@@ -217,12 +227,13 @@ __global__ void tables_kernel(const padsim_model m, double* spre, double* sdec, 
 __global__ void reduce_kernel(const int* rep_met, const int* rep_near, const double* rep_good,
                               int CQ, int S, long long* met, double* good, long long* near,
                               const int* rep_metk, const double* rep_watts, int nk,
-                              long long* metk, double* qpw, double* watts) {
+                              long long* metk, double* qpw, double* watts,
+                              const double* rep_sq, const double* rep_se, double* qsum, double* esum) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= CQ) return;
     long long m = 0, nn = 0;
     long long mk[kMaxSloSweep] = {0, 0, 0, 0, 0, 0, 0, 0};
-    double g = 0.0, qw = 0.0, ws = 0.0;
+    double g = 0.0, qw = 0.0, ws = 0.0, sq = 0.0, se = 0.0;
     const long long base = (long long)k * S;
     for (int s = 0; s < S; s++) {      // ascending trace order (c.4)
         const long long r = base + s;
@@ -232,14 +243,56 @@ __global__ void reduce_kernel(const int* rep_met, const int* rep_near, const dou
         const double w = rep_watts[r];
         qw += w > 0 ? rep_good[r] / w : 0.0;     // QPS/W = goodput / avg provisioned W
         ws += w;
+        sq += rep_sq[r];
+        se += rep_se[r];
         for (int z = 0; z < nk; z++) mk[z] += rep_metk[r * kMaxSloSweep + z];
     }
+    qsum[k] = sq;
+    esum[k] = se;
     met[k] = m;
     near[k] = nn;
     good[k] = g;
     qpw[k] = qw;
     watts[k] = ws;
     for (int z = 0; z < kMaxSloSweep; z++) metk[(long long)k * kMaxSloSweep + z] = z < nk ? mk[z] : 0;
+}
+
+// Nearest-rank percentiles (1-based rank ceil(p·n/100), integer
+// form (p·n+99)/100) of each replay's per-request TTFT and TPOT records
+// (records mode). One CTA per replay at a time; bitonic sort of the padded
+// power-of-two buffer in shared memory, or in a per-CTA global slice when the
+// trace does not fit. Exact: a sort moves values, no arithmetic.
+__global__ void __launch_bounds__(512) percentile_kernel(const double* rec_ttft, const double* rec_tpot,
+                                                         const int* nreq, int S, int Rmax, int n2,
+                                                         long long n_rep, const int* pcts, int np,
+                                                         double* out, double* gscratch) {
+    extern __shared__ __align__(16) double psm[];
+    double* buf = gscratch ? gscratch + (size_t)blockIdx.x * n2 : psm;
+    for (long long r = blockIdx.x; r < n_rep; r += gridDim.x) {
+        const int R = nreq[r % S];
+        for (int m = 0; m < 2; m++) {
+            const double* src = (m ? rec_tpot : rec_ttft) + r * Rmax;
+            for (int i = threadIdx.x; i < n2; i += blockDim.x) buf[i] = i < R ? src[i] : PAD_INF;
+            __syncthreads();
+            for (int k = 2; k <= n2; k <<= 1) {
+                for (int j = k >> 1; j > 0; j >>= 1) {
+                    for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+                        const int l = i ^ j;
+                        if (l > i) {
+                            const double a = buf[i], b = buf[l];
+                            if (((i & k) == 0) ? (a > b) : (a < b)) { buf[i] = b; buf[l] = a; }
+                        }
+                    }
+                    __syncthreads();
+                }
+            }
+            for (int z = threadIdx.x; z < np; z += blockDim.x) {
+                const int p = pcts[z];
+                out[(r * 2 + m) * kMaxPct + z] = R > 0 ? buf[(p * R + 99) / 100 - 1] : __longlong_as_double(0x7ff8000000000000LL);
+            }
+            __syncthreads();
+        }
+    }
 }
 
 // Max QPS at >= 80% SLO attainment per candidate, for the main SLO
@@ -444,12 +497,14 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
     SRec* d_rec;
     SHot* d_hot;
     long long* d_evA;
+    double *d_asq, *d_ase;
     const long long GQS = (long long)G * Q * S;
     const size_t Rm = (size_t)F.Rmax;
 #define AL(p, n) do { int r_ = dalloc(ctx, &(p), (size_t)(n)); if (r_) return r_; } while (0)
     AL(d_gx, G); AL(d_gcap, (size_t)G * kNW); AL(d_ccc, NC); AL(d_ccg, NC); AL(d_ccy, NC);
     AL(d_ccd, (size_t)NC * kNW);
     AL(d_rec, GQS * Rm); AL(d_hot, GQS * Rm); AL(d_pe, GQS * Rm); AL(d_evA, GQS);
+    AL(d_asq, GQS); AL(d_ase, GQS);
     CK(cudaMemcpy(d_gx, gx.data(), sizeof(int) * G, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(d_gcap, gcap.data(), sizeof(int) * G * kNW, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(d_ccc, cc_cand.data(), sizeof(int) * NC, cudaMemcpyHostToDevice));
@@ -458,6 +513,7 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
     CK(cudaMemcpy(d_ccd, cc_dcap.data(), sizeof(int) * NC * kNW, cudaMemcpyHostToDevice));
     F.gx = d_gx; F.gcap = d_gcap; F.cc_cand = d_ccc; F.cc_group = d_ccg; F.cc_y = d_ccy; F.cc_dcap = d_ccd;
     F.st_rec = d_rec; F.st_hot = d_hot; F.st_pe = d_pe; F.evA = d_evA;
+    F.a_sq = d_asq; F.a_se = d_ase;
     ctx->d_evA = d_evA;
     ctx->n_evA = (int)GQS;
     // stage A scratch per warp: per-lane prompt rings (kNW workers + the KV-wait
@@ -538,11 +594,11 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
         AL(scr, (size_t)grid * per_cta);
         F.scrC = scr;
         ctx->fC_grid = (int)grid;
-        ctx->fC_per_trace = (int)(grid / S);
         // pipeline stage A ahead of stage C in trace chunks when stage A alone has
         // enough replays to fill the GPU (else it is latency-bound and splitting
         // only serialises it)
         ctx->n_chunks = GQS >= 8LL * ctx->n_sm * kThreads ? std::min(S, 4) : 1;
+        if (const char* e = getenv("PADSIM_CHUNKS")) ctx->n_chunks = std::max(1, std::min(S, atoi(e)));
     }
     F.rep_met = ctx->d_rep_met; F.rep_near = ctx->d_rep_near; F.rep_dur = ctx->d_rep_dur;
     F.rep_good = ctx->d_rep_good; F.rep_events = ctx->d_rep_events;
@@ -764,15 +820,37 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
     AL(ctx->d_qpw, CQ);
     AL(ctx->d_watts, CQ);
     AL(ctx->d_max80, (long long)C * (1 + kMaxSloSweep));
+    AL(ctx->d_rep_sq, R_all);
+    AL(ctx->d_rep_se, R_all);
+    AL(ctx->d_qsum, CQ);
+    AL(ctx->d_esum, CQ);
     ctx->sweep = SloSweep{};
     ctx->sweep.rep_met = ctx->d_rep_metk;
     ctx->sweep.rep_watts = ctx->d_rep_watts;
+    ctx->sweep.rep_sq = ctx->d_rep_sq;
+    ctx->sweep.rep_se = ctx->d_rep_se;
     ctx->sweep.capsum = ctx->d_capsum;
     ctx->n_req_total = 0;
     for (int s2 = 0; s2 < n_traces; s2++) ctx->n_req_total += traces[s2].n_req;
     AL(ctx->d_work, 4);
     if (flags & PADSIM_RECORDS) {
         for (auto& r : ctx->d_rec) AL(r, (size_t)R_all * std::max(Rmax, 1));
+        AL(ctx->d_pct, kMaxPct);
+        AL(ctx->d_pct_out, (size_t)R_all * 2 * kMaxPct);
+        int n2 = 1;
+        while (n2 < Rmax) n2 <<= 1;
+        ctx->pct_n2 = n2;
+        if ((size_t)n2 * sizeof(double) <= kPctSmemMax) {
+            ctx->pct_smem = (size_t)n2 * sizeof(double);
+            ctx->pct_grid = (int)std::min<long long>(R_all, (long long)ctx->n_sm * 8);
+            ctx->d_pct_scratch = nullptr;
+        } else {
+            ctx->pct_smem = 0;
+            ctx->pct_grid = (int)std::min<long long>(R_all, (long long)ctx->n_sm * 2);
+            AL(ctx->d_pct_scratch, (size_t)ctx->pct_grid * n2);
+        }
+        CK(cudaFuncSetAttribute(percentile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)kPctSmemMax));
     }
     CK(cudaMemcpy(ctx->d_toff, toff.data(), sizeof(long long) * (n_traces + 1), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(ctx->d_nreq, nreq.data(), sizeof(int) * n_traces, cudaMemcpyHostToDevice));
@@ -978,7 +1056,9 @@ int padsim_run(padsim_ctx* ctx, void* stream) {
             if (F.s_count <= 0) break;
             CK(cudaStreamWaitEvent(st, ctx->evAc[j], 0));
             if (j == 0) CK(cudaEventRecord(ctx->evC0, st));
-            const int gc = ctx->fC_per_trace * F.s_count;
+            // every chunk gets the full resident grid (CTAs round-robin over the
+            // chunk's traces, warps pull work items per trace)
+            const int gc = ctx->fC_grid;
             if (ctx->fC_idx16) {
                 if (cm) stageC_kernel<true, unsigned short><<<gc, kThreads, ctx->fC_smem, st>>>(F);
                 else stageC_kernel<false, unsigned short><<<gc, kThreads, ctx->fC_smem, st>>>(F);
@@ -1000,7 +1080,8 @@ int padsim_run(padsim_ctx* ctx, void* stream) {
     reduce_kernel<<<(CQ + 255) / 256, 256, 0, st>>>(ctx->d_rep_met, ctx->d_rep_near, ctx->d_rep_good,
                                                     CQ, ctx->S, ctx->d_met, ctx->d_good, ctx->d_near,
                                                     ctx->d_rep_metk, ctx->d_rep_watts, ctx->sweep.n,
-                                                    ctx->d_metk, ctx->d_qpw, ctx->d_watts);
+                                                    ctx->d_metk, ctx->d_qpw, ctx->d_watts,
+                                                    ctx->d_rep_sq, ctx->d_rep_se, ctx->d_qsum, ctx->d_esum);
     CK(cudaGetLastError());
     max80_kernel<<<(ctx->C + 127) / 128, 128, 0, st>>>(ctx->d_met, ctx->d_metk, ctx->d_qps, ctx->C, ctx->Q,
                                                        ctx->sweep.n, ctx->n_req_total, ctx->d_max80);
@@ -1081,6 +1162,49 @@ int padsim_fetch_extras(padsim_ctx* ctx, void* stream, int64_t* met_sweep, doubl
     if (max_qps80)
         CK(cudaMemcpyAsync(max_qps80, ctx->d_max80, (size_t)ctx->C * (1 + kMaxSloSweep) * 4,
                            cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return PADSIM_OK;
+}
+
+int padsim_fetch_decomposition(padsim_ctx* ctx, void* stream, double* rep_queue, double* rep_exec,
+                               double* sum_queue, double* sum_exec) {
+    if (!ctx) return PADSIM_EINVAL;
+    if (!ctx->planned) return fail(ctx, PADSIM_EINVAL, "no plan");
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t n = (size_t)ctx->C * ctx->Q * ctx->S;
+    const size_t CQ = (size_t)ctx->C * ctx->Q;
+    if (rep_queue) CK(cudaMemcpyAsync(rep_queue, ctx->d_rep_sq, n * 8, cudaMemcpyDeviceToHost, st));
+    if (rep_exec) CK(cudaMemcpyAsync(rep_exec, ctx->d_rep_se, n * 8, cudaMemcpyDeviceToHost, st));
+    if (sum_queue) CK(cudaMemcpyAsync(sum_queue, ctx->d_qsum, CQ * 8, cudaMemcpyDeviceToHost, st));
+    if (sum_exec) CK(cudaMemcpyAsync(sum_exec, ctx->d_esum, CQ * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return PADSIM_OK;
+}
+
+int padsim_fetch_percentiles(padsim_ctx* ctx, void* stream, const int32_t* pcts, int32_t n_pct,
+                             double* out) {
+    if (!ctx || !pcts || !out) return PADSIM_EINVAL;
+    if (!ctx->planned || !(ctx->flags & PADSIM_RECORDS))
+        return fail(ctx, PADSIM_EINVAL, "plan without PADSIM_RECORDS");
+    if (!ctx->ev_recorded) return fail(ctx, PADSIM_EINVAL, "no run recorded");
+    if (n_pct < 1 || n_pct > kMaxPct) return fail(ctx, PADSIM_EINVAL, "n_pct out of range");
+    for (int z = 0; z < n_pct; z++)
+        if (pcts[z] < 1 || pcts[z] > 100) return fail(ctx, PADSIM_EINVAL, "percentile outside 1..100");
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    static_assert(kMaxPct == PADSIM_MAX_PCT, "ABI constant");
+    const long long n_rep = (long long)ctx->C * ctx->Q * ctx->S;
+    CK(cudaMemcpyAsync(ctx->d_pct, pcts, sizeof(int) * n_pct, cudaMemcpyHostToDevice, st));
+    if (n_rep > 0) {
+        percentile_kernel<<<ctx->pct_grid, 512, ctx->pct_smem, st>>>(
+            ctx->d_rec[0], ctx->d_rec[1], ctx->d_nreq, ctx->S, std::max(ctx->Rmax, 1), ctx->pct_n2, n_rep,
+            ctx->d_pct, n_pct, ctx->d_pct_out, ctx->d_pct_scratch);
+        CK(cudaGetLastError());
+    }
+    // compact [r][2][kMaxPct] -> [r][2][n_pct] on the host side of the copy
+    CK(cudaMemcpy2DAsync(out, sizeof(double) * n_pct, ctx->d_pct_out, sizeof(double) * kMaxPct,
+                         sizeof(double) * n_pct, (size_t)n_rep * 2, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     return PADSIM_OK;
 }

@@ -91,6 +91,8 @@ struct FPlan {
     struct SHot* st_hot;    // same stream, hot 16-B part
     double* st_pe;          // prefill end, indexed by request id (stage A scratch)
     long long* evA;         // [G*Q*S] stage-A instants
+    double* a_sq;           // [G*Q*S] Σ queueing delay (prefill start − arrival)
+    double* a_se;           // [G*Q*S] Σ prefill exec time (end − start)
     char* scrA;
     size_t a_warp_bytes, a_off_tte, a_off_tid, a_off_tpe, a_off_ring, a_ring_lane;
     int a_blocks_per_trace;   // stage A grid = S × this; a CTA never straddles traces
@@ -132,7 +134,7 @@ struct FPlan {
 // memory for 32-thread CTAs) with the earliest (te, id) cached in registers.
 // ---------------------------------------------------------------------------
 template <int TB>
-__host__ __device__ constexpr size_t a_work_bytes() { return (size_t)kNW * TB * (sizeof(double) + 4 * sizeof(int)); }
+__host__ __device__ constexpr size_t a_work_bytes() { return (size_t)kNW * TB * (2 * sizeof(double) + 4 * sizeof(int)); }
 template <int TB>
 __host__ __device__ constexpr size_t a_slot_bytes() {   // KV slots kept in smem for small CTAs
     return TB == 32 ? (size_t)PADSIM_MAX_SLOTS * TB * (2 * sizeof(double) + sizeof(int)) : 0;
@@ -181,7 +183,8 @@ __global__ void __launch_bounds__(TB) stageA_kernel(const __grid_constant__ FPla
     const long long u = (long long)blockIdx.x * TB + tid;    // scratch slot
     const int n_sm = kNW * TB;
     double* Wsp = (double*)smem + tid;
-    int* ib = (int*)(smem + (size_t)n_sm * sizeof(double));
+    double* Wbs = (double*)smem + n_sm + tid;   // start time of the batch in service
+    int* ib = (int*)(smem + (size_t)2 * n_sm * sizeof(double));
     int* Wqh = ib + 0 * n_sm + tid;     // ring index of the queue head
     int* Wql = ib + 1 * n_sm + tid;     // queue length
     int* Wbh = ib + 2 * n_sm + tid;     // ring index of the batch in service
@@ -229,6 +232,7 @@ __global__ void __launch_bounds__(TB) stageA_kernel(const __grid_constant__ FPla
     int na = 0, k = 0;
     double ta = R > 0 ? su[0] * inv_lam : PAD_INF;
     long long inst = 0;
+    double sq = 0.0, se = 0.0;
     while (k < R) {
         double t = ta < mte ? ta : mte;
 #pragma unroll
@@ -244,6 +248,7 @@ __global__ void __launch_bounds__(TB) stageA_kernel(const __grid_constant__ FPla
             const int* rw = ring + (size_t)w * R;
             int j = Wbh[o];
             const int n = Wbn[o];
+            const double bstart = Wbs[o];
             long long dec = 0;
             for (int z0 = 0; z0 < n; z0 += kPre) {
                 int ids[kPre];
@@ -258,6 +263,8 @@ __global__ void __launch_bounds__(TB) stageA_kernel(const __grid_constant__ FPla
                     if (z0 + z >= n) break;
                     const int i = ids[z];
                     dec += it[i];
+                    sq = sq + (bstart - su[i] * inv_lam);     // Fig. 6 decomposition
+                    se = se + (t - bstart);
                     if (tbusy < slots) {
                         const double te = t + kv[i];
                         tte[tbusy * ss] = te;
@@ -372,13 +379,17 @@ __global__ void __launch_bounds__(TB) stageA_kernel(const __grid_constant__ FPla
             }
             Wbh[o] = h;
             Wbn[o] = b;
+            Wbs[o] = t;
             Wql[o] = qn - b;
             int nh = h + b;
             Wqh[o] = nh >= R ? nh - R : nh;
             set_tnext(w, t + ((double)tok / P.m.den[b]) / Wsp[o]);
         }
     }
-    P.evA[(g * P.Q + q) * (long long)P.S + s] = inst;
+    const long long ga = (g * P.Q + q) * (long long)P.S + s;
+    P.evA[ga] = inst;
+    P.a_sq[ga] = sq;
+    P.a_se[ga] = se;
 }
 
 __device__ __forceinline__ int first_boundary_ge(double tseg, double L, int st0, int stm, double tau) {
@@ -669,6 +680,11 @@ __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant_
         P.rep_dur[r] = dur;
         P.rep_good[r] = dur > 0 ? (double)met / dur : 0.0;
         P.rep_events[r] = inst;
+        {
+            const long long ga = (g * P.Q + q) * (long long)P.S + s;
+            P.sw.rep_sq[r] = P.a_sq[ga];
+            P.sw.rep_se[r] = P.a_se[ga];
+        }
         {   // static caps: provisioned power is Σ caps over [a_0, last completion]
             const double cs = (double)P.sw.capsum[c];
             const double acc = R > 0 ? cs * dur : 0.0;
