@@ -294,7 +294,220 @@ static int valid_model(const or_model* m) {
     if (!(m->rate > 0 && m->eff >= 0 && m->dec_fixed > 0 && m->dec_per_seq >= 0 &&
           m->dec_per_ctx >= 0 && m->kvb > 0 && m->bw > 0 && m->ovh > 0)) return 0;
     if (m->max_pb < 1 || m->pb_tokens < 1 || m->max_db < 1 || m->slots < 1 || m->slots > 32) return 0;
+    if (m->chunk < 1) return 0;
     return 1;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Coalesced (non-disaggregated) replay — the paper's baseline: "vLLM in    */
+/* coalesced mode ... generated using chunked prefill", SPEC         */
+/* coalesced_step, readings A33–A37:             */
+/*  A33 every GPU serves both phases at its cap; roles are ignored; no KV    */
+/*      transfer (transfer_end = prefill_end).                               */
+/*  A34 arrivals go to the GPU with the least outstanding prompt tokens      */
+/*      (remaining, queued + in service), lowest id (as A8).                 */
+/*  A35 one engine step = at most one chunk of ≤ chunk tokens of the head    */
+/*      prompt (FIFO, no packing across prompts) fused with every active     */
+/*      decode sequence: lat = prefill_lat(c,1,w) + decode_lat(n,C,w) when   */
+/*      both are present, else the one present.  A chunk step ends   */
+/*      at t + lat.                                                          */
+/*  A36 the last chunk's step end is the first token (prefill_end, TTFT);    */
+/*      the request then joins this GPU's decode batch at that boundary      */
+/*      (pending FIFO when max_db is full) and needs out−1 more steps;       */
+/*      out = 1 completes at prefill_end with TPOT 0 (A7).                   */
+/*  A37 runs of decode-only steps are constant-composition segments,         */
+/*      boundary k at t_seg + (double)k·L (A14); a chunk step, a join or a   */
+/*      leave ends the segment.                                              */
+/* One heap event per engine step; kind order as A10 (step end < arrival).  */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+    ring_t q; int done_tok; long outstanding;          /* prompt FIFO, head progress */
+    int* act_id; int* act_fin; int n_act; long ctx;     /* decode batch               */
+    ring_t pend; int step, step0; double t_seg, L;
+    int in_step, at_boundary, comp_changed, seg_valid;
+    int c_id, c_tok;                                     /* chunk of the step in flight */
+} cw_t;
+
+static int replay_coalesced(const or_model* m, int32_t N, const int32_t* cap, int32_t B,
+                            const or_slo* slo, int32_t R, const double* s_unit,
+                            const int32_t* in_tok, const int32_t* out_tok, const uint8_t* phase,
+                            double qps, double* o_ttft, double* o_tpot, double* o_pe, double* o_comp,
+                            double* o_te, double* o_ps, or_summary* sum) {
+    long capsum = 0;
+    for (int g = 0; g < N; g++) {
+        if (cap[g] < m->min_w || cap[g] > m->max_w) return -2;
+        capsum += cap[g];
+    }
+    if (capsum > B) return -3;
+    for (int i = 0; i < R; i++) {
+        if (in_tok[i] < 1 || out_tok[i] < 1) return -6;
+        if (!(s_unit[i] >= 0) || !isfinite(s_unit[i])) return -1;
+        if (i > 0 && !(s_unit[i] >= s_unit[i - 1])) return -1;
+        if (phase[i] > 1) return -1;
+    }
+    memset(sum, 0, sizeof(*sum));
+    sum->n_req = R;
+    sum->avg_watts = (double)capsum;
+    if (R == 0) return 0;
+
+    int rc = -8;
+    double* a = (double*)malloc(sizeof(double) * (size_t)R);
+    double* pe = (double*)malloc(sizeof(double) * (size_t)R);
+    double* ps = (double*)malloc(sizeof(double) * (size_t)R);
+    double* comp = (double*)malloc(sizeof(double) * (size_t)R);
+    double* tpot = (double*)malloc(sizeof(double) * (size_t)R);
+    cw_t* W = (cw_t*)calloc((size_t)N, sizeof(cw_t));
+    heap_t h = {0};
+    if (!a || !pe || !ps || !comp || !tpot || !W) goto out;
+    for (int g = 0; g < N; g++) {
+        cw_t* w = &W[g];
+        w->q.buf = (int*)malloc(sizeof(int) * (size_t)R); w->q.cap = R;
+        w->pend.buf = (int*)malloc(sizeof(int) * (size_t)R); w->pend.cap = R;
+        w->act_id = (int*)malloc(sizeof(int) * (size_t)m->max_db);
+        w->act_fin = (int*)malloc(sizeof(int) * (size_t)m->max_db);
+        w->c_id = -1;
+        if (!w->q.buf || !w->pend.buf || !w->act_id || !w->act_fin) goto out;
+    }
+    double inv_lam = 1.0 / (qps * (double)N);          /* a2 */
+    for (int i = 0; i < R; i++) a[i] = s_unit[i] * inv_lam;
+    for (int i = 0; i < R; i++)
+        if (heap_push(&h, a[i], K_ARR, i)) goto out;
+
+    int completed = 0;
+    int64_t events = 0;
+    while (completed < R) {
+        if (h.n == 0) { rc = -9; goto out; }
+        double t = h.a[0].t;
+        while (h.n > 0 && h.a[0].t == t) {
+            ev_t e = heap_pop(&h);
+            events++;
+            if (e.kind == K_DSTEP) {
+                cw_t* w = &W[e.key];
+                w->step++;
+                w->in_step = 0;
+                w->at_boundary = 1;
+                int k = 0;
+                while (k < w->n_act) {             /* sequences emitting their last token */
+                    if (w->act_fin[k] == w->step) {
+                        int i = w->act_id[k];
+                        comp[i] = t;
+                        tpot[i] = (t - pe[i]) / (double)(out_tok[i] - 1);
+                        completed++;
+                        w->ctx -= in_tok[i];
+                        w->act_id[k] = w->act_id[w->n_act - 1];
+                        w->act_fin[k] = w->act_fin[w->n_act - 1];
+                        w->n_act--;
+                        w->comp_changed = 1;
+                    } else {
+                        k++;
+                    }
+                }
+                if (w->c_id >= 0) {                /* the step's prefill chunk (A35/A36) */
+                    int i = w->c_id;
+                    w->done_tok += w->c_tok;
+                    w->outstanding -= w->c_tok;
+                    if (w->done_tok == in_tok[i]) {
+                        ring_pop(&w->q);
+                        w->done_tok = 0;
+                        pe[i] = t;
+                        if (out_tok[i] == 1) {
+                            comp[i] = t;
+                            tpot[i] = 0.0;
+                            completed++;
+                        } else {
+                            ring_push(&w->pend, i);
+                        }
+                    }
+                    w->c_id = -1;
+                }
+            } else {                               /* K_ARR (A34) */
+                int i = e.key;
+                int best = 0;
+                for (int g = 1; g < N; g++)
+                    if (W[g].outstanding < W[best].outstanding) best = g;
+                ring_push(&W[best].q, i);
+                W[best].outstanding += in_tok[i];
+            }
+        }
+        /* dispatch after the instant, worker-id order (A10) */
+        for (int g = 0; g < N; g++) {
+            cw_t* w = &W[g];
+            if (w->in_step) { w->at_boundary = 0; continue; }
+            int was_idle = !w->at_boundary;
+            int joined = 0;
+            while (w->n_act < m->max_db && w->pend.len > 0) {
+                int i = ring_pop(&w->pend);
+                w->act_id[w->n_act] = i;
+                w->act_fin[w->n_act] = w->step + (out_tok[i] - 1);
+                w->n_act++;
+                w->ctx += in_tok[i];
+                joined = 1;
+            }
+            if (w->q.len > 0) {
+                int i = ring_at(&w->q, 0);
+                int c = in_tok[i] - w->done_tok;
+                if (c > m->chunk) c = m->chunk;
+                if (w->done_tok == 0) ps[i] = t;
+                double lat = or_prefill_lat(m, c, 1, cap[g]);
+                if (w->n_act > 0) lat = lat + or_decode_lat(m, w->n_act, w->ctx, cap[g]);
+                if (heap_push(&h, t + lat, K_DSTEP, g)) goto out;
+                w->c_id = i;
+                w->c_tok = c;
+                w->in_step = 1;
+                w->seg_valid = 0;
+            } else if (w->n_act > 0) {
+                if (was_idle || joined || w->comp_changed || !w->seg_valid) {
+                    w->t_seg = t;
+                    w->step0 = w->step;
+                    w->L = or_decode_lat(m, w->n_act, w->ctx, cap[g]);
+                    w->seg_valid = 1;
+                }
+                double nb = w->t_seg + (double)(w->step + 1 - w->step0) * w->L;
+                if (heap_push(&h, nb, K_DSTEP, g)) goto out;
+                w->in_step = 1;
+            }
+            w->at_boundary = 0;
+            w->comp_changed = 0;
+        }
+    }
+    {
+        int met = 0, near = 0;
+        double last = 0.0, sq = 0.0, se = 0.0;
+        for (int i = 0; i < R; i++) {
+            sq = sq + (ps[i] - a[i]);
+            se = se + (pe[i] - ps[i]);
+            double tt = pe[i] - a[i];
+            double ts = slo->tpot[phase[i]];
+            if (tt <= slo->ttft && tpot[i] <= ts) met++;
+            if (fabs(tt - slo->ttft) <= 1e-9 * slo->ttft || fabs(tpot[i] - ts) <= 1e-9 * ts) near++;
+            if (i == 0 || comp[i] > last) last = comp[i];
+            if (o_ttft) o_ttft[i] = tt;
+            if (o_tpot) o_tpot[i] = tpot[i];
+            if (o_pe) o_pe[i] = pe[i];
+            if (o_comp) o_comp[i] = comp[i];
+            if (o_te) o_te[i] = pe[i];
+            if (o_ps) o_ps[i] = ps[i];
+        }
+        sum->met = met;
+        sum->near_boundary = near;
+        sum->duration = last - a[0];
+        sum->goodput = sum->duration > 0 ? (double)met / sum->duration : 0.0;
+        sum->events = events;
+        sum->avg_watts = (double)capsum;
+        sum->qps_per_watt = sum->goodput / sum->avg_watts;
+        sum->sum_queue = sq;
+        sum->sum_exec = se;
+    }
+    rc = 0;
+out:
+    if (W) {
+        for (int g = 0; g < N; g++) {
+            free(W[g].q.buf); free(W[g].pend.buf); free(W[g].act_id); free(W[g].act_fin);
+        }
+    }
+    free(W); free(a); free(pe); free(ps); free(comp); free(tpot);
+    free(h.a);
+    return rc;
 }
 
 /* The replay: c.2 (static) + c.3 (dynamic).                                 */
@@ -307,6 +520,9 @@ int or_replay(const or_model* m, int32_t N, const uint8_t* role, const int32_t* 
     if (!m || !role || !cap || !pol || !slo || !sum || N < 2 || N > OR_MAX_GPUS || R < 0) return -1;
     if (!valid_model(m)) return -5;
     if (!(qps > 0) || !(slo->ttft > 0 && slo->tpot[0] > 0 && slo->tpot[1] > 0)) return -1;
+    if (pol->kind == 4)
+        return replay_coalesced(m, N, cap, B, slo, R, s_unit, in_tok, out_tok, phase, qps, o_ttft,
+                                o_tpot, o_pe, o_comp, o_te, o_ps, sum);
     int np = 0;
     long capsum = 0;
     for (int g = 0; g < N; g++) {

@@ -42,10 +42,12 @@ typedef struct {
     int32_t pb_tokens;    /* prefill batch token budget                      */
     int32_t max_db;       /* max decode batch                                */
     int32_t slots;        /* KV transfer request buffer (32)          */
+    int32_t chunk;        /* coalesced mode: prefill chunk tokens (512) */
 } or_model;
 
 typedef struct {
-    int32_t kind;         /* 0 static, 1 dyn-power, 2 dyn-gpu, 3 dyn-both   */
+    int32_t kind;         /* 0 static, 1 dyn-power, 2 dyn-gpu, 3 dyn-both,
+                             4 coalesced (non-disaggregated, chunked prefill) */
     int32_t threshold;    /* Alg.1 THRESHOLD on |Q_P|                        */
     int32_t step_w;       /* MovePower step (W)                              */
     int32_t dec_ceiling_w;/* decode dynamic ceiling (600 W)           */

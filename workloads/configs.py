@@ -20,6 +20,7 @@ DEFAULT_MODEL = {
     "dec_fixed": 0.008, "dec_per_seq": 0.00025, "dec_per_ctx": 0.0,
     "kvb": 131072.0, "bw": 48e9, "ovh": 0.0005,
     "max_pb": 16, "pb_tokens": 16384, "max_db": 64, "slots": 32,
+    "chunk": 512,                                             # S:264 coalesced-mode chunk
 }
 
 # Alg. 1 constants (S:372 defaults; P:294 sub-second tick, P:300 cooldown 2–6 s,
@@ -28,7 +29,8 @@ DEFAULT_POLICY = {
     "kind": 0, "threshold": 8, "step_w": 50, "dec_ceiling_w": 600,
     "cooldown_s": 4.0, "tick_s": 0.25, "window_s": 5.0, "settle_s": 0.3, "reassign_s": 3.0,
 }
-KIND = {"static": 0, "dyn-power": 1, "dyn-gpu": 2, "dyn-both": 3}
+KIND = {"static": 0, "dyn-power": 1, "dyn-gpu": 2, "dyn-both": 3,
+        "coalesced": 4}   # non-disaggregated baseline with chunked prefill
 
 DEFAULT_SLO = {"ttft": 1.0, "tpot": (0.040, 0.040)}    # Fig. 5a
 PHASE_SLO = {"ttft": 1.0, "tpot": (0.040, 0.020)}      # §5.2
