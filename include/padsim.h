@@ -82,7 +82,7 @@ typedef struct { int32_t n; int32_t w[PADSIM_MAX_ANCHORS]; double s[PADSIM_MAX_A
  *   decode_lat(n,C,w)  = (fixed + per_seq*n [+ per_ctx*C]) / s_dec(w)
  *   kv_lat(T)          = overhead + (T*kv_bytes)/fabric_bw                  */
 typedef struct {
-    int32_t min_w, max_w;              /* cap range (400–750 W)          */
+    int32_t min_w, max_w;              /* cap range (400–750 W), max_w − min_w ≤ 511 */
     padsim_curve prefill, decode;
     double prefill_base_rate;          /* tokens/s at min_w, batch 1  (> 0)     */
     double prefill_batch_eff;          /* per extra batch member      (>= 0)    */
@@ -96,10 +96,16 @@ typedef struct {
     int32_t prefill_token_budget;      /* >= 1      (16384)               */
     int32_t max_decode_batch;          /* [1, 256]  (64)                  */
     int32_t transfer_slots;            /* [1, 32]   (32)                  */
+    int32_t prefill_chunk_tokens;      /* >= 1, coalesced mode only (512) */
 } padsim_model;
 
 /* Algorithm 1 constants for one candidate.  kind: 0 static,
- * 1 dyn-power, 2 dyn-gpu, 3 dyn-both.  For kind != 0:
+ * 1 dyn-power, 2 dyn-gpu, 3 dyn-both, 4 coalesced — the
+ * paper's non-disaggregated baseline with chunked prefill (SPEC
+ * S:262–269; readings A33–A37): every GPU serves both phases at its cap,
+ * role[] is ignored, no KV transfer (transfer_end = prefill_end), one engine
+ * step = ≤ prefill_chunk_tokens of the head prompt fused with the active
+ * decode batch.  For kind 1–3:
  * tick_s > 0 (MIN_TIME), settle_s > 0, reassign_s > 0
  * (P:294), cooldown_s >= settle_s, window_s >= 0, power_step_w > 0,
  * decode_ceiling_w ∈ [min_w, max_w], queue_threshold >= 0.        */
@@ -192,8 +198,9 @@ int padsim_replay_kernel_ms(padsim_ctx* ctx, float* ms);
 
 /* Per-kernel device times of the last padsim_run in ms (CUDA events on the
  * run's stream): [0] stage A (static prefill), [1] stage C (static decode),
- * [2] joint replay (dynamic candidates / static when N > 8), which runs on
- * a side stream concurrently with [0]+[1]; 0 if not run.                   */
+ * [2] joint + coalesced replays (dynamic candidates, static when N > 8,
+ * policy kind 4), which start after [0] on a side stream concurrently with
+ * [1]; 0 if not run.                                                       */
 int padsim_kernel_times_ms(padsim_ctx* ctx, float* ms3);
 
 /* ---- SLO scaling, QPS/W, max QPS at 80 % ---------------

@@ -35,6 +35,7 @@ struct DevModel {
     int min_w, max_w, ncap;            // ncap = max_w - min_w + 1
     double rate, eff, dec_fixed, dec_per_seq, dec_per_ctx, kvb, bw, ovh;
     int max_pb, pb_tokens, max_db, slots;
+    int chunk;                         // coalesced mode: prefill chunk tokens
     const double* spre;                // [ncap]  s_pre(w)
     const double* sdec;                // [ncap]  s_dec(w)
     const double* den;                 // [max_pb+1] rate*(1+eff*(b-1))

@@ -237,7 +237,6 @@ struct JReplay {
     int nk;
     long long w_sum;
     double w_acc, w_prev, a0t;
-    double dq_sum, de_sum;   // Fig. 6 decomposition sums
 
     __device__ JReplay(const Plan& p, const TraceView& t, const Scratch& x, const JWork& w)
         : P(p), T(t), X(x), W(w) {}
@@ -330,13 +329,14 @@ struct JReplay {
         int i = W.b0[o];
         const int n = W.b1[o];
         const double bstart = W.tseg[o];      // prefill workers keep the batch start here
+        double bq = 0.0, be = 0.0;            // Fig. 6 decomposition, this batch
         int dec = 0;
         for (int z = 0; z < n; z++) {
             const int nx = LNK(i);
             PE(i) = t;
             dec += T.in_tok[i];
-            dq_sum = dq_sum + (bstart - arr(i));
-            de_sum = de_sum + (t - bstart);
+            bq = bq + (bstart - arr(i));
+            be = be + (t - bstart);
             if (DYN) {
                 const double ttft = t - arr(i);
                 const unsigned char f = (ttft <= P.ttft_slo ? 1 : 0) | (ttft < P.ttft_slo ? 2 : 0);
@@ -359,6 +359,11 @@ struct JReplay {
                 twl++;
             }
             i = nx;
+        }
+        {   // this replay's output slot, recovered from its sweep-counter row
+            const long long r = (long long)(metk - P.sw.rep_met) / kMaxSloSweep;
+            P.sw.rep_sq[r] += bq;
+            P.sw.rep_se[r] += be;
         }
         W.a0[o] -= dec;
         if (!(W.fl[o] & JF_DRAIN)) add_kp(g, -dec);
@@ -725,7 +730,11 @@ struct JReplay {
         a0t = R > 0 ? arr(0) : 0.0;
         w_acc = 0.0;
         w_prev = a0t;
-        dq_sum = de_sum = 0.0;
+        {
+            const long long r = (long long)(metk - P.sw.rep_met) / kMaxSloSweep;
+            P.sw.rep_sq[r] = 0.0;
+            P.sw.rep_se[r] = 0.0;
+        }
         long long events = 0;
         int na = 0;
         double ta = R > 0 ? arr(0) : PAD_INF;
@@ -873,8 +882,6 @@ __global__ void __launch_bounds__(TB) joint_kernel(const __grid_constant__ Plan 
         P.rep_good[r] = res.goodput;
         P.rep_events[r] = res.events;
         P.sw.rep_watts[r] = res.watts;
-        P.sw.rep_sq[r] = rp.dq_sum;
-        P.sw.rep_se[r] = rp.de_sum;
     }
 }
 

@@ -18,6 +18,7 @@
 
 #include "common.cuh"
 #include "controller.cuh"
+#include "coalesced.cuh"
 #include "replay.cuh"
 #include "static_path.cuh"
 #include "dynamic_path.cuh"
@@ -36,7 +37,7 @@ struct padsim_ctx {
     int N = 0, C = 0, Q = 0, S = 0, Rmax = 0, B = 0;
     padsim_model model{};
     padsim_slo slo{};
-    std::vector<int> static_list, dyn_list;
+    std::vector<int> static_list, dyn_list, coal_list;
     std::vector<long long> toff;
     std::vector<int> capsum_h;
     // device buffers
@@ -94,6 +95,9 @@ struct padsim_ctx {
     char* d_scratch_dyn = nullptr;
     Plan plan_static{}, plan_dyn{};
     int grid_static = 0, grid_dyn = 0;
+    Plan plan_coal{};                // coalesced baseline (policy kind 4)
+    int grid_coal = 0;
+    int* d_clist_coal = nullptr;
     size_t smem_static = 0, smem_dyn = 0;
     // host staging for the one-shot API
     padsim_ctrl_state* d_ctl_state = nullptr;
@@ -101,10 +105,8 @@ struct padsim_ctx {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, evA = nullptr, evC = nullptr;
     cudaEvent_t evJ0 = nullptr, evJ1 = nullptr;
     cudaStream_t side = nullptr;     // joint kernel runs concurrently with stages A/C
-    cudaStream_t sideA = nullptr;    // stage A chunks run ahead of stage C chunks
-    cudaEvent_t evAc[4] = {nullptr, nullptr, nullptr, nullptr};
     cudaEvent_t evC0 = nullptr;
-    int n_chunks = 1;
+    bool j_with_a = false;           // experiment knob: joint replays next to stage A
     bool ev_recorded = false;
     // factorized static path (N <= 8)
     bool fact = false;
@@ -179,6 +181,7 @@ static void free_plan(padsim_ctx* ctx) {
     ctx->j8[0] = ctx->j8[1] = false;
     ctx->static_list.clear();
     ctx->dyn_list.clear();
+    ctx->coal_list.clear();
     for (auto& r : ctx->d_rec) r = nullptr;
 }
 
@@ -399,6 +402,7 @@ __global__ void controller_kernel(const padsim_policy pol, const int min_w, cons
 static int validate_model(padsim_ctx* ctx, const padsim_model* m) {
     if (!m) return fail(ctx, PADSIM_EINVAL, "model is NULL");
     if (!(m->min_w > 0 && m->min_w < m->max_w)) return fail(ctx, PADSIM_EMODEL, "min_w/max_w");
+    if (m->max_w - m->min_w > 511) return fail(ctx, PADSIM_EMODEL, "cap range wider than 511 W");
     const padsim_curve* cs[2] = {&m->prefill, &m->decode};
     for (const padsim_curve* c : cs) {
         if (c->n < 2 || c->n > PADSIM_MAX_ANCHORS) return fail(ctx, PADSIM_EMODEL, "curve anchor count");
@@ -418,15 +422,15 @@ static int validate_model(padsim_ctx* ctx, const padsim_model* m) {
     if (m->max_prefill_batch < 1 || m->max_prefill_batch > PADSIM_MAX_PREFILL_BATCH ||
         m->prefill_token_budget < 1 || m->max_decode_batch < 1 ||
         m->max_decode_batch > PADSIM_MAX_DECODE_BATCH || m->transfer_slots < 1 ||
-        m->transfer_slots > PADSIM_MAX_SLOTS)
-        return fail(ctx, PADSIM_EMODEL, "batch / slot limits");
+        m->transfer_slots > PADSIM_MAX_SLOTS || m->prefill_chunk_tokens < 1)
+        return fail(ctx, PADSIM_EMODEL, "batch / slot / chunk limits");
     return PADSIM_OK;
 }
 
 static int validate_policy(padsim_ctx* ctx, const padsim_policy* p, const padsim_model* m, int N,
                            int B) {
-    if (p->kind < 0 || p->kind > 3) return fail(ctx, PADSIM_EINVAL, "policy kind");
-    if (p->kind == 0) return PADSIM_OK;
+    if (p->kind < 0 || p->kind > 4) return fail(ctx, PADSIM_EINVAL, "policy kind");
+    if (p->kind == 0 || p->kind == 4) return PADSIM_OK;
     if (!(p->tick_s > 0 && p->settle_s > 0 && p->reassign_s > 0 && p->cooldown_s >= p->settle_s &&
           p->window_s >= 0 && p->power_step_w > 0 && p->queue_threshold >= 0 &&
           p->decode_ceiling_w >= m->min_w && p->decode_ceiling_w <= m->max_w &&
@@ -571,8 +575,11 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
         const size_t wbytes = kCWorkBytes + (ctxm ? kCWorkCtxBytes : 0);
         const size_t bbytes = (size_t)kNW * (wheel / 32) * kThreads * sizeof(unsigned);
         F.bits_in_smem = wheel <= 256 ? 1 : 0;
+        if (getenv("PADSIM_BITS_GLOBAL")) F.bits_in_smem = 0;          // experiment knob
+        F.c_prefetch = getenv("PADSIM_NO_PREFETCH") ? 0 : 1;            // experiment knob
         F.smem_trace = 0;
-        ctx->fC_smem = wbytes + (F.bits_in_smem ? bbytes : 0);
+        F.c_off_sdec = wbytes + (F.bits_in_smem ? bbytes : 0);
+        ctx->fC_smem = F.c_off_sdec + (size_t)F.m.ncap * sizeof(double);
         const void* fn = ctxm ? (idx16 ? (const void*)stageC_kernel<true, unsigned short>
                                        : (const void*)stageC_kernel<true, unsigned>)
                               : (idx16 ? (const void*)stageC_kernel<false, unsigned short>
@@ -594,11 +601,7 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
         AL(scr, (size_t)grid * per_cta);
         F.scrC = scr;
         ctx->fC_grid = (int)grid;
-        // pipeline stage A ahead of stage C in trace chunks when stage A alone has
-        // enough replays to fill the GPU (else it is latency-bound and splitting
-        // only serialises it)
-        ctx->n_chunks = GQS >= 8LL * ctx->n_sm * kThreads ? std::min(S, 4) : 1;
-        if (const char* e = getenv("PADSIM_CHUNKS")) ctx->n_chunks = std::max(1, std::min(S, atoi(e)));
+        ctx->j_with_a = getenv("PADSIM_JOINT_WITH_A") != nullptr;
     }
     F.rep_met = ctx->d_rep_met; F.rep_near = ctx->d_rep_near; F.rep_dur = ctx->d_rep_dur;
     F.rep_good = ctx->d_rep_good; F.rep_events = ctx->d_rep_events;
@@ -650,8 +653,6 @@ void padsim_destroy(padsim_ctx* ctx) {
     if (ctx->evJ0) cudaEventDestroy(ctx->evJ0);
     if (ctx->evJ1) cudaEventDestroy(ctx->evJ1);
     if (ctx->side) cudaStreamDestroy(ctx->side);
-    if (ctx->sideA) cudaStreamDestroy(ctx->sideA);
-    for (auto& e : ctx->evAc) if (e) cudaEventDestroy(e);
     if (ctx->evC0) cudaEventDestroy(ctx->evC0);
     delete ctx;
 }
@@ -726,7 +727,8 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
             }
             cs += w;
         }
-        if (np < 1 || np > N - 1) {
+        const bool coal = cands->policy[c].kind == 4;     // roles ignored (A33)
+        if (!coal && (np < 1 || np > N - 1)) {
             if (bad_index) *bad_index = c;
             return fail(ctx, PADSIM_EROLE, "need >= 1 prefill and >= 1 decode GPU");
         }
@@ -764,7 +766,10 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
     ctx->flags = flags;
     ctx->capsum_h = capsum;
     ctx->toff = toff;
-    for (int c = 0; c < C; c++) (cands->policy[c].kind == 0 ? ctx->static_list : ctx->dyn_list).push_back(c);
+    for (int c = 0; c < C; c++) {
+        const int k = cands->policy[c].kind;
+        (k == 0 ? ctx->static_list : k == 4 ? ctx->coal_list : ctx->dyn_list).push_back(c);
+    }
 
     // host staging of the padded SoA trace arrays
     std::vector<double> hs(tot, 0.0);
@@ -801,6 +806,7 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
     AL(ctx->d_qps, n_qps);
     AL(ctx->d_clist_static, std::max<size_t>(1, ctx->static_list.size()));
     AL(ctx->d_clist_dyn, std::max<size_t>(1, ctx->dyn_list.size()));
+    AL(ctx->d_clist_coal, std::max<size_t>(1, ctx->coal_list.size()));
     AL(ctx->d_spre, ncap);
     AL(ctx->d_sdec, ncap);
     AL(ctx->d_den, model->max_prefill_batch + 1);
@@ -868,6 +874,9 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
                       cudaMemcpyHostToDevice));
     if (!ctx->dyn_list.empty())
         CK(cudaMemcpy(ctx->d_clist_dyn, ctx->dyn_list.data(), sizeof(int) * ctx->dyn_list.size(),
+                      cudaMemcpyHostToDevice));
+    if (!ctx->coal_list.empty())
+        CK(cudaMemcpy(ctx->d_clist_coal, ctx->coal_list.data(), sizeof(int) * ctx->coal_list.size(),
                       cudaMemcpyHostToDevice));
     tables_kernel<<<std::max(1, ctx->n_sm), 256>>>(*model, ctx->d_spre, ctx->d_sdec, ctx->d_den,
                                                     ctx->d_ltab, ctx->d_in, ctx->d_kv, tot);
@@ -977,9 +986,58 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
         (dyn ? ctx->grid_dyn : ctx->grid_static) = (int)gridj;
         (dyn ? ctx->smem_dyn : ctx->smem_static) = jb;
     }
+    // coalesced baseline replays (policy kind 4): one warp per CTA
+    std::memset(&ctx->plan_coal, 0, sizeof(Plan));
+    if (!ctx->coal_list.empty()) {
+        Plan& P = ctx->plan_coal;
+        P.m.min_w = model->min_w; P.m.max_w = model->max_w; P.m.ncap = ncap;
+        P.m.rate = model->prefill_base_rate; P.m.eff = model->prefill_batch_eff;
+        P.m.dec_fixed = model->decode_fixed_s; P.m.dec_per_seq = model->decode_per_seq_s;
+        P.m.dec_per_ctx = model->decode_per_ctx_tok_s;
+        P.m.max_db = model->max_decode_batch; P.m.chunk = model->prefill_chunk_tokens;
+        P.m.spre = ctx->d_spre; P.m.sdec = ctx->d_sdec; P.m.den = ctx->d_den; P.m.ltab = ctx->d_ltab;
+        P.N = N; P.C = C; P.Q = n_qps; P.S = n_traces; P.Rmax = Rmax; P.B = B;
+        P.toff = ctx->d_toff; P.nreq = ctx->d_nreq; P.s_unit = ctx->d_s_unit; P.kv = ctx->d_kv;
+        P.in_tok = ctx->d_in; P.out_tok = ctx->d_out; P.phase = ctx->d_phase;
+        P.role = ctx->d_role; P.cap = ctx->d_cap; P.pol = ctx->d_pol; P.qps = ctx->d_qps;
+        P.ttft_slo = slo->ttft_s; P.tpot_slo0 = slo->tpot_s[0]; P.tpot_slo1 = slo->tpot_s[1];
+        P.clist = ctx->d_clist_coal;
+        P.n_clist = (int)ctx->coal_list.size();
+        P.rep_met = ctx->d_rep_met; P.rep_near = ctx->d_rep_near; P.rep_dur = ctx->d_rep_dur;
+        P.rep_good = ctx->d_rep_good; P.rep_events = ctx->d_rep_events;
+        if (flags & PADSIM_RECORDS) {
+            P.rec_ttft = ctx->d_rec[0]; P.rec_tpot = ctx->d_rec[1]; P.rec_pe = ctx->d_rec[2];
+            P.rec_comp = ctx->d_rec[3]; P.rec_te = ctx->d_rec[4];
+        }
+        const size_t R = (size_t)std::max(Rmax, 1);
+        size_t off = 0;
+        auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~(size_t)255; return o; };
+        P.off_link = take(R * 32 * sizeof(int));
+        P.off_pe = take(R * 32 * sizeof(double));
+        P.off_jw = take(coal_worker_bytes(N));
+        P.off_heads = take((size_t)N * model->max_decode_batch * 32 * sizeof(int));   // act_id
+        P.off_bits = take((size_t)N * model->max_decode_batch * 32 * sizeof(int));    // act_fin
+        P.warp_bytes = off;
+        const long long U = (long long)n_traces * n_qps * P.n_clist;
+        const long long items = (U + 31) / 32;
+        int occ = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, coalesced_kernel<false>, 32, 0));
+        occ = std::max(occ, 1);
+        size_t frc = 0, tmc = 0;
+        CK(cudaMemGetInfo(&frc, &tmc));
+        const long long cap_ctas = std::max<long long>(1, (long long)((tmc / 10) / P.warp_bytes));
+        long long gridc = std::min<long long>(items, (long long)ctx->n_sm * occ);
+        gridc = std::max<long long>(1, std::min(gridc, cap_ctas));
+        char* scr = nullptr;
+        AL(scr, (size_t)gridc * P.warp_bytes);
+        P.scratch = scr;
+        P.scratch_per_cta = P.warp_bytes;
+        ctx->grid_coal = (int)gridc;
+    }
 #undef AL
     ctx->plan_static.sw = ctx->sweep;
     ctx->plan_dyn.sw = ctx->sweep;
+    ctx->plan_coal.sw = ctx->sweep;
     ctx->fplan.sw = ctx->sweep;
     CK(cudaDeviceSynchronize());
     ctx->planned = true;
@@ -1000,16 +1058,29 @@ int padsim_run(padsim_ctx* ctx, void* stream) {
         CK(cudaEventCreate(&ctx->evJ0));
         CK(cudaEventCreate(&ctx->evJ1));
         CK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
-        CK(cudaStreamCreateWithFlags(&ctx->sideA, cudaStreamNonBlocking));
-        for (auto& e : ctx->evAc) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         CK(cudaEventCreate(&ctx->evC0));
     }
     CK(cudaEventRecord(ctx->ev0, st));
-    // fork: the joint replay (dynamic candidates, or static when N > 8) runs on a
-    // side stream concurrently with the factorized static stages
-    const bool any_joint = ctx->plan_dyn.n_clist > 0 || ctx->plan_static.n_clist > 0;
+    // Schedule (measured on cfg 4): stage A runs first on the whole GPU; the joint
+    // replays (dynamic candidates, static ones when N > 8, coalesced baselines) then
+    // run on a side stream concurrently with stage C.  Stage C's resident grid is
+    // capped by shared memory (3 CTAs/SM), leaving registers and issue slots that
+    // the latency-bound joint warps fill; running them next to stage A instead
+    // starved stage A of registers and serialised the two stages.
+    if (ctx->fact) {
+        FPlan F = ctx->fplan;
+        F.s_begin = 0;
+        F.s_count = ctx->S;
+        const int ga = F.a_blocks_per_trace * F.s_count;
+        if (ctx->fA_tb == kThreads) stageA_kernel<kThreads><<<ga, kThreads, ctx->fA_smem, st>>>(F);
+        else stageA_kernel<32><<<ga, 32, ctx->fA_smem, st>>>(F);
+        CK(cudaGetLastError());
+    }
+    CK(cudaEventRecord(ctx->evA, st));
+    const bool any_joint = ctx->plan_dyn.n_clist > 0 || ctx->plan_static.n_clist > 0 ||
+                           ctx->plan_coal.n_clist > 0;
     cudaStream_t js = ctx->fact && any_joint ? ctx->side : st;
-    if (js != st) CK(cudaStreamWaitEvent(js, ctx->ev0, 0));
+    if (js != st) CK(cudaStreamWaitEvent(js, ctx->j_with_a ? ctx->ev0 : ctx->evA, 0));
     CK(cudaEventRecord(ctx->evJ0, js));
     for (int dyn = 0; dyn < 2; dyn++) {
         const Plan& P = dyn ? ctx->plan_dyn : ctx->plan_static;
@@ -1029,48 +1100,30 @@ int padsim_run(padsim_ctx* ctx, void* stream) {
         }
         CK(cudaGetLastError());
     }
+    if (ctx->plan_coal.n_clist > 0) {
+        if (ctx->model.decode_per_ctx_tok_s != 0.0)
+            coalesced_kernel<true><<<ctx->grid_coal, 32, 0, js>>>(ctx->plan_coal);
+        else
+            coalesced_kernel<false><<<ctx->grid_coal, 32, 0, js>>>(ctx->plan_coal);
+        CK(cudaGetLastError());
+    }
     CK(cudaEventRecord(ctx->evJ1, js));
+    CK(cudaEventRecord(ctx->evC0, st));
     if (ctx->fact) {
-        // stage A chunk j runs on sideA while stage C consumes chunk j-1 on st
         CK(cudaMemsetAsync(ctx->d_workC, 0, (size_t)ctx->S * sizeof(unsigned), st));
-        CK(cudaStreamWaitEvent(ctx->sideA, ctx->ev0, 0));
-        const int nch = ctx->n_chunks;
-        const int per = (ctx->S + nch - 1) / nch;
+        FPlan F = ctx->fplan;
+        F.s_begin = 0;
+        F.s_count = ctx->S;
         const bool cm = ctx->model.decode_per_ctx_tok_s != 0.0;
-        for (int j = 0; j < nch; j++) {
-            FPlan F = ctx->fplan;
-            F.s_begin = j * per;
-            F.s_count = std::min(per, ctx->S - F.s_begin);
-            if (F.s_count <= 0) break;
-            const int ga = F.a_blocks_per_trace * F.s_count;
-            if (ctx->fA_tb == kThreads) stageA_kernel<kThreads><<<ga, kThreads, ctx->fA_smem, ctx->sideA>>>(F);
-            else stageA_kernel<32><<<ga, 32, ctx->fA_smem, ctx->sideA>>>(F);
-            CK(cudaGetLastError());
-            CK(cudaEventRecord(ctx->evAc[j], ctx->sideA));
+        const int gc = ctx->fC_grid;
+        if (ctx->fC_idx16) {
+            if (cm) stageC_kernel<true, unsigned short><<<gc, kThreads, ctx->fC_smem, st>>>(F);
+            else stageC_kernel<false, unsigned short><<<gc, kThreads, ctx->fC_smem, st>>>(F);
+        } else {
+            if (cm) stageC_kernel<true, unsigned><<<gc, kThreads, ctx->fC_smem, st>>>(F);
+            else stageC_kernel<false, unsigned><<<gc, kThreads, ctx->fC_smem, st>>>(F);
         }
-        CK(cudaEventRecord(ctx->evA, ctx->sideA));
-        for (int j = 0; j < nch; j++) {
-            FPlan F = ctx->fplan;
-            F.s_begin = j * per;
-            F.s_count = std::min(per, ctx->S - F.s_begin);
-            if (F.s_count <= 0) break;
-            CK(cudaStreamWaitEvent(st, ctx->evAc[j], 0));
-            if (j == 0) CK(cudaEventRecord(ctx->evC0, st));
-            // every chunk gets the full resident grid (CTAs round-robin over the
-            // chunk's traces, warps pull work items per trace)
-            const int gc = ctx->fC_grid;
-            if (ctx->fC_idx16) {
-                if (cm) stageC_kernel<true, unsigned short><<<gc, kThreads, ctx->fC_smem, st>>>(F);
-                else stageC_kernel<false, unsigned short><<<gc, kThreads, ctx->fC_smem, st>>>(F);
-            } else {
-                if (cm) stageC_kernel<true, unsigned><<<gc, kThreads, ctx->fC_smem, st>>>(F);
-                else stageC_kernel<false, unsigned><<<gc, kThreads, ctx->fC_smem, st>>>(F);
-            }
-            CK(cudaGetLastError());
-        }
-    } else {
-        CK(cudaEventRecord(ctx->evA, st));
-        CK(cudaEventRecord(ctx->evC0, st));
+        CK(cudaGetLastError());
     }
     CK(cudaEventRecord(ctx->evC, st));
     if (js != st) CK(cudaStreamWaitEvent(st, ctx->evJ1, 0));   // join
@@ -1144,6 +1197,7 @@ int padsim_set_slo_sweep(padsim_ctx* ctx, const padsim_slo* slos, int32_t n_slo)
     }
     ctx->plan_static.sw = ctx->sweep;
     ctx->plan_dyn.sw = ctx->sweep;
+    ctx->plan_coal.sw = ctx->sweep;
     ctx->fplan.sw = ctx->sweep;
     return PADSIM_OK;
 }
@@ -1214,7 +1268,7 @@ int padsim_kernel_times_ms(padsim_ctx* ctx, float* ms3) {
     if (!ctx->ev_recorded) return fail(ctx, PADSIM_EINVAL, "no run recorded");
     CK(cudaSetDevice(ctx->device));
     CK(cudaEventSynchronize(ctx->ev1));
-    CK(cudaEventElapsedTime(&ms3[0], ctx->ev0, ctx->evA));   // stage A span (its own stream)
+    CK(cudaEventElapsedTime(&ms3[0], ctx->ev0, ctx->evA));
     CK(cudaEventElapsedTime(&ms3[1], ctx->evC0, ctx->evC));
     CK(cudaEventElapsedTime(&ms3[2], ctx->evJ0, ctx->evJ1));
     return PADSIM_OK;

@@ -110,6 +110,8 @@ struct FPlan {
     size_t c_warp_bytes, c_off_heads, c_off_bits;
     int wheel;              // decode timing wheel size (power of 2 ≥ max out_tok, ≥ 32)
     int bits_in_smem;       // wheel occupancy bitmap in shared memory (wheel ≤ 256)
+    size_t c_off_sdec;      // byte offset of the s_dec(w) table in shared memory
+    int c_prefetch;         // prefetch the completion record into L2 at decode join
     int smem_trace;
     // outputs (r = (c*Q + q)*S + s)
     int* rep_met;
@@ -460,6 +462,12 @@ __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant_
             bstride = 32;
         }
     }
+    // s_dec(w) for every cap in shared memory: a decode segment's step latency is
+    // (fixed + per_seq·n) / s_dec(d) computed in place (the same expression as the
+    // a3 table, so bit-identical) instead of a dependent global table load
+    double* sdt = (double*)(smem + P.c_off_sdec);
+    for (int i = tid; i < P.m.ncap; i += kThreads) sdt[i] = P.m.sdec[i];
+    __syncthreads();
     const int s = P.s_begin + blockIdx.x % P.s_count;
     const long long off = P.toff[s];
     const int R = P.nreq[s];
@@ -482,6 +490,11 @@ __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant_
         const SRec* recs = P.st_rec + sb;
         const SHot* hots = P.st_hot + sb;
         const long long rb = P.rec_ttft ? r * P.Rmax : -1;
+        // decode cap indices of this candidate, 9 bits per worker (ncap ≤ 512)
+        unsigned long long dcx = 0ull;
+#pragma unroll
+        for (int w = 0; w < kNW; w++)
+            dcx |= (unsigned long long)(P.cc_dcap[cc * kNW + w] - P.m.min_w) << (9 * w);
         double tnext[kNW];
         int ld[kNW];                       // routing load: active + pending (A13)
 #pragma unroll
@@ -629,6 +642,7 @@ __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant_
                     qn--;
                     if (qn > 0) h = (int)link[(size_t)kk * 32];
                     const int out = hots[kk].meta & 0x7fffffff;
+                    if (P.c_prefetch) asm volatile("prefetch.global.L2 [%0];" :: "l"(recs + kk));
                     const int fin = step + (out - 1);
                     const int b = fin & Wm;
                     unsigned* wp = bw + (size_t)(b >> 5) * bstride;
@@ -655,14 +669,10 @@ __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant_
                     if (was_idle || joined || ((touched >> (w + 16)) & 1u)) {
                         ts0 = t;
                         s0 = step;
-                        const int cix = P.cc_dcap[cc * kNW + w] - P.m.min_w;
-                        if (CTX) {
-                            double xv = P.m.dec_fixed + P.m.dec_per_seq * (double)n;
-                            xv = xv + P.m.dec_per_ctx * (double)W.ctx[o];
-                            L = xv / P.m.sdec[cix];
-                        } else {
-                            L = P.m.ltab[(size_t)cix * max_db + (n - 1)];
-                        }
+                        const int cix = (int)((dcx >> (9 * w)) & 511u);
+                        double xv = P.m.dec_fixed + P.m.dec_per_seq * (double)n;
+                        if (CTX) xv = xv + P.m.dec_per_ctx * (double)W.ctx[o];
+                        L = xv / sdt[cix];
                         W.tseg[o] = ts0; W.st0[o] = s0; W.Ls[o] = L;
                     }
                     W.mfin[o] = mf;
