@@ -86,6 +86,7 @@ struct Plan {
     int wheel;                         // wheel size: power of 2 ≥ max out_tok, ≥ 32
     size_t warp_bytes;
     int smem_trace;                    // stage the trace in shared memory (TMA bulk)
+    float sync_win;                    // lane clock window, mean inter-arrival times (0 = off)
     size_t smem_trace_bytes;
 };
 

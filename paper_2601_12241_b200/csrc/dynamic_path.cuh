@@ -183,6 +183,20 @@ __host__ __device__ constexpr size_t j_work_bytes() { return (size_t)kJG * TB * 
 
 enum : unsigned char { JF_DRAIN = 1, JF_DIRTY = 2 };
 
+// dynamic shared memory of the joint kernel (same base as the kernel's smem[])
+extern __shared__ __align__(128) unsigned char joint_dyn_smem[];
+
+template <int NG, int TB>
+__host__ __device__ constexpr size_t joint_smem_base() {
+    return NG == 8 ? j_work_bytes<TB>() : (size_t)NG * TB * (sizeof(double) + 2 * sizeof(int));
+}
+// + the per-thread Fig. 6 decomposition accumulators (2 doubles)
+template <int NG, int TB>
+__host__ __device__ constexpr size_t joint_smem_bytes() {
+    return ((joint_smem_base<NG, TB>() + 15) & ~(size_t)15) + 2 * TB * sizeof(double);
+}
+
+
 template <typename Mask>
 struct JCtlView {
     const JWork* W;
@@ -217,8 +231,8 @@ struct JReplay {
     int* tti;
     int* heads;          // [(g*wheel + b)*32]
     unsigned* bits;      // [(g*wheel/32 + k)*32]
-    double* wts;         // TTFT window stamps [k*32]
-    unsigned char* wtf;  // TTFT window flags (≤ SLO, < SLO) [k*32]
+    double* wts;         // TTFT window stamps [k], per-lane contiguous (FIFO walk)
+    unsigned char* wtf;  // TTFT window flags (≤ SLO, < SLO) [k]
     int Wh, Wm, nwords;
     int tbusy, mk, mid, twh, twt, twl;
     double mte;
@@ -277,8 +291,8 @@ struct JReplay {
         if (DYN) {
             const unsigned char f = (tpot <= P.tpot_slo0 ? 1 : 0) | (tpot < P.tpot_slo0 ? 2 : 0) |
                                     (tpot <= P.tpot_slo1 ? 4 : 0) | (tpot < P.tpot_slo1 ? 8 : 0);
-            X.tst[(size_t)w_ph * 32] = t;
-            X.tfl[(size_t)w_ph * 32] = f;
+            X.tst[w_ph] = t;
+            X.tfl[w_ph] = f;
             w_ph++;
             w_ple0 += f & 1; w_plt0 += (f >> 1) & 1; w_ple1 += (f >> 2) & 1; w_plt1 += (f >> 3) & 1;
         }
@@ -340,8 +354,8 @@ struct JReplay {
             if (DYN) {
                 const double ttft = t - arr(i);
                 const unsigned char f = (ttft <= P.ttft_slo ? 1 : 0) | (ttft < P.ttft_slo ? 2 : 0);
-                wts[(size_t)w_th * 32] = t;
-                wtf[(size_t)w_th * 32] = f;
+                wts[w_th] = t;
+                wtf[w_th] = f;
                 w_th++;
                 w_tle += f & 1;
                 w_tlt += f >> 1;
@@ -360,10 +374,11 @@ struct JReplay {
             }
             i = nx;
         }
-        {   // this replay's output slot, recovered from its sweep-counter row
-            const long long r = (long long)(metk - P.sw.rep_met) / kMaxSloSweep;
-            P.sw.rep_sq[r] += bq;
-            P.sw.rep_se[r] += be;
+        {   // per-thread accumulators in shared memory (no extra registers)
+            double* acc = (double*)(joint_dyn_smem + ((joint_smem_base<NG, TB>() + 15) & ~(size_t)15)) +
+                          threadIdx.x;
+            acc[0] = acc[0] + bq;
+            acc[TB] = acc[TB] + be;
         }
         W.a0[o] -= dec;
         if (!(W.fl[o] & JF_DRAIN)) add_kp(g, -dec);
@@ -569,14 +584,14 @@ struct JReplay {
         if ((t - last_move) > pol.cooldown_s) {
             acted = 1;
             const double lo = t - pol.window_s;
-            while (w_tlo < w_th && wts[(size_t)w_tlo * 32] < lo) {
-                const unsigned char f = wtf[(size_t)w_tlo * 32];
+            while (w_tlo < w_th && wts[w_tlo] < lo) {
+                const unsigned char f = wtf[w_tlo];
                 w_tle -= f & 1;
                 w_tlt -= f >> 1;
                 w_tlo++;
             }
-            while (w_plo < w_ph && X.tst[(size_t)w_plo * 32] < lo) {
-                const unsigned char f = X.tfl[(size_t)w_plo * 32];
+            while (w_plo < w_ph && X.tst[w_plo] < lo) {
+                const unsigned char f = X.tfl[w_plo];
                 w_ple0 -= f & 1; w_plt0 -= (f >> 1) & 1; w_ple1 -= (f >> 2) & 1; w_plt1 -= (f >> 3) & 1;
                 w_plo++;
             }
@@ -674,8 +689,8 @@ struct JReplay {
             k = cooldown_tick(k0);           // no tick before it can act, whatever happens
         } else {
             k = tick_at_or_after(next_event, k0);
-            if (w_tlo < w_th) k = min(k, expiry_tick(wts[(size_t)w_tlo * 32], k0));
-            if (w_plo < w_ph) k = min(k, expiry_tick(X.tst[(size_t)w_plo * 32], k0));
+            if (w_tlo < w_th) k = min(k, expiry_tick(wts[w_tlo], k0));
+            if (w_plo < w_ph) k = min(k, expiry_tick(X.tst[w_plo], k0));
         }
         if (k > k0 && k != 0x7fffffffffffffffLL) {
             tick_k = k;
@@ -731,19 +746,29 @@ struct JReplay {
         w_acc = 0.0;
         w_prev = a0t;
         {
-            const long long r = (long long)(metk - P.sw.rep_met) / kMaxSloSweep;
-            P.sw.rep_sq[r] = 0.0;
-            P.sw.rep_se[r] = 0.0;
+            double* acc = (double*)(joint_dyn_smem + ((joint_smem_base<NG, TB>() + 15) & ~(size_t)15)) +
+                          threadIdx.x;
+            acc[0] = 0.0;
+            acc[TB] = 0.0;
         }
         long long events = 0;
         int na = 0;
         double ta = R > 0 ? arr(0) : PAD_INF;
+        // keep the simulated clocks of a warp's lanes within sync_win mean
+        // inter-arrival times (same trace → shared cache lines); scheduling only,
+        // results are independent of it (see stageC_kernel)
+        const float win = P.sync_win > 0.f ? (float)((double)P.sync_win * inv_lam) : 0.f;
         while (completed < R) {
             double t = tab.tmin(ta < mte ? ta : mte);
             if (DYN) {
                 t = tick_t < t ? tick_t : t;
                 t = settle_t < t ? settle_t : t;
                 t = flip_t < t ? flip_t : t;
+            }
+            if (win > 0.f) {
+                const float tf = (float)t;
+                const unsigned mn = __reduce_min_sync(__activemask(), __float_as_uint(tf));
+                if (tf > __uint_as_float(mn) + win) continue;
             }
             events++;
             touched = 0;
@@ -801,7 +826,7 @@ struct JReplay {
 
 // CTAs bound to one trace (s = blockIdx.x mod S); warps pull 32-replay items.
 template <bool DYN, int TB, int NG>
-__global__ void __launch_bounds__(TB) joint_kernel(const __grid_constant__ Plan P) {
+__global__ void __launch_bounds__(TB) __maxnreg__(TB == 32 ? 232 : 168) joint_kernel(const __grid_constant__ Plan P) {
     extern __shared__ __align__(128) unsigned char smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     char* wbase = P.scratch + ((size_t)blockIdx.x * (TB / 32) + warp) * P.warp_bytes;
@@ -839,8 +864,10 @@ __global__ void __launch_bounds__(TB) joint_kernel(const __grid_constant__ Plan 
     X.pe = (double*)(wbase + P.off_pe) + lane;
     X.mem = nullptr;
     X.ordt = nullptr;
-    X.tst = DYN ? (double*)(wbase + P.off_tst) + lane : nullptr;
-    X.tfl = DYN ? (unsigned char*)(wbase + P.off_tfl) + lane : nullptr;
+    // window FIFOs are appended and expired in order: per-lane contiguous, so a
+    // lane's consecutive stamps share cache lines
+    X.tst = DYN ? (double*)(wbase + P.off_tst) + (size_t)lane * P.Rmax : nullptr;
+    X.tfl = DYN ? (unsigned char*)(wbase + P.off_tfl) + (size_t)lane * P.Rmax : nullptr;
     double* tte = (double*)(wbase + P.off_tte) + lane;
     int* tti = (int*)(wbase + P.off_tti) + lane;
     const int s = blockIdx.x % P.S;
@@ -873,8 +900,8 @@ __global__ void __launch_bounds__(TB) joint_kernel(const __grid_constant__ Plan 
         rp.tti = tti;
         rp.heads = (int*)(wbase + P.off_heads) + lane;
         rp.bits = (unsigned*)(wbase + P.off_bits) + lane;
-        rp.wts = DYN ? (double*)(wbase + P.off_wts) + lane : nullptr;
-        rp.wtf = DYN ? (unsigned char*)(wbase + P.off_wtf) + lane : nullptr;
+        rp.wts = DYN ? (double*)(wbase + P.off_wts) + (size_t)lane * P.Rmax : nullptr;
+        rp.wtf = DYN ? (unsigned char*)(wbase + P.off_wtf) + (size_t)lane * P.Rmax : nullptr;
         const ReplayResult res = rp.run(c, q, P.rec_ttft ? r * P.Rmax : -1);
         P.rep_met[r] = res.met;
         P.rep_near[r] = res.near;
@@ -882,13 +909,14 @@ __global__ void __launch_bounds__(TB) joint_kernel(const __grid_constant__ Plan 
         P.rep_good[r] = res.goodput;
         P.rep_events[r] = res.events;
         P.sw.rep_watts[r] = res.watts;
+        {
+            const double* acc = (const double*)(smem + ((joint_smem_base<NG, TB>() + 15) & ~(size_t)15)) + tid;
+            P.sw.rep_sq[r] = acc[0];
+            P.sw.rep_se[r] = acc[TB];
+        }
     }
 }
 
-template <int NG, int TB>
-__host__ __device__ constexpr size_t joint_smem_bytes() {
-    return NG == 8 ? j_work_bytes<TB>() : (size_t)NG * TB * (sizeof(double) + 2 * sizeof(int));
-}
 constexpr size_t joint_global_bytes_per_warp(int NG) {   // per-GPU SoA for NG = 64
     return NG == 8 ? 0 : (size_t)NG * 32 * (2 * sizeof(double) + 13 * sizeof(int) + 1);
 }

@@ -577,6 +577,8 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
         F.bits_in_smem = wheel <= 256 ? 1 : 0;
         if (getenv("PADSIM_BITS_GLOBAL")) F.bits_in_smem = 0;          // experiment knob
         F.c_prefetch = getenv("PADSIM_NO_PREFETCH") ? 0 : 1;            // experiment knob
+        F.sync_win = 16.f;
+        if (const char* e = getenv("PADSIM_SYNC_WIN")) F.sync_win = (float)atof(e);   // experiment knob
         F.smem_trace = 0;
         F.c_off_sdec = wbytes + (F.bits_in_smem ? bbytes : 0);
         ctx->fC_smem = F.c_off_sdec + (size_t)F.m.ncap * sizeof(double);
@@ -950,6 +952,8 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
         ctx->d_workJ[dyn] = d_wj;
         P.work = d_wj;
         P.smem_trace = 0;
+        P.sync_win = 16.f;
+        if (const char* e = getenv("PADSIM_SYNC_WIN")) P.sync_win = (float)atof(e);   // experiment knob
         const long long UJ = (long long)n_traces * n_qps * P.n_clist;
         const int tbj = (NG == 8 && UJ >= (long long)ctx->n_sm * 3 * kThreads) ? kThreads : 32;
         ctx->j_tb[dyn] = tbj;

@@ -33,8 +33,8 @@ struct Scratch {
     double* pe;            // [i*32]
     int2* mem;             // [(g*max_db + k)*32]  {fin, id}
     int* ordt;             // [k*32] TTFT window: request ids in prefill-end order
-    double* tst;           // [k*32] TPOT window: completion stamps
-    unsigned char* tfl;    // [k*32] TPOT window: flags (le0, lt0, le1, lt1)
+    double* tst;           // [k] per lane (lane·Rmax + k) TPOT window: completion stamps
+    unsigned char* tfl;    // [k] per lane, TPOT window: flags (le0, lt0, le1, lt1)
 };
 
 struct ReplayResult {

@@ -112,6 +112,7 @@ struct FPlan {
     int bits_in_smem;       // wheel occupancy bitmap in shared memory (wheel ≤ 256)
     size_t c_off_sdec;      // byte offset of the s_dec(w) table in shared memory
     int c_prefetch;         // prefetch the completion record into L2 at decode join
+    float sync_win;         // lane clock window in mean inter-arrival times (0 = off)
     int smem_trace;
     // outputs (r = (c*Q + q)*S + s)
     int* rep_met;
@@ -539,10 +540,22 @@ __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant_
                 P.rec_comp[rb + rc.id] = t;
             }
         };
+        // lanes of a warp replay the same trace at the same QPS (mostly the same
+        // transfer-end stream): keep their simulated clocks within sync_win of
+        // each other so their stream / trace reads hit the same cache lines.  A
+        // pure scheduling choice — each lane's replay is independent, any
+        // interleaving gives identical results; the lane with the smallest clock
+        // always proceeds, so there is no deadlock.
+        const float win = P.sync_win > 0.f ? P.sync_win / (float)(P.qps[q] * (double)P.N) : 0.f;
         while (completed < R) {
             double t = tk;
 #pragma unroll
             for (int w = 0; w < kNW; w++) t = tnext[w] < t ? tnext[w] : t;
+            if (win > 0.f) {
+                const float tf = (float)t;
+                const unsigned mn = __reduce_min_sync(__activemask(), __float_as_uint(tf));
+                if (tf > __uint_as_float(mn) + win) continue;
+            }
             inst++;
             unsigned bnd = 0, touched = 0;
 #pragma unroll

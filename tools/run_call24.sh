@@ -1,0 +1,6 @@
+python -m pytest tests -m gpu -q -x 2>&1 | tail -30 > gpurun_out/gpu_tests.log
+python bench.py --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 0 > gpurun_out/bench19_cfg4.log 2>&1
+PADSIM_JOINT_WITH_A=1 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 0 > gpurun_out/bench19_cfg4_jwa.log 2>&1
+python bench.py --config cfg3 --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 0 > gpurun_out/bench19_cfg3.log 2>&1
+python tools/time_subset.py --config cfg5 --cands 64 --qps 2 --traces 1 > gpurun_out/cfg5_subset3.log 2>&1
+tail -4 gpurun_out/gpu_tests.log
