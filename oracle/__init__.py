@@ -49,7 +49,7 @@ class Model(C.Structure):
                 ("dec_per_seq", C.c_double), ("dec_per_ctx", C.c_double), ("kvb", C.c_double),
                 ("bw", C.c_double), ("ovh", C.c_double), ("max_pb", C.c_int32),
                 ("pb_tokens", C.c_int32), ("max_db", C.c_int32), ("slots", C.c_int32),
-                ("chunk", C.c_int32)]
+                ("chunk", C.c_int32), ("ctx_growth", C.c_int32)]
 
 
 class Policy(C.Structure):
@@ -166,6 +166,7 @@ def make_model(m: dict) -> Model:
     for k in ("max_pb", "pb_tokens", "max_db", "slots"):
         setattr(M, k, int(m[k]))
     M.chunk = int(m.get("chunk", 512))      # S:264 default chunk
+    M.ctx_growth = int(m.get("ctx_growth", 0))   # A40
     return M
 
 

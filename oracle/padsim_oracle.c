@@ -54,6 +54,28 @@ double or_decode_lat(const or_model* m, int32_t n, int64_t ctx, int32_t w) {
     return t / or_speedup(&m->decode, w);
 }
 
+/* A40 context-growing decode: the decode context of the step that ends at
+ * boundary s is C(s) = Σ_active (in_i + s − join_i) (prompt plus the tokens
+ * generated before the step), so within a constant-composition segment the
+ * step latency grows by d = per_ctx·n / s_dec(w) per step and boundary k of
+ * the segment is the arithmetic-series sum
+ *     t_seg + ((double)k·L1 + (double)(k(k−1)/2)·d),
+ * L1 = decode_lat(n, C(step0+1), w).  With ctx_growth = 0 the context is
+ * Σ in_i (A15) and the boundary is A14's t_seg + (double)k·L.              */
+static long seg_ctx(const or_model* m, long ctx_in, int n, int step_next, long sum_join) {
+    if (!m->ctx_growth) return ctx_in;
+    return ctx_in + (long)n * step_next - sum_join;
+}
+static double seg_growth(const or_model* m, int n, int32_t w) {
+    if (!m->ctx_growth || m->dec_per_ctx == 0.0) return 0.0;
+    return (m->dec_per_ctx * (double)n) / or_speedup(&m->decode, w);
+}
+static double seg_boundary(const or_model* m, double t_seg, double L1, double d, int k) {
+    if (!m->ctx_growth) return t_seg + (double)k * L1;
+    long tri = (long)k * (long)(k - 1) / 2;
+    return t_seg + ((double)k * L1 + (double)tri * d);
+}
+
 /* kv_transfer_latency: bulk KV pull, lands in TPOT.      */
 double or_kv_lat(const or_model* m, int32_t tokens) {
     return m->ovh + ((double)tokens * m->kvb) / m->bw;
@@ -263,8 +285,8 @@ typedef struct {
     /* prefill worker (P:281 local scheduler) */
     ring_t q; long outstanding; int busy; int* batch; int bn;
     /* decode worker (continuous batching) */
-    int* act_id; int* act_fin; int n_act; long ctx;
-    ring_t pend; int step, step0; double t_seg, L;
+    int* act_id; int* act_fin; int n_act; long ctx; long sum_join;
+    ring_t pend; int step, step0; double t_seg, L, dL;
     int in_step, at_boundary, comp_changed, dirty;
 } wk_t;
 
@@ -295,6 +317,7 @@ static int valid_model(const or_model* m) {
           m->dec_per_ctx >= 0 && m->kvb > 0 && m->bw > 0 && m->ovh > 0)) return 0;
     if (m->max_pb < 1 || m->pb_tokens < 1 || m->max_db < 1 || m->slots < 1 || m->slots > 32) return 0;
     if (m->chunk < 1) return 0;
+    if (m->ctx_growth != 0 && m->ctx_growth != 1) return 0;
     return 1;
 }
 
@@ -323,7 +346,8 @@ static int valid_model(const or_model* m) {
 typedef struct {
     ring_t q; int done_tok; long outstanding;          /* prompt FIFO, head progress */
     int* act_id; int* act_fin; int n_act; long ctx;     /* decode batch               */
-    ring_t pend; int step, step0; double t_seg, L;
+    long sum_join;                                       /* Σ join steps (A40)         */
+    ring_t pend; int step, step0; double t_seg, L, dL;
     int in_step, at_boundary, comp_changed, seg_valid;
     int c_id, c_tok;                                     /* chunk of the step in flight */
 } cw_t;
@@ -394,6 +418,7 @@ static int replay_coalesced(const or_model* m, int32_t N, const int32_t* cap, in
                         tpot[i] = (t - pe[i]) / (double)(out_tok[i] - 1);
                         completed++;
                         w->ctx -= in_tok[i];
+                        w->sum_join -= w->act_fin[k] - (out_tok[i] - 1);
                         w->act_id[k] = w->act_id[w->n_act - 1];
                         w->act_fin[k] = w->act_fin[w->n_act - 1];
                         w->n_act--;
@@ -441,6 +466,7 @@ static int replay_coalesced(const or_model* m, int32_t N, const int32_t* cap, in
                 w->act_fin[w->n_act] = w->step + (out_tok[i] - 1);
                 w->n_act++;
                 w->ctx += in_tok[i];
+                w->sum_join += w->step;
                 joined = 1;
             }
             if (w->q.len > 0) {
@@ -449,7 +475,9 @@ static int replay_coalesced(const or_model* m, int32_t N, const int32_t* cap, in
                 if (c > m->chunk) c = m->chunk;
                 if (w->done_tok == 0) ps[i] = t;
                 double lat = or_prefill_lat(m, c, 1, cap[g]);
-                if (w->n_act > 0) lat = lat + or_decode_lat(m, w->n_act, w->ctx, cap[g]);
+                if (w->n_act > 0)
+                    lat = lat + or_decode_lat(m, w->n_act,
+                                              seg_ctx(m, w->ctx, w->n_act, w->step + 1, w->sum_join), cap[g]);
                 if (heap_push(&h, t + lat, K_DSTEP, g)) goto out;
                 w->c_id = i;
                 w->c_tok = c;
@@ -459,10 +487,12 @@ static int replay_coalesced(const or_model* m, int32_t N, const int32_t* cap, in
                 if (was_idle || joined || w->comp_changed || !w->seg_valid) {
                     w->t_seg = t;
                     w->step0 = w->step;
-                    w->L = or_decode_lat(m, w->n_act, w->ctx, cap[g]);
+                    w->L = or_decode_lat(m, w->n_act, seg_ctx(m, w->ctx, w->n_act, w->step + 1, w->sum_join),
+                                         cap[g]);
+                    w->dL = seg_growth(m, w->n_act, cap[g]);
                     w->seg_valid = 1;
                 }
-                double nb = w->t_seg + (double)(w->step + 1 - w->step0) * w->L;
+                double nb = seg_boundary(m, w->t_seg, w->L, w->dL, w->step + 1 - w->step0);
                 if (heap_push(&h, nb, K_DSTEP, g)) goto out;
                 w->in_step = 1;
             }
@@ -648,7 +678,7 @@ int or_replay(const or_model* m, int32_t N, const uint8_t* role, const int32_t* 
                 w->draining = 0;
                 w->flip_sched = 0;
                 w->busy = 0; w->bn = 0; w->outstanding = 0;
-                w->n_act = 0; w->ctx = 0; w->in_step = 0; w->dirty = 0; w->step0 = w->step;
+                w->n_act = 0; w->ctx = 0; w->sum_join = 0; w->in_step = 0; w->dirty = 0; w->step0 = w->step;
                 drain_pending = 0;
                 sum->n_flips++;
                 if (lg) {
@@ -694,6 +724,7 @@ int or_replay(const or_model* m, int32_t N, const uint8_t* role, const int32_t* 
                         double tp = (t - pe[i]) / (double)(out_tok[i] - 1);
                         COMPLETE(i, t, tp);
                         w->ctx -= in_tok[i];
+                        w->sum_join -= w->act_fin[k] - (out_tok[i] - 1);
                         w->act_id[k] = w->act_id[w->n_act - 1];
                         w->act_fin[k] = w->act_fin[w->n_act - 1];
                         w->n_act--;
@@ -874,6 +905,7 @@ int or_replay(const or_model* m, int32_t N, const uint8_t* role, const int32_t* 
                 w->act_fin[w->n_act] = w->step + (out_tok[i] - 1);
                 w->n_act++;
                 w->ctx += in_tok[i];
+                w->sum_join += w->step;
                 joined = 1;
             }
             if (w->n_act > 0) {
@@ -881,11 +913,13 @@ int or_replay(const or_model* m, int32_t N, const uint8_t* role, const int32_t* 
                     /* new constant-composition segment, reads the effective cap */
                     w->t_seg = t;
                     w->step0 = w->step;
-                    w->L = or_decode_lat(m, w->n_act, w->ctx, w->eff);
+                    w->L = or_decode_lat(m, w->n_act, seg_ctx(m, w->ctx, w->n_act, w->step + 1, w->sum_join),
+                                         w->eff);
+                    w->dL = seg_growth(m, w->n_act, w->eff);
                     w->dirty = 0;
                 }
-                /* A14: step k of a segment ends at t_seg + (double)k * L */
-                double nb = w->t_seg + (double)(w->step + 1 - w->step0) * w->L;
+                /* A14: step k of a segment ends at t_seg + (double)k * L (A40 with growth) */
+                double nb = seg_boundary(m, w->t_seg, w->L, w->dL, w->step + 1 - w->step0);
                 if (heap_push(&h, nb, K_DSTEP, g)) goto out;
                 w->in_step = 1;
             }

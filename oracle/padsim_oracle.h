@@ -43,6 +43,7 @@ typedef struct {
     int32_t max_db;       /* max decode batch                                */
     int32_t slots;        /* KV transfer request buffer (32)          */
     int32_t chunk;        /* coalesced mode: prefill chunk tokens (512) */
+    int32_t ctx_growth;   /* 1: decode context counts generated tokens (A40)  */
 } or_model;
 
 typedef struct {
