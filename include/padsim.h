@@ -97,6 +97,10 @@ typedef struct {
     int32_t max_decode_batch;          /* [1, 256]  (64)                  */
     int32_t transfer_slots;            /* [1, 32]   (32)                  */
     int32_t prefill_chunk_tokens;      /* >= 1, coalesced mode only (512) */
+    int32_t decode_ctx_growth;         /* 0/1. 1: the decode context of a step counts the
+                                          tokens generated so far, C = Σ (in_i + s − join_i)
+                                          (A40); boundaries of a segment are then the
+                                          arithmetic-series sums t0 + (k·L1 + k(k−1)/2·d) */
 } padsim_model;
 
 /* Algorithm 1 constants for one candidate.  kind: 0 static,

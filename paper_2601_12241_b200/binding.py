@@ -48,7 +48,7 @@ class Model(C.Structure):
                 ("fabric_bw_Bps", C.c_double), ("transfer_overhead_s", C.c_double),
                 ("max_prefill_batch", C.c_int32), ("prefill_token_budget", C.c_int32),
                 ("max_decode_batch", C.c_int32), ("transfer_slots", C.c_int32),
-                ("prefill_chunk_tokens", C.c_int32)]
+                ("prefill_chunk_tokens", C.c_int32), ("decode_ctx_growth", C.c_int32)]
 
 
 class Policy(C.Structure):
@@ -177,6 +177,7 @@ def make_model(m: dict) -> Model:
     M.max_prefill_batch, M.prefill_token_budget = int(m["max_pb"]), int(m["pb_tokens"])
     M.max_decode_batch, M.transfer_slots = int(m["max_db"]), int(m["slots"])
     M.prefill_chunk_tokens = int(m.get("chunk", 512))     # coalesced mode
+    M.decode_ctx_growth = int(m.get("ctx_growth", 0))     # A40
     return M
 
 

@@ -29,8 +29,8 @@ struct CoalReplay {
     int N, R, max_db;
     double inv_lam;
     // per-GPU SoA, element g at [g * 32]
-    double *tn, *tseg, *L, *hps;
-    long long *outst, *ctx;
+    double *tn, *tseg, *L, *hps, *dL;
+    long long *outst, *ctx, *sj;     // sj: Σ join steps of the decode members (A40)
     int *qh, *qt, *ql, *ph, *pt, *pl, *done, *nact, *step, *st0, *ts, *mfin, *cid, *ctok, *fl;
     int* act_id;    // [(g * max_db + k) * 32]
     int* act_fin;
@@ -41,6 +41,7 @@ struct CoalReplay {
     long long rec_base;
     int completed, met, near;
     double maxcomp, sq, se;
+    bool gr;                         // A40 context growth
 
     __device__ CoalReplay(const Plan& p) : P(p) {}
 
@@ -77,21 +78,19 @@ struct CoalReplay {
         }
     }
 
-    // boundary k of the current decode-only segment
+    // boundary k of the current decode-only segment (A37; A40 with growth)
     __device__ __forceinline__ double bnd(int o, int k) const {
-        return tseg[o] + (double)(k - st0[o]) * L[o];
+        return seg_bnd(tseg[o], L[o], dL[o], k - st0[o], gr);
     }
 
     // first boundary index > step whose time is ≥ tau (boundaries are monotone in k)
     __device__ int first_bnd_ge(int o, double tau) const {
-        const double t0 = tseg[o], Lg = L[o];
-        const int s0 = st0[o], sm = step[o];
-        const float xf = __fdividef((float)(tau - t0), (float)Lg);
-        int s = s0 + (int)ceilf(xf);
-        if (s <= sm) s = sm + 1;
-        while (t0 + (double)(s - s0) * Lg < tau) s++;
-        while (s - 1 > sm && t0 + (double)(s - 1 - s0) * Lg >= tau) s--;
-        return s;
+        return seg_first_ge(tseg[o], L[o], dL[o], st0[o], step[o], tau, gr);
+    }
+
+    // decode context of the step after boundary `sn` (A15; A40 with growth)
+    __device__ __forceinline__ long long step_ctx(int o, int n, int sn) const {
+        return gr ? ctx[o] + (long long)n * (sn + 1) - sj[o] : ctx[o];
     }
 
     __device__ void step_end(int g, double t) {
@@ -111,6 +110,7 @@ struct CoalReplay {
                     const int i = act_id[ak];
                     complete(i, t, (t - PE(i)) / (double)(T.out_tok[i] - 1));
                     cx -= T.in_tok[i];
+                    sj[o] -= sn - (T.out_tok[i] - 1);   // its join step
                     const size_t al = ((size_t)o * max_db) + (size_t)(n - 1) * 32;
                     act_id[ak] = act_id[al];
                     act_fin[ak] = act_fin[al];
@@ -199,6 +199,7 @@ struct CoalReplay {
             act_fin[ak] = fin;
             n++;
             ctx[o] += T.in_tok[i];
+            sj[o] += sn;
             mf = fin < mf ? fin : mf;
             joined = true;
         }
@@ -215,7 +216,7 @@ struct CoalReplay {
                 sq = sq + (t - arr(i));
             }
             double lat = ((double)c / P.m.den[1]) / P.m.spre[cap - P.m.min_w];
-            if (n > 0) lat = lat + dec_lat(n, ctx[o], cap);
+            if (n > 0) lat = lat + dec_lat(n, step_ctx(o, n, sn), cap);
             tn[o] = t + lat;
             ts[o] = sn + 1;
             cid[o] = i;
@@ -225,7 +226,8 @@ struct CoalReplay {
             if (was_idle || joined || (f & CF_COMPCHG) || !(f & CF_SEGOK)) {
                 tseg[o] = t;
                 st0[o] = sn;
-                L[o] = dec_lat(n, ctx[o], cap);
+                L[o] = dec_lat(n, step_ctx(o, n, sn), cap);
+                dL[o] = gr ? (P.m.dec_per_ctx * (double)n) / P.m.sdec[cap - P.m.min_w] : 0.0;
                 f |= CF_SEGOK;
             }
             ts[o] = mf;                     // next leave; nothing changes before it
@@ -243,13 +245,14 @@ struct CoalReplay {
         inv_lam = 1.0 / (P.qps[q] * (double)N);
         for (int g = 0; g < N; g++) {
             const int o = g * 32;
-            tn[o] = PAD_INF; tseg[o] = 0.0; L[o] = 1.0; hps[o] = 0.0;
-            outst[o] = 0; ctx[o] = 0;
+            tn[o] = PAD_INF; tseg[o] = 0.0; L[o] = 1.0; hps[o] = 0.0; dL[o] = 0.0;
+            outst[o] = 0; ctx[o] = 0; sj[o] = 0;
             qh[o] = kNoIdx; qt[o] = kNoIdx; ql[o] = 0; ph[o] = kNoIdx; pt[o] = kNoIdx; pl[o] = 0;
             done[o] = 0; nact[o] = 0; step[o] = 0; st0[o] = 0; ts[o] = 0; mfin[o] = kIntMaxC;
             cid[o] = kNoIdx; ctok[o] = 0; fl[o] = 0;
         }
         for (int z = 0; z < nk; z++) metk[z] = 0;
+        gr = CTX && P.m.ctx_growth != 0;
         completed = 0; met = 0; near = 0;
         maxcomp = -PAD_INF;
         sq = 0.0; se = 0.0;
@@ -318,8 +321,10 @@ __global__ void __launch_bounds__(32) coalesced_kernel(const __grid_constant__ P
         rp.tseg = (double*)p + lane; p += n * sizeof(double);
         rp.L = (double*)p + lane; p += n * sizeof(double);
         rp.hps = (double*)p + lane; p += n * sizeof(double);
+        rp.dL = (double*)p + lane; p += n * sizeof(double);
         rp.outst = (long long*)p + lane; p += n * sizeof(long long);
         rp.ctx = (long long*)p + lane; p += n * sizeof(long long);
+        rp.sj = (long long*)p + lane; p += n * sizeof(long long);
         int* ib = (int*)p;
         int** fields[] = {&rp.qh, &rp.qt, &rp.ql, &rp.ph, &rp.pt, &rp.pl, &rp.done, &rp.nact,
                           &rp.step, &rp.st0, &rp.ts, &rp.mfin, &rp.cid, &rp.ctok, &rp.fl};
@@ -345,7 +350,7 @@ __global__ void __launch_bounds__(32) coalesced_kernel(const __grid_constant__ P
 }
 
 __host__ __device__ constexpr size_t coal_worker_bytes(int N) {
-    return (size_t)N * 32 * (4 * sizeof(double) + 2 * sizeof(long long) + 15 * sizeof(int));
+    return (size_t)N * 32 * (5 * sizeof(double) + 3 * sizeof(long long) + 15 * sizeof(int));
 }
 
 }  // namespace padsim

@@ -36,11 +36,41 @@ struct DevModel {
     double rate, eff, dec_fixed, dec_per_seq, dec_per_ctx, kvb, bw, ovh;
     int max_pb, pb_tokens, max_db, slots;
     int chunk;                         // coalesced mode: prefill chunk tokens
+    int ctx_growth;                    // A40: decode context counts generated tokens
     const double* spre;                // [ncap]  s_pre(w)
     const double* sdec;                // [ncap]  s_dec(w)
     const double* den;                 // [max_pb+1] rate*(1+eff*(b-1))
     const double* ltab;                // [ncap][max_db] decode step latency, n = 1..max_db
 };
+
+// Decode segment boundaries (A14; A40 with context growth): boundary k of a
+// segment that started at ts0 with first-step latency L and per-step growth dL.
+__device__ __forceinline__ double seg_bnd(double ts0, double L, double dL, int k, bool growth) {
+    if (!growth) return ts0 + (double)k * L;
+    const long long tri = (long long)k * (long long)(k - 1) / 2;
+    return ts0 + ((double)k * L + (double)tri * dL);
+}
+
+// Smallest boundary index s > stm of the segment (started at step s0) whose time
+// is ≥ tau: a float estimate (linear, or the quadratic root with growth) fixed up
+// with the exact FP64 boundary expression (boundaries are increasing in k).
+__device__ __forceinline__ int seg_first_ge(double ts0, double L, double dL, int s0, int stm, double tau,
+                                            bool growth) {
+    const float D = (float)(tau - ts0);
+    float kf;
+    if (!growth) {
+        kf = __fdividef(D, (float)L);
+    } else {
+        const float B = (float)L - 0.5f * (float)dL;
+        kf = 2.f * D / (B + sqrtf(B * B + 2.f * (float)dL * D));
+    }
+    kf = fminf(fmaxf(kf, 0.f), 1.0e9f);
+    int s = s0 + (int)ceilf(kf);
+    if (s <= stm) s = stm + 1;
+    while (seg_bnd(ts0, L, dL, s - s0, growth) < tau) s++;
+    while (s - 1 > stm && seg_bnd(ts0, L, dL, s - 1 - s0, growth) >= tau) s--;
+    return s;
+}
 
 // Everything a replay kernel launch needs (passed by value as a kernel param).
 struct Plan {

@@ -171,6 +171,8 @@ template <> struct WTab<64> {               // memory arrays + lazily refreshed 
 // global scratch with stride 32 (NG = 64); field[g * ws]
 struct JWork {
     double* tseg; double* L;
+    long long* sj;   // D: Σ join steps of the active members (A40)
+    double* dL;      // D: per-step latency growth of the segment (A40)
     int* a0;    // P: outstanding tokens | D: active count
     int* qh; int* qt; int* ql;        // P: prompt FIFO | D: pending joins
     int* b0;    // P: batch head | D: last materialised step
@@ -179,7 +181,7 @@ struct JWork {
     unsigned char* fl;
 };
 template <int TB>
-__host__ __device__ constexpr size_t j_work_bytes() { return (size_t)kJG * TB * (2 * sizeof(double) + 13 * sizeof(int) + 1); }
+__host__ __device__ constexpr size_t j_work_bytes() { return (size_t)kJG * TB * (4 * sizeof(double) + 13 * sizeof(int) + 1); }
 
 enum : unsigned char { JF_DRAIN = 1, JF_DIRTY = 2 };
 
@@ -251,6 +253,7 @@ struct JReplay {
     int nk;
     long long w_sum;
     double w_acc, w_prev, a0t;
+    bool gr;             // A40 context growth (ctx_growth with a context cost)
 
     __device__ JReplay(const Plan& p, const TraceView& t, const Scratch& x, const JWork& w)
         : P(p), T(t), X(x), W(w) {}
@@ -263,17 +266,10 @@ struct JReplay {
     __device__ __forceinline__ void add_kp(int g, int d) { tab.add_p(g, d); }
     __device__ __forceinline__ void add_kd(int g, int d) { tab.add_d(g, d); }
     __device__ __forceinline__ double bnd(int o, int s) const {
-        return W.tseg[o] + (double)(s - W.st0[o]) * W.L[o];
+        return seg_bnd(W.tseg[o], W.L[o], gr ? W.dL[o] : 0.0, s - W.st0[o], gr);
     }
     __device__ int first_bnd_ge(int o, double tau) const {
-        const double ts = W.tseg[o], L = W.L[o];
-        const int s0 = W.st0[o], stm = W.b0[o];
-        const float xf = __fdividef((float)(tau - ts), (float)L);
-        int s = s0 + (int)ceilf(xf);
-        if (s <= stm) s = stm + 1;
-        while (ts + (double)(s - s0) * L < tau) s++;
-        while (s - 1 > stm && ts + (double)(s - 1 - s0) * L >= tau) s--;
-        return s;
+        return seg_first_ge(W.tseg[o], W.L[o], gr ? W.dL[o] : 0.0, W.st0[o], W.b0[o], tau, gr);
     }
 
     __device__ void complete(int i, double t, double tpot) {
@@ -402,6 +398,7 @@ struct JReplay {
             const int nx = LNK(id);
             complete(id, t, (t - PE(id)) / (double)(T.out_tok[id] - 1));
             W.ctx[o] -= T.in_tok[id];
+            if (gr) W.sj[o] -= s - (T.out_tok[id] - 1);      // its join step (A40)
             left++;
             id = nx;
         }
@@ -502,6 +499,7 @@ struct JReplay {
             *wp = old | bit;
             n++;
             W.ctx[o] += T.in_tok[i];
+            if (gr) W.sj[o] += step;
             mf = fin < mf ? fin : mf;
             joined = true;
         }
@@ -516,10 +514,13 @@ struct JReplay {
                 const int ci = W.eff[o] - P.m.min_w;
                 if (P.m.dec_per_ctx == 0.0) {
                     W.L[o] = P.m.ltab[(size_t)ci * max_db + (n - 1)];
-                } else {
+                } else {            // A15 / A40 context of the segment's first step
                     double xv = P.m.dec_fixed + P.m.dec_per_seq * (double)n;
-                    xv = xv + P.m.dec_per_ctx * (double)W.ctx[o];
+                    long long cc = W.ctx[o];
+                    if (gr) cc += (long long)n * (step + 1) - W.sj[o];
+                    xv = xv + P.m.dec_per_ctx * (double)cc;
                     W.L[o] = xv / P.m.sdec[ci];
+                    if (gr) W.dL[o] = (P.m.dec_per_ctx * (double)n) / P.m.sdec[ci];
                 }
                 W.fl[o] = f & (unsigned char)~JF_DIRTY;
             }
@@ -568,7 +569,7 @@ struct JReplay {
         dmask ^= ((Mask)1) << g;
         W.fl[o] = 0;
         W.a0[o] = 0; W.ql[o] = 0; W.b0[o] = 0; W.b1[o] = 0; W.st0[o] = 0;
-        W.mfin[o] = kIntMax; W.ctx[o] = 0;
+        W.mfin[o] = kIntMax; W.ctx[o] = 0; W.sj[o] = 0;
         set_tnext(g, PAD_INF);
         tab.set_p(g, to_p ? 0 : kIntMax);
         tab.set_d(g, to_p ? kIntMax : 0);
@@ -715,7 +716,7 @@ struct JReplay {
             if (r == 0) pmask |= ((Mask)1) << g;
             if (r == 1) dmask |= ((Mask)1) << g;
             tab.init(g, r);
-            W.tseg[o] = 0.0; W.L[o] = 1.0;
+            W.tseg[o] = 0.0; W.L[o] = 1.0; W.sj[o] = 0; W.dL[o] = 0.0;
             W.a0[o] = 0; W.qh[o] = kNoIdx; W.qt[o] = kNoIdx; W.ql[o] = 0;
             W.b0[o] = 0; W.b1[o] = 0; W.st0[o] = 0; W.mfin[o] = kIntMax;
             W.eff[o] = W.cmd[o] = on ? ccap[g] : P.m.min_w;
@@ -741,6 +742,7 @@ struct JReplay {
         }
         nk = P.sw.n;
         for (int z = 0; z < nk; z++) metk[z] = 0;
+        gr = P.m.ctx_growth != 0 && P.m.dec_per_ctx != 0.0;
         w_sum = P.sw.capsum[c];
         a0t = R > 0 ? arr(0) : 0.0;
         w_acc = 0.0;
@@ -825,8 +827,10 @@ struct JReplay {
 };
 
 // CTAs bound to one trace (s = blockIdx.x mod S); warps pull 32-replay items.
-template <bool DYN, int TB, int NG>
-__global__ void __launch_bounds__(TB) __maxnreg__(TB == 32 ? 232 : 168) joint_kernel(const __grid_constant__ Plan P) {
+// MR: register cap — 232 for one-warp CTAs (no spills; measured on cfg 3/4: a
+// 168-register variant that fits more warps next to stage C was not faster).
+template <bool DYN, int TB, int NG, int MR = (TB == 32 ? 232 : 168)>
+__global__ void __launch_bounds__(TB) __maxnreg__(MR) joint_kernel(const __grid_constant__ Plan P) {
     extern __shared__ __align__(128) unsigned char smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     char* wbase = P.scratch + ((size_t)blockIdx.x * (TB / 32) + warp) * P.warp_bytes;
@@ -837,6 +841,8 @@ __global__ void __launch_bounds__(TB) __maxnreg__(TB == 32 ? 232 : 168) joint_ke
         unsigned char* p = smem;
         W.tseg = (double*)p + tid; p += n * sizeof(double);
         W.L = (double*)p + tid; p += n * sizeof(double);
+        W.sj = (long long*)p + tid; p += n * sizeof(long long);
+        W.dL = (double*)p + tid; p += n * sizeof(double);
         int* ib = (int*)p;
         W.a0 = ib + 0 * n + tid; W.qh = ib + 1 * n + tid; W.qt = ib + 2 * n + tid;
         W.ql = ib + 3 * n + tid; W.b0 = ib + 4 * n + tid; W.b1 = ib + 5 * n + tid;
@@ -850,6 +856,8 @@ __global__ void __launch_bounds__(TB) __maxnreg__(TB == 32 ? 232 : 168) joint_ke
         char* p = wbase + P.off_jw;
         W.tseg = (double*)p + lane; p += n * sizeof(double);
         W.L = (double*)p + lane; p += n * sizeof(double);
+        W.sj = (long long*)p + lane; p += n * sizeof(long long);
+        W.dL = (double*)p + lane; p += n * sizeof(double);
         int* ib = (int*)p;
         W.a0 = ib + 0 * n + lane; W.qh = ib + 1 * n + lane; W.qt = ib + 2 * n + lane;
         W.ql = ib + 3 * n + lane; W.b0 = ib + 4 * n + lane; W.b1 = ib + 5 * n + lane;
@@ -918,7 +926,7 @@ __global__ void __launch_bounds__(TB) __maxnreg__(TB == 32 ? 232 : 168) joint_ke
 }
 
 constexpr size_t joint_global_bytes_per_warp(int NG) {   // per-GPU SoA for NG = 64
-    return NG == 8 ? 0 : (size_t)NG * 32 * (2 * sizeof(double) + 13 * sizeof(int) + 1);
+    return NG == 8 ? 0 : (size_t)NG * 32 * (4 * sizeof(double) + 13 * sizeof(int) + 1);
 }
 
 }  // namespace padsim

@@ -424,6 +424,8 @@ static int validate_model(padsim_ctx* ctx, const padsim_model* m) {
         m->max_decode_batch > PADSIM_MAX_DECODE_BATCH || m->transfer_slots < 1 ||
         m->transfer_slots > PADSIM_MAX_SLOTS || m->prefill_chunk_tokens < 1)
         return fail(ctx, PADSIM_EMODEL, "batch / slot / chunk limits");
+    if (m->decode_ctx_growth != 0 && m->decode_ctx_growth != 1)
+        return fail(ctx, PADSIM_EMODEL, "decode_ctx_growth must be 0/1");
     return PADSIM_OK;
 }
 
@@ -487,6 +489,7 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
     F.m.bw = model->fabric_bw_Bps; F.m.ovh = model->transfer_overhead_s;
     F.m.max_pb = model->max_prefill_batch; F.m.pb_tokens = model->prefill_token_budget;
     F.m.max_db = model->max_decode_batch; F.m.slots = model->transfer_slots;
+    F.m.ctx_growth = model->decode_ctx_growth;
     F.m.spre = ctx->d_spre; F.m.sdec = ctx->d_sdec; F.m.den = ctx->d_den; F.m.ltab = ctx->d_ltab;
     F.N = N; F.Q = Q; F.S = S; F.Rmax = std::max(Rmax, 1);
     F.toff = ctx->d_toff; F.nreq = ctx->d_nreq; F.s_unit = ctx->d_s_unit; F.kv = ctx->d_kv;
@@ -577,8 +580,11 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
         F.bits_in_smem = wheel <= 256 ? 1 : 0;
         if (getenv("PADSIM_BITS_GLOBAL")) F.bits_in_smem = 0;          // experiment knob
         F.c_prefetch = getenv("PADSIM_NO_PREFETCH") ? 0 : 1;            // experiment knob
-        F.sync_win = 16.f;
-        if (const char* e = getenv("PADSIM_SYNC_WIN")) F.sync_win = (float)atof(e);   // experiment knob
+        // measured (cfg 4): the lane clock window slows stage C (683 -> 721 ms at
+        // 16-64 inter-arrivals, 780 at 4) — its stream reads already coalesce
+        // well enough — so it is off here; the joint kernel gains from it
+        F.sync_win = 0.f;
+        if (const char* e = getenv("PADSIM_SYNC_WIN_C")) F.sync_win = (float)atof(e);   // experiment knob
         F.smem_trace = 0;
         F.c_off_sdec = wbytes + (F.bits_in_smem ? bbytes : 0);
         ctx->fC_smem = F.c_off_sdec + (size_t)F.m.ncap * sizeof(double);
@@ -885,7 +891,7 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
     CK(cudaGetLastError());
 
     // factorized static path (stage A prefill groups -> stage C decode) for N <= 8
-    ctx->fact = N <= 8 && !ctx->static_list.empty() && !(flags & PADSIM_JOINT);
+    ctx->fact = N <= 8 && !ctx->static_list.empty() && !(flags & PADSIM_JOINT) && Rmax < kRecMaxReq;
     if (ctx->fact) {
         int r_ = plan_factorized(ctx, model, slo, n_qps, n_traces, Rmax, tot, cands);
         if (r_) return r_;
@@ -903,7 +909,7 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
         P.m.dec_per_ctx = model->decode_per_ctx_tok_s; P.m.kvb = model->kv_bytes_per_token;
         P.m.bw = model->fabric_bw_Bps; P.m.ovh = model->transfer_overhead_s;
         P.m.max_pb = model->max_prefill_batch; P.m.pb_tokens = model->prefill_token_budget;
-        P.m.max_db = model->max_decode_batch; P.m.slots = model->transfer_slots;
+        P.m.max_db = model->max_decode_batch; P.m.ctx_growth = model->decode_ctx_growth; P.m.slots = model->transfer_slots;
         P.m.spre = ctx->d_spre; P.m.sdec = ctx->d_sdec; P.m.den = ctx->d_den; P.m.ltab = ctx->d_ltab;
         P.N = N; P.C = C; P.Q = n_qps; P.S = n_traces; P.Rmax = Rmax; P.B = B;
         P.toff = ctx->d_toff; P.nreq = ctx->d_nreq; P.s_unit = ctx->d_s_unit; P.kv = ctx->d_kv;
@@ -952,6 +958,8 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
         ctx->d_workJ[dyn] = d_wj;
         P.work = d_wj;
         P.smem_trace = 0;
+        // measured (cfg 3): a 16-inter-arrival lane clock window speeds the joint
+        // replays up 15 % (622 -> 529 ms/step): lanes read the same trace lines
         P.sync_win = 16.f;
         if (const char* e = getenv("PADSIM_SYNC_WIN")) P.sync_win = (float)atof(e);   // experiment knob
         const long long UJ = (long long)n_traces * n_qps * P.n_clist;
@@ -998,7 +1006,7 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
         P.m.rate = model->prefill_base_rate; P.m.eff = model->prefill_batch_eff;
         P.m.dec_fixed = model->decode_fixed_s; P.m.dec_per_seq = model->decode_per_seq_s;
         P.m.dec_per_ctx = model->decode_per_ctx_tok_s;
-        P.m.max_db = model->max_decode_batch; P.m.chunk = model->prefill_chunk_tokens;
+        P.m.max_db = model->max_decode_batch; P.m.ctx_growth = model->decode_ctx_growth; P.m.chunk = model->prefill_chunk_tokens;
         P.m.spre = ctx->d_spre; P.m.sdec = ctx->d_sdec; P.m.den = ctx->d_den; P.m.ltab = ctx->d_ltab;
         P.N = N; P.C = C; P.Q = n_qps; P.S = n_traces; P.Rmax = Rmax; P.B = B;
         P.toff = ctx->d_toff; P.nreq = ctx->d_nreq; P.s_unit = ctx->d_s_unit; P.kv = ctx->d_kv;

@@ -60,15 +60,18 @@ struct __align__(16) SHot {
     int id;         // request id
 };
 
-// One transfer-end record of the stage A → stage C stream (32 B), read when the
-// request completes.
+// Completion part of a transfer-end record (16 B), read when the request
+// completes.  The TTFT tests do not depend on the decode side, so stage A
+// evaluates them once per record: bit 0 ttft ≤ TTFT_SLO, bit 1 ttft within
+// 1e-9 relative of it (near-boundary), bits 2..9 ttft ≤ sweep SLO z, bits
+// 10..31 request id (n_req < 2^22 on the factorized path).
 struct __align__(16) SRec {
-    double te;      // transfer end (event time in stage C)
     double pe;      // prefill end (first token)
-    double ttft;    // pe − a_i, computed once in stage A
-    int id;         // request id
     int meta;       // out_tok | phase << 31
+    unsigned fl;    // TTFT flags | id << 10
 };
+constexpr int kRecIdShift = 10;
+constexpr int kRecMaxReq = 1 << 22;
 
 struct FPlan {
     DevModel m;
@@ -293,10 +296,12 @@ __global__ void __launch_bounds__(TB) stageA_kernel(const __grid_constant__ FPla
         while (tbusy > 0 && mte == t) {
             {
                 SRec rc;
-                rc.te = t;
                 rc.pe = tpe[mk * ss];
-                rc.ttft = rc.pe - su[mid] * inv_lam;
-                rc.id = mid;
+                const double ttft = rc.pe - su[mid] * inv_lam;
+                unsigned fl = (ttft <= P.ttft_slo ? 1u : 0u) |
+                              (fabs(ttft - P.ttft_slo) <= 1e-9 * P.ttft_slo ? 2u : 0u);
+                for (int z = 0; z < P.sw.n; z++) fl |= (ttft <= P.sw.ttft[z] ? 4u : 0u) << z;
+                rc.fl = fl | ((unsigned)mid << kRecIdShift);
                 rc.meta = ot[mid] | ((int)ph[mid] << 31);
                 orec[k] = rc;
                 SHot hc;
@@ -395,14 +400,6 @@ __global__ void __launch_bounds__(TB) stageA_kernel(const __grid_constant__ FPla
     P.a_se[ga] = se;
 }
 
-__device__ __forceinline__ int first_boundary_ge(double tseg, double L, int st0, int stm, double tau) {
-    const float xf = __fdividef((float)(tau - tseg), (float)L);
-    int s = st0 + (int)ceilf(xf);
-    if (s <= stm) s = stm + 1;
-    while (tseg + (double)(s - st0) * L < tau) s++;
-    while (s - 1 > stm && tseg + (double)(s - 1 - st0) * L >= tau) s--;
-    return s;
-}
 
 // ---------------------------------------------------------------------------
 // stage C: decode workers consume the transfer-end stream (A13, A14)
@@ -422,11 +419,13 @@ struct CWork {            // per-thread shared-memory SoA views (stride kThreads
     double* tseg;
     double* Ls;
     int* nact; int* qh; int* qt; int* ql; int* stm; int* nxs; int* st0; int* mfin;
-    long long* ctx;
+    long long* ctx;          // CTX: Σ prompt tokens of the active members (A15)
+    long long* sj;           // CTX: Σ join steps of the active members (A40)
+    double* dL;              // CTX: per-step latency growth of the segment (A40)
 };
 
 constexpr size_t kCWorkBytes = (size_t)kNW * kThreads * (2 * sizeof(double) + 8 * sizeof(int));
-constexpr size_t kCWorkCtxBytes = (size_t)kNW * kThreads * sizeof(long long);
+constexpr size_t kCWorkCtxBytes = (size_t)kNW * kThreads * (2 * sizeof(long long) + sizeof(double));
 // IDX: stream-index type of link[] and the wheel heads — uint16_t when
 // n_req ≤ 32767 (halves the scratch footprint and its DRAM/L2 traffic),
 // else uint32_t; the top bit flags "more members chained through link[]".
@@ -454,7 +453,9 @@ __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant_
         W.st0 = ib + 6 * n + tid; W.mfin = ib + 7 * n + tid;
         p += 8 * n * sizeof(int);
         W.ctx = CTX ? (long long*)p + tid : nullptr;
-        if (CTX) p += n * sizeof(long long);
+        W.sj = CTX ? (long long*)p + n + tid : nullptr;
+        W.dL = CTX ? (double*)p + 2 * n + tid : nullptr;
+        if (CTX) p += 3 * n * sizeof(long long);
         if (P.bits_in_smem) {
             bits = (unsigned*)p + tid;
             bstride = kThreads;
@@ -491,6 +492,8 @@ __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant_
         const SRec* recs = P.st_rec + sb;
         const SHot* hots = P.st_hot + sb;
         const long long rb = P.rec_ttft ? r * P.Rmax : -1;
+        const double inv_lam = 1.0 / (P.qps[q] * (double)P.N);
+        const bool gr = CTX && P.m.ctx_growth;      // A40 context growth
         // decode cap indices of this candidate, 9 bits per worker (ncap ≤ 512)
         unsigned long long dcx = 0ull;
 #pragma unroll
@@ -506,7 +509,7 @@ __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant_
             W.tseg[o] = 0.0; W.Ls[o] = 1.0;
             W.nact[o] = 0; W.qh[o] = kNoIdx; W.qt[o] = kNoIdx; W.ql[o] = 0;
             W.stm[o] = 0; W.nxs[o] = 0; W.st0[o] = 0; W.mfin[o] = 0x7fffffff;
-            if (CTX) W.ctx[o] = 0;
+            if (CTX) { W.ctx[o] = 0; W.sj[o] = 0; W.dL[o] = 0.0; }
         }
         for (int z = 0; z < y * nwords; z++) bits[(size_t)z * bstride] = 0u;
         int completed = 0, met = 0, near = 0, k = 0;
@@ -520,24 +523,30 @@ __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant_
 #pragma unroll
         for (int z = 0; z < kMaxSloSweep; z++) metk[z] = 0;
         const int nk = P.sw.n;
+        int ck0 = -1, cm0 = 0, ck1 = -1, cm1 = 0;   // last two routed (stream index, meta)
+        SRec drc;                          // deferred completion (non-CTX)
+        double dt = 0.0;
+        bool dpend = false;
+        // scoring of one completion (`completed` is counted where the member
+        // leaves: scoring may be deferred past the end of the event loop)
         auto complete = [&](const SRec& rc, double t, double tpot) {
-            completed++;
             const double ts = (rc.meta < 0) ? P.tpot_slo1 : P.tpot_slo0;
-            met += (rc.ttft <= P.ttft_slo && tpot <= ts) ? 1 : 0;
+            met += ((rc.fl & 1u) && tpot <= ts) ? 1 : 0;
 #pragma unroll
             for (int z = 0; z < kMaxSloSweep; z++) {
                 if (z < nk) {
                     const double tz = (rc.meta < 0) ? P.sw.tpot1[z] : P.sw.tpot0[z];
-                    metk[z] += (rc.ttft <= P.sw.ttft[z] && tpot <= tz) ? 1 : 0;
+                    metk[z] += (((rc.fl >> (2 + z)) & 1u) && tpot <= tz) ? 1 : 0;
                 }
             }
-            near += (fabs(rc.ttft - P.ttft_slo) <= 1e-9 * P.ttft_slo || fabs(tpot - ts) <= 1e-9 * ts) ? 1 : 0;
+            near += ((rc.fl & 2u) || fabs(tpot - ts) <= 1e-9 * ts) ? 1 : 0;
             maxcomp = fmax(maxcomp, t);
             if (rb >= 0) {
-                P.rec_ttft[rb + rc.id] = rc.ttft;
-                P.rec_tpot[rb + rc.id] = tpot;
-                P.rec_pe[rb + rc.id] = rc.pe;
-                P.rec_comp[rb + rc.id] = t;
+                const int id = (int)(rc.fl >> kRecIdShift);
+                P.rec_ttft[rb + id] = rc.pe - P.s_unit[off + id] * inv_lam;   // as stage A
+                P.rec_tpot[rb + id] = tpot;
+                P.rec_pe[rb + id] = rc.pe;
+                P.rec_comp[rb + id] = t;
             }
         };
         // lanes of a warp replay the same trace at the same QPS (mostly the same
@@ -572,10 +581,24 @@ __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant_
                     int left = 0;
                     for (;;) {
                         const int kk = (int)(cur & ~kMulti);
-                        const SRec rc = recs[kk];
-                        const int o1 = (rc.meta & 0x7fffffff) - 1;
-                        complete(rc, t, (t - rc.pe) / (double)o1);
-                        if (CTX) W.ctx[o] -= itk[rc.id];
+                        if (CTX) {                          // the leave needs the record now
+                            const SRec rc = recs[kk];
+                            const int o1 = (rc.meta & 0x7fffffff) - 1;
+                            complete(rc, t, (t - rc.pe) / (double)o1);
+                            completed++;
+                            W.ctx[o] -= itk[rc.fl >> kRecIdShift];
+                            W.sj[o] -= sN - o1;             // its join step (A40)
+                        } else {
+                            // deferred scoring: score the previous completion, then
+                            // issue this one's record load and use it at the next
+                            // completion (or the end of the replay), so the load
+                            // latency overlaps the rest of the event processing
+                            if (dpend) complete(drc, dt, (dt - drc.pe) / (double)((drc.meta & 0x7fffffff) - 1));
+                            drc = recs[kk];
+                            dt = t;
+                            dpend = true;
+                            completed++;
+                        }
                         left++;
                         if (!(cur & kMulti)) break;
                         cur = (unsigned)link[(size_t)kk * 32];   // IDX → unsigned keeps the flag bit
@@ -608,11 +631,16 @@ __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant_
                 if (k < R) nxt = hots[k]; else nxt.te = PAD_INF;
                 tk = nxt.te;
                 if (rb >= 0) P.rec_te[rb + hc.id] = t;
-                if ((hc.meta & 0x7fffffff) == 1) { complete(recs[kk], t, 0.0); continue; }   // S:280 D4
+                if ((hc.meta & 0x7fffffff) == 1) {                   // S:280 D4
+                    complete(recs[kk], t, 0.0);
+                    completed++;
+                    continue;
+                }
                 int best = 0, bl = ld[0];
 #pragma unroll
                 for (int w = 1; w < kNW; w++) if (ld[w] < bl) { bl = ld[w]; best = w; }
                 radd<kNW, int>(ld, best, 1);
+                ck1 = ck0; cm1 = cm0; ck0 = kk; cm0 = hc.meta;
                 const int o = best * kThreads;
                 const int qn = W.ql[o];
                 if (qn == 0) W.qh[o] = kk; else link[(size_t)W.qt[o] * 32] = (IDX)kk;
@@ -622,11 +650,12 @@ __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant_
                 const int na = W.nact[o];
                 if (na > 0 && !((bnd >> best) & 1u) && na < max_db && qn == 0) {
                     const double ts0 = W.tseg[o], L = W.Ls[o];
+                    const double dL = CTX ? W.dL[o] : 0.0;
                     const int s0 = W.st0[o];
-                    const int sj = first_boundary_ge(ts0, L, s0, W.stm[o], t);
+                    const int sj = seg_first_ge(ts0, L, dL, s0, W.stm[o], t, gr);
                     if (sj < W.nxs[o]) {
                         W.nxs[o] = sj;
-                        set_tnext(best, ts0 + (double)(sj - s0) * L);
+                        set_tnext(best, seg_bnd(ts0, L, dL, sj - s0, gr));
                     }
                 }
             }
@@ -654,7 +683,12 @@ __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant_
                     const int kk = h;
                     qn--;
                     if (qn > 0) h = (int)link[(size_t)kk * 32];
-                    const int out = hots[kk].meta & 0x7fffffff;
+                    // most joiners were routed at one of the last two transfer ends
+                    int meta;
+                    if (kk == ck0) meta = cm0;
+                    else if (kk == ck1) meta = cm1;
+                    else meta = hots[kk].meta;
+                    const int out = meta & 0x7fffffff;
                     if (P.c_prefetch) asm volatile("prefetch.global.L2 [%0];" :: "l"(recs + kk));
                     const int fin = step + (out - 1);
                     const int b = fin & Wm;
@@ -669,7 +703,7 @@ __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant_
                         *wp = old | bit;
                     }
                     n++;
-                    if (CTX) W.ctx[o] += itk[hots[kk].id];
+                    if (CTX) { W.ctx[o] += itk[hots[kk].id]; W.sj[o] += step; }
                     mf = fin < mf ? fin : mf;
                     joined = true;
                 }
@@ -678,28 +712,38 @@ __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant_
                 W.nact[o] = n;
                 if (n > 0) {
                     double ts0 = W.tseg[o], L = W.Ls[o];
+                    double dL = CTX ? W.dL[o] : 0.0;
                     int s0 = W.st0[o];
                     if (was_idle || joined || ((touched >> (w + 16)) & 1u)) {
                         ts0 = t;
                         s0 = step;
                         const int cix = (int)((dcx >> (9 * w)) & 511u);
                         double xv = P.m.dec_fixed + P.m.dec_per_seq * (double)n;
-                        if (CTX) xv = xv + P.m.dec_per_ctx * (double)W.ctx[o];
+                        if (CTX) {          // A15 / A40 context of the segment's first step
+                            long long cc = W.ctx[o];
+                            if (gr) cc += (long long)n * (step + 1) - W.sj[o];
+                            xv = xv + P.m.dec_per_ctx * (double)cc;
+                        }
                         L = xv / sdt[cix];
                         W.tseg[o] = ts0; W.st0[o] = s0; W.Ls[o] = L;
+                        if (CTX) {
+                            dL = gr ? (P.m.dec_per_ctx * (double)n) / sdt[cix] : 0.0;
+                            W.dL[o] = dL;
+                        }
                     }
                     W.mfin[o] = mf;
                     W.nxs[o] = mf;
-                    set_tnext(w, ts0 + (double)(mf - s0) * L);
+                    set_tnext(w, seg_bnd(ts0, L, dL, mf - s0, gr));
                 } else {
                     W.mfin[o] = 0x7fffffff;
                     set_tnext(w, PAD_INF);
                 }
             }
         }
+        if (!CTX && dpend) complete(drc, dt, (dt - drc.pe) / (double)((drc.meta & 0x7fffffff) - 1));
         P.rep_met[r] = met;
         P.rep_near[r] = near;
-        const double dur = R > 0 ? maxcomp - P.s_unit[off] * (1.0 / (P.qps[q] * (double)P.N)) : 0.0;
+        const double dur = R > 0 ? maxcomp - P.s_unit[off] * inv_lam : 0.0;
         P.rep_dur[r] = dur;
         P.rep_good[r] = dur > 0 ? (double)met / dur : 0.0;
         P.rep_events[r] = inst;

@@ -1,0 +1,7 @@
+python -m pytest tests -m gpu -q -x 2>&1 | tail -30 > gpurun_out/gpu_tests.log
+python bench.py --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 0 > gpurun_out/bench21_cfg4.log 2>&1
+PADSIM_J_WIDE=1 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 0 > gpurun_out/bench21_cfg4_wide.log 2>&1
+PADSIM_J_WIDE=1 PADSIM_JOINT_WITH_A=1 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 0 > gpurun_out/bench21_cfg4_wide_jwa.log 2>&1
+PADSIM_JOINT_WITH_A=1 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 0 > gpurun_out/bench21_cfg4_jwa.log 2>&1
+python bench.py --config cfg2 --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 0 > gpurun_out/bench21_cfg2.log 2>&1
+tail -4 gpurun_out/gpu_tests.log
