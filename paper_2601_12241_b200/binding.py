@@ -12,7 +12,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpadsim.so")
+# PADSIM_LIB: load another build of the same library (A/B experiments only)
+LIB_PATH = os.environ.get("PADSIM_LIB") or os.path.join(HERE, "libpadsim.so")
 
 MAX_GPUS = 64
 MAX_ANCHORS = 8

@@ -117,6 +117,7 @@ struct Plan {
     size_t warp_bytes;
     int smem_trace;                    // stage the trace in shared memory (TMA bulk)
     float sync_win;                    // lane clock window, mean inter-arrival times (0 = off)
+    int lpw;                           // replays per warp item (joint kernel; 32, or fewer for small workloads)
     size_t smem_trace_bytes;
 };
 

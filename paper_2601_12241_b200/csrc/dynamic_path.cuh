@@ -889,9 +889,11 @@ __global__ void __launch_bounds__(TB) __maxnreg__(MR) joint_kernel(const __grid_
         int item = 0;
         if (lane == 0) item = (int)atomicAdd(P.work + s, 1u);
         item = __shfl_sync(0xffffffffu, item, 0);
-        if (item * 32 >= QC) break;
-        const int u = item * 32 + lane;
-        if (u >= QC) continue;
+        // an item is P.lpw replays: fewer than 32 lanes per warp when the whole
+        // workload has too few replays to give every SM several warps
+        if (item * P.lpw >= QC) break;
+        const int u = item * P.lpw + lane;
+        if (lane >= P.lpw || u >= QC) continue;
         const int q = u / P.n_clist;
         const int c = P.clist[u - q * P.n_clist];
         const long long r = ((long long)c * P.Q + q) * P.S + s;

@@ -609,7 +609,10 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
         AL(scr, (size_t)grid * per_cta);
         F.scrC = scr;
         ctx->fC_grid = (int)grid;
-        ctx->j_with_a = getenv("PADSIM_JOINT_WITH_A") != nullptr;
+        // the joint replays wait for stage A only when stage A has enough replays
+        // to fill the GPU on its own (cfg 4); a small stage A (cfg 3: 32 long
+        // replays, latency-bound) runs next to them instead of delaying them
+        ctx->j_with_a = GQS < (long long)ctx->n_sm * kThreads || getenv("PADSIM_JOINT_WITH_A") != nullptr;
     }
     F.rep_met = ctx->d_rep_met; F.rep_near = ctx->d_rep_near; F.rep_dur = ctx->d_rep_dur;
     F.rep_good = ctx->d_rep_good; F.rep_events = ctx->d_rep_events;
@@ -981,7 +984,17 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
         int occj = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occj, fnj, tbj, jb));
         occj = std::max(occj, 1);
-        const long long items = ((long long)n_qps * P.n_clist + 31) / 32;
+        // replays per warp item: 32, or fewer when the joint workload would leave
+        // the SMs with fewer than ~4 latency-bound warps each (measured on cfg 3,
+        // 13.4k replays: 32 lanes 464 ms, 16 lanes 387 ms, 8 lanes 452 ms)
+        {
+            const long long UJ2 = (long long)n_traces * n_qps * P.n_clist;
+            int lpw = 32;
+            while (lpw > 4 && UJ2 / lpw < (long long)ctx->n_sm * 4) lpw >>= 1;
+            if (const char* e = getenv("PADSIM_J_LPW")) lpw = std::max(1, std::min(32, atoi(e)));   // knob
+            P.lpw = lpw;
+        }
+        const long long items = ((long long)n_qps * P.n_clist + P.lpw - 1) / P.lpw;
         const int wpc = tbj / 32;
         long long per_trace = std::max<long long>(1, ((long long)ctx->n_sm * occj) / n_traces);
         per_trace = std::min<long long>(per_trace, (items + wpc - 1) / wpc);

@@ -71,6 +71,10 @@ struct __align__(16) SRec {
     unsigned fl;    // TTFT flags | id << 10
 };
 constexpr int kRecIdShift = 10;
+#ifndef PADSIM_KDEFER
+#define PADSIM_KDEFER 1
+#endif
+constexpr int kDefer = PADSIM_KDEFER;     // stage C completion scoring delay (records in flight)
 constexpr int kRecMaxReq = 1 << 22;
 
 struct FPlan {
@@ -429,8 +433,10 @@ constexpr size_t kCWorkCtxBytes = (size_t)kNW * kThreads * (2 * sizeof(long long
 // IDX: stream-index type of link[] and the wheel heads — uint16_t when
 // n_req ≤ 32767 (halves the scratch footprint and its DRAM/L2 traffic),
 // else uint32_t; the top bit flags "more members chained through link[]".
+// 168 registers: shared memory already caps stage C at 3 CTAs/SM, which 168
+// registers still allow (3 x 128 x 168 <= 64 K); launched with kThreads threads
 template <bool CTX, typename IDX>
-__global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant__ FPlan P) {
+__global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) {
     constexpr unsigned kMulti = sizeof(IDX) == 2 ? 0x8000u : 0x80000000u;
     extern __shared__ __align__(128) unsigned char smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -524,9 +530,12 @@ __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant_
         for (int z = 0; z < kMaxSloSweep; z++) metk[z] = 0;
         const int nk = P.sw.n;
         int ck0 = -1, cm0 = 0, ck1 = -1, cm1 = 0;   // last two routed (stream index, meta)
-        SRec drc;                          // deferred completion (non-CTX)
-        double dt = 0.0;
-        bool dpend = false;
+        // deferred completions (non-CTX): a kDefer-deep FIFO in registers, shifted
+        // with static indices; an entry is scored kDefer completions after its
+        // record load was issued, so the load latency is hidden
+        SRec drc[kDefer];
+        double dt[kDefer];
+        int dn = 0;                        // valid entries (0..kDefer)
         // scoring of one completion (`completed` is counted where the member
         // leaves: scoring may be deferred past the end of the event loop)
         auto complete = [&](const SRec& rc, double t, double tpot) {
@@ -593,10 +602,16 @@ __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant_
                             // issue this one's record load and use it at the next
                             // completion (or the end of the replay), so the load
                             // latency overlaps the rest of the event processing
-                            if (dpend) complete(drc, dt, (dt - drc.pe) / (double)((drc.meta & 0x7fffffff) - 1));
-                            drc = recs[kk];
-                            dt = t;
-                            dpend = true;
+                            if (dn == kDefer) {
+                                const SRec& e = drc[kDefer - 1];
+                                complete(e, dt[kDefer - 1], (dt[kDefer - 1] - e.pe) / (double)((e.meta & 0x7fffffff) - 1));
+                            } else {
+                                dn++;
+                            }
+#pragma unroll
+                            for (int z = kDefer - 1; z > 0; z--) { drc[z] = drc[z - 1]; dt[z] = dt[z - 1]; }
+                            drc[0] = recs[kk];
+                            dt[0] = t;
                             completed++;
                         }
                         left++;
@@ -740,7 +755,11 @@ __global__ void __launch_bounds__(kThreads) stageC_kernel(const __grid_constant_
                 }
             }
         }
-        if (!CTX && dpend) complete(drc, dt, (dt - drc.pe) / (double)((drc.meta & 0x7fffffff) - 1));
+        if (!CTX) {
+#pragma unroll
+            for (int z = 0; z < kDefer; z++)
+                if (z < dn) complete(drc[z], dt[z], (dt[z] - drc[z].pe) / (double)((drc[z].meta & 0x7fffffff) - 1));
+        }
         P.rep_met[r] = met;
         P.rep_near[r] = near;
         const double dur = R > 0 ? maxcomp - P.s_unit[off] * inv_lam : 0.0;
