@@ -106,6 +106,9 @@ struct padsim_ctx {
     cudaEvent_t evJ0 = nullptr, evJ1 = nullptr;
     cudaStream_t side = nullptr;     // joint kernel runs concurrently with stages A/C
     cudaEvent_t evC0 = nullptr;
+    cudaStream_t sideC[kNumKC] = {nullptr, nullptr, nullptr};   // stage C classes run concurrently
+    cudaEvent_t evCk[kNumKC] = {nullptr, nullptr, nullptr};    // class joins
+    cudaEvent_t evCf = nullptr;                                  // class fork
     bool j_with_a = false;           // experiment knob: joint replays next to stage A
     bool ev_recorded = false;
     // factorized static path (N <= 8)
@@ -113,6 +116,10 @@ struct padsim_ctx {
     FPlan fplan{};
     int fA_grid = 0, fC_grid = 0;
     size_t fC_smem = 0, fA_smem = 0;
+    // stage C decode-pool classes (static_path.cuh kc_class): cc range, grid, smem
+    int kc_base[kNumKC] = {0, 0, 0}, kc_n[kNumKC] = {0, 0, 0}, kc_grid[kNumKC] = {0, 0, 0};
+    size_t kc_smem[kNumKC] = {0, 0, 0}, kc_off_sdec[kNumKC] = {0, 0, 0};
+    char* kc_scr[kNumKC] = {nullptr, nullptr, nullptr};
     int fA_tb = kThreads;
     bool fC_idx16 = false;
     int j_tb[2] = {kThreads, kThreads};
@@ -441,6 +448,32 @@ static int validate_policy(padsim_ctx* ctx, const padsim_policy* p, const padsim
     return PADSIM_OK;
 }
 
+// stage C instantiation for (context term, 16-bit indices, decode-pool class)
+template <int KW>
+static const void* stagec_fn_kw(bool cm, bool i16) {
+    return cm ? (i16 ? (const void*)stageC_kernel<true, unsigned short, KW> : (const void*)stageC_kernel<true, unsigned, KW>)
+              : (i16 ? (const void*)stageC_kernel<false, unsigned short, KW> : (const void*)stageC_kernel<false, unsigned, KW>);
+}
+static const void* stagec_fn(bool cm, bool i16, int kc) {
+    return kc == 0 ? stagec_fn_kw<kc_kw(0)>(cm, i16) : kc == 1 ? stagec_fn_kw<kc_kw(1)>(cm, i16)
+                                                               : stagec_fn_kw<kc_kw(2)>(cm, i16);
+}
+template <int KW>
+static void stagec_launch_kw(bool cm, bool i16, int grid, size_t smem, cudaStream_t st, const FPlan& F) {
+    if (i16) {
+        if (cm) stageC_kernel<true, unsigned short, KW><<<grid, kThreads, smem, st>>>(F);
+        else stageC_kernel<false, unsigned short, KW><<<grid, kThreads, smem, st>>>(F);
+    } else {
+        if (cm) stageC_kernel<true, unsigned, KW><<<grid, kThreads, smem, st>>>(F);
+        else stageC_kernel<false, unsigned, KW><<<grid, kThreads, smem, st>>>(F);
+    }
+}
+static void stagec_launch(bool cm, bool i16, int kc, int grid, size_t smem, cudaStream_t st, const FPlan& F) {
+    if (kc == 0) stagec_launch_kw<kc_kw(0)>(cm, i16, grid, smem, st, F);
+    else if (kc == 1) stagec_launch_kw<kc_kw(1)>(cm, i16, grid, smem, st, F);
+    else stagec_launch_kw<kc_kw(2)>(cm, i16, grid, smem, st, F);
+}
+
 // Groups static candidates by their prefill pool (caps of the prefill GPUs in
 // GPU-id order) and lays out stage A / stage C (static_path.cuh).
 static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const padsim_slo* slo, int Q,
@@ -473,8 +506,17 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
         for (int w = 0; w < kNW; w++) e.dcap[w] = w < e.y ? dc[w] : model->min_w;
         ccs.push_back(e);
     }
-    std::stable_sort(ccs.begin(), ccs.end(), [](const CC& a, const CC& b) { return a.group < b.group; });
+    // decode-pool classes (y ≤ 2, ≤ 4, ≤ 7): one stage C launch per class with
+    // register arrays / shared-memory SoA sized to the class; within a class
+    // lanes of a warp are consecutive candidates sorted by prefill group
+    std::stable_sort(ccs.begin(), ccs.end(), [](const CC& a, const CC& b) {
+        const int ka = kc_class(a.y), kb = kc_class(b.y);
+        return ka != kb ? ka < kb : a.group < b.group;
+    });
     const int G = (int)gx.size(), NC = (int)ccs.size();
+    for (int k = 0; k < kNumKC; k++) { ctx->kc_base[k] = 0; ctx->kc_n[k] = 0; }
+    for (int k = 0; k < NC; k++) ctx->kc_n[kc_class(ccs[k].y)]++;
+    for (int k = 1; k < kNumKC; k++) ctx->kc_base[k] = ctx->kc_base[k - 1] + ctx->kc_n[k - 1];
     std::vector<int> cc_cand(NC), cc_group(NC), cc_y(NC), cc_dcap((size_t)NC * kNW);
     for (int k = 0; k < NC; k++) {
         cc_cand[k] = ccs[k].cand; cc_group[k] = ccs[k].group; cc_y[k] = ccs[k].y;
@@ -571,12 +613,10 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
         F.c_off_bits = take((size_t)kNW * (wheel / 32) * 32 * sizeof(unsigned));
         F.c_warp_bytes = off;
         unsigned* d_wc;
-        AL(d_wc, S);
+        AL(d_wc, (size_t)kNumKC * S);             // work counters per (class, trace)
         F.work = d_wc;
         ctx->d_workC = d_wc;
         const bool ctxm = model->decode_per_ctx_tok_s != 0.0;
-        const size_t wbytes = kCWorkBytes + (ctxm ? kCWorkCtxBytes : 0);
-        const size_t bbytes = (size_t)kNW * (wheel / 32) * kThreads * sizeof(unsigned);
         F.bits_in_smem = wheel <= 256 ? 1 : 0;
         if (getenv("PADSIM_BITS_GLOBAL")) F.bits_in_smem = 0;          // experiment knob
         F.c_prefetch = getenv("PADSIM_NO_PREFETCH") ? 0 : 1;            // experiment knob
@@ -586,29 +626,42 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
         F.sync_win = 0.f;
         if (const char* e = getenv("PADSIM_SYNC_WIN_C")) F.sync_win = (float)atof(e);   // experiment knob
         F.smem_trace = 0;
-        F.c_off_sdec = wbytes + (F.bits_in_smem ? bbytes : 0);
-        ctx->fC_smem = F.c_off_sdec + (size_t)F.m.ncap * sizeof(double);
-        const void* fn = ctxm ? (idx16 ? (const void*)stageC_kernel<true, unsigned short>
-                                       : (const void*)stageC_kernel<true, unsigned>)
-                              : (idx16 ? (const void*)stageC_kernel<false, unsigned short>
-                                       : (const void*)stageC_kernel<false, unsigned>);
-        CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->fC_smem));
-        int occ = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, ctx->fC_smem));
-        occ = std::max(occ, 1);
-        const long long items = ((long long)Q * NC + 31) / 32;        // warp items per trace
-        long long per_trace = std::max<long long>(1, ((long long)ctx->n_sm * occ) / S);
-        per_trace = std::min<long long>(per_trace, (items + kWarps - 1) / kWarps);
         size_t fr = 0, tm = 0;
         CK(cudaMemGetInfo(&fr, &tm));
         const size_t per_cta = off * kWarps;
         const long long cap_ctas = std::max<long long>(S, (long long)((tm * 3 / 10) / per_cta));
-        long long grid = std::min<long long>(per_trace * S, (cap_ctas / S) * S);
-        grid = std::max<long long>(grid, S);
-        char* scr;
-        AL(scr, (size_t)grid * per_cta);
-        F.scrC = scr;
-        ctx->fC_grid = (int)grid;
+        long long grid_max = S;
+        for (int kc = 0; kc < kNumKC; kc++) {
+            ctx->kc_grid[kc] = 0;
+            if (ctx->kc_n[kc] == 0) continue;
+            const int KWc = kc_kw(kc);
+            const size_t wbytes = (size_t)KWc * kThreads * (kCWorkSlotBytes + (ctxm ? kCWorkCtxSlotBytes : 0));
+            const size_t bbytes = (size_t)KWc * (wheel / 32) * kThreads * sizeof(unsigned);
+            ctx->kc_off_sdec[kc] = wbytes + (F.bits_in_smem ? bbytes : 0);
+            ctx->kc_smem[kc] = ctx->kc_off_sdec[kc] + (size_t)F.m.ncap * sizeof(double);
+            const void* fn = stagec_fn(ctxm, idx16, kc);
+            CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->kc_smem[kc]));
+            int occ = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, ctx->kc_smem[kc]));
+            occ = std::max(occ, 1);
+            const long long items = ((long long)Q * ctx->kc_n[kc] + 31) / 32;   // warp items per trace
+            long long per_trace = std::max<long long>(1, ((long long)ctx->n_sm * occ) / S);
+            per_trace = std::min<long long>(per_trace, (items + kWarps - 1) / kWarps);
+            long long grid = std::min<long long>(per_trace * S, (cap_ctas / S) * S);
+            grid = std::max<long long>(grid, S);
+            ctx->kc_grid[kc] = (int)grid;
+            grid_max = std::max(grid_max, grid);
+        }
+        // classes run concurrently: each has its own scratch slice
+        for (int kc = 0; kc < kNumKC; kc++) {
+            ctx->kc_scr[kc] = nullptr;
+            if (ctx->kc_n[kc] == 0) continue;
+            char* scr;
+            AL(scr, (size_t)ctx->kc_grid[kc] * per_cta);
+            ctx->kc_scr[kc] = scr;
+        }
+        F.scrC = nullptr;
+        ctx->fC_grid = (int)grid_max;
         // the joint replays wait for stage A only when stage A has enough replays
         // to fill the GPU on its own (cfg 4); a small stage A (cfg 3: 32 long
         // replays, latency-bound) runs next to them instead of delaying them
@@ -665,6 +718,9 @@ void padsim_destroy(padsim_ctx* ctx) {
     if (ctx->evJ1) cudaEventDestroy(ctx->evJ1);
     if (ctx->side) cudaStreamDestroy(ctx->side);
     if (ctx->evC0) cudaEventDestroy(ctx->evC0);
+    for (auto& x : ctx->sideC) if (x) cudaStreamDestroy(x);
+    for (auto& e : ctx->evCk) if (e) cudaEventDestroy(e);
+    if (ctx->evCf) cudaEventDestroy(ctx->evCf);
     delete ctx;
 }
 
@@ -1084,6 +1140,9 @@ int padsim_run(padsim_ctx* ctx, void* stream) {
         CK(cudaEventCreate(&ctx->evJ1));
         CK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
         CK(cudaEventCreate(&ctx->evC0));
+        for (auto& x : ctx->sideC) CK(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+        for (auto& e : ctx->evCk) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ctx->evCf, cudaEventDisableTiming));
     }
     CK(cudaEventRecord(ctx->ev0, st));
     // Schedule (measured on cfg 4): stage A runs first on the whole GPU; the joint
@@ -1135,20 +1194,33 @@ int padsim_run(padsim_ctx* ctx, void* stream) {
     CK(cudaEventRecord(ctx->evJ1, js));
     CK(cudaEventRecord(ctx->evC0, st));
     if (ctx->fact) {
-        CK(cudaMemsetAsync(ctx->d_workC, 0, (size_t)ctx->S * sizeof(unsigned), st));
-        FPlan F = ctx->fplan;
-        F.s_begin = 0;
-        F.s_count = ctx->S;
+        CK(cudaMemsetAsync(ctx->d_workC, 0, (size_t)kNumKC * ctx->S * sizeof(unsigned), st));
+        CK(cudaEventRecord(ctx->evCf, st));
         const bool cm = ctx->model.decode_per_ctx_tok_s != 0.0;
-        const int gc = ctx->fC_grid;
-        if (ctx->fC_idx16) {
-            if (cm) stageC_kernel<true, unsigned short><<<gc, kThreads, ctx->fC_smem, st>>>(F);
-            else stageC_kernel<false, unsigned short><<<gc, kThreads, ctx->fC_smem, st>>>(F);
-        } else {
-            if (cm) stageC_kernel<true, unsigned><<<gc, kThreads, ctx->fC_smem, st>>>(F);
-            else stageC_kernel<false, unsigned><<<gc, kThreads, ctx->fC_smem, st>>>(F);
+        // one launch per decode-pool class, on their own streams so that each
+        // class's tail overlaps the others (they share nothing but the stream
+        // records written by stage A and the scratch — each class gets its own
+        // scratch slice)
+        for (int kc = 0; kc < kNumKC; kc++) {
+            if (ctx->kc_n[kc] == 0) continue;
+            cudaStream_t cs = ctx->sideC[kc];
+            CK(cudaStreamWaitEvent(cs, ctx->evCf, 0));
+            FPlan F = ctx->fplan;
+            F.s_begin = 0;
+            F.s_count = ctx->S;
+            F.cc_base = ctx->kc_base[kc];
+            F.n_cc = ctx->kc_n[kc];
+            F.work = ctx->d_workC + (size_t)kc * ctx->S;
+            F.c_off_sdec = ctx->kc_off_sdec[kc];
+            F.scrC = ctx->kc_scr[kc];
+            stagec_launch(cm, ctx->fC_idx16, kc, ctx->kc_grid[kc], ctx->kc_smem[kc], cs, F);
+            CK(cudaGetLastError());
         }
-        CK(cudaGetLastError());
+        for (int kc = 0; kc < kNumKC; kc++) {
+            if (ctx->kc_n[kc] == 0) continue;
+            CK(cudaEventRecord(ctx->evCk[kc], ctx->sideC[kc]));
+            CK(cudaStreamWaitEvent(st, ctx->evCk[kc], 0));
+        }
     }
     CK(cudaEventRecord(ctx->evC, st));
     if (js != st) CK(cudaStreamWaitEvent(st, ctx->evJ1, 0));   // join

@@ -33,6 +33,11 @@ namespace padsim {
 
 constexpr int kNW = 7;   // ≤ 7 workers per role when N ≤ 8 (each role has ≥ 1 GPU)
 
+// stage C decode-pool classes: y ≤ 2, y ≤ 4, y ≤ 7 decode GPUs → KW = 2, 4, 7
+constexpr int kNumKC = 3;
+__host__ __device__ constexpr int kc_class(int y) { return y <= 2 ? 0 : (y <= 4 ? 1 : 2); }
+__host__ __device__ constexpr int kc_kw(int k) { return k == 0 ? 2 : (k == 1 ? 4 : kNW); }
+
 // Register-array helpers: a run-time index selects with predicated moves only
 // (no branches, no local memory).
 template <int N, class T>
@@ -111,6 +116,7 @@ struct FPlan {
     const int* cc_group;    // [n_cc] prefill group
     const int* cc_y;        // [n_cc] decode workers
     const int* cc_dcap;     // [n_cc][kNW] decode caps, D-id order
+    int cc_base;            // this launch's candidate class: cc entries [cc_base, cc_base + n_cc)
     int items_per_trace, n_items;
     unsigned* work;
     char* scrC;
@@ -428,14 +434,18 @@ struct CWork {            // per-thread shared-memory SoA views (stride kThreads
     double* dL;              // CTX: per-step latency growth of the segment (A40)
 };
 
-constexpr size_t kCWorkBytes = (size_t)kNW * kThreads * (2 * sizeof(double) + 8 * sizeof(int));
-constexpr size_t kCWorkCtxBytes = (size_t)kNW * kThreads * (2 * sizeof(long long) + sizeof(double));
+// stage C shared-memory SoA bytes per decode-worker slot (× KW × kThreads)
+constexpr size_t kCWorkSlotBytes = 2 * sizeof(double) + 8 * sizeof(int);
+constexpr size_t kCWorkCtxSlotBytes = 2 * sizeof(long long) + sizeof(double);
 // IDX: stream-index type of link[] and the wheel heads — uint16_t when
 // n_req ≤ 32767 (halves the scratch footprint and its DRAM/L2 traffic),
 // else uint32_t; the top bit flags "more members chained through link[]".
-// 168 registers: shared memory already caps stage C at 3 CTAs/SM, which 168
-// registers still allow (3 x 128 x 168 <= 64 K); launched with kThreads threads
-template <bool CTX, typename IDX>
+// KW: decode-worker slots (2, 4 or 7).  Candidates are launched in classes by
+// their decode pool size y ≤ KW, so replays with few decode GPUs run with
+// smaller register arrays / shared-memory SoA (fewer instructions per event,
+// more resident warps).  168 registers: shared memory caps KW = 7 at 3 CTAs/SM,
+// which 168 registers still allow; launched with kThreads threads.
+template <bool CTX, typename IDX, int KW>
 __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) {
     constexpr unsigned kMulti = sizeof(IDX) == 2 ? 0x8000u : 0x80000000u;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -443,14 +453,14 @@ __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) 
     char* wb = P.scrC + ((size_t)blockIdx.x * kWarps + warp) * P.c_warp_bytes;
     IDX* link = (IDX*)wb + lane;                                       // [k*32]
     const int Wh = P.wheel, Wm = P.wheel - 1, nwords = P.wheel >> 5;
-    IDX* heads = (IDX*)(wb + P.c_off_heads) + (size_t)lane * kNW * Wh;   // per lane
+    IDX* heads = (IDX*)(wb + P.c_off_heads) + (size_t)lane * KW * Wh;    // per lane
     const int max_db = P.m.max_db;
     CWork W;
     unsigned* bits;
     int bstride;
     {
         unsigned char* p = smem;
-        const int n = kNW * kThreads;
+        const int n = KW * kThreads;
         W.tseg = (double*)p + tid; p += n * sizeof(double);
         W.Ls = (double*)p + tid; p += n * sizeof(double);
         int* ib = (int*)p;
@@ -489,7 +499,7 @@ __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) 
         const int u = item * 32 + lane;
         if (u >= QC) continue;
         const int q = u / P.n_cc;
-        const int cc = u - q * P.n_cc;
+        const int cc = P.cc_base + (u - q * P.n_cc);
         const int c = P.cc_cand[cc];
         const int g = P.cc_group[cc];
         const int y = P.cc_y[cc];
@@ -503,12 +513,12 @@ __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) 
         // decode cap indices of this candidate, 9 bits per worker (ncap ≤ 512)
         unsigned long long dcx = 0ull;
 #pragma unroll
-        for (int w = 0; w < kNW; w++)
+        for (int w = 0; w < KW; w++)
             dcx |= (unsigned long long)(P.cc_dcap[cc * kNW + w] - P.m.min_w) << (9 * w);
-        double tnext[kNW];
-        int ld[kNW];                       // routing load: active + pending (A13)
+        double tnext[KW];
+        int ld[KW];                        // routing load: active + pending (A13)
 #pragma unroll
-        for (int w = 0; w < kNW; w++) {
+        for (int w = 0; w < KW; w++) {
             const int o = w * kThreads;
             tnext[w] = PAD_INF;
             ld[w] = w < y ? 0 : 0x7fffffff;
@@ -524,7 +534,7 @@ __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) 
         if (R > 0) nxt = hots[0]; else { nxt.te = PAD_INF; nxt.meta = 0; nxt.id = 0; }
         double tk = nxt.te;
         long long inst = 0;
-        auto set_tnext = [&](int wd, double v) { rset<kNW>(tnext, wd, v); };
+        auto set_tnext = [&](int wd, double v) { rset<KW>(tnext, wd, v); };
         int metk[kMaxSloSweep];
 #pragma unroll
         for (int z = 0; z < kMaxSloSweep; z++) metk[z] = 0;
@@ -568,7 +578,7 @@ __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) 
         while (completed < R) {
             double t = tk;
 #pragma unroll
-            for (int w = 0; w < kNW; w++) t = tnext[w] < t ? tnext[w] : t;
+            for (int w = 0; w < KW; w++) t = tnext[w] < t ? tnext[w] : t;
             if (win > 0.f) {
                 const float tf = (float)t;
                 const unsigned mn = __reduce_min_sync(__activemask(), __float_as_uint(tf));
@@ -577,7 +587,7 @@ __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) 
             inst++;
             unsigned bnd = 0, touched = 0;
 #pragma unroll
-            for (int w = 0; w < kNW; w++) if (tnext[w] == t) bnd |= 1u << w;
+            for (int w = 0; w < KW; w++) if (tnext[w] == t) bnd |= 1u << w;
             // kind 3: materialised step boundaries, worker order
             for (unsigned m = bnd; m; m &= m - 1) {
                 const int w = __ffs(m) - 1;
@@ -634,7 +644,7 @@ __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) 
                         mf = sN + ((((wi << 5) + __ffs(mword) - 1) - b) & Wm);
                     }
                     W.mfin[o] = mf;
-                    radd<kNW, int>(ld, w, -left);
+                    radd<KW, int>(ld, w, -left);
                     touched |= 1u << (w + 16);          // composition changed
                 }
             }
@@ -653,8 +663,8 @@ __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) 
                 }
                 int best = 0, bl = ld[0];
 #pragma unroll
-                for (int w = 1; w < kNW; w++) if (ld[w] < bl) { bl = ld[w]; best = w; }
-                radd<kNW, int>(ld, best, 1);
+                for (int w = 1; w < KW; w++) if (ld[w] < bl) { bl = ld[w]; best = w; }
+                radd<KW, int>(ld, best, 1);
                 ck1 = ck0; cm1 = cm0; ck0 = kk; cm0 = hc.meta;
                 const int o = best * kThreads;
                 const int qn = W.ql[o];
@@ -681,7 +691,7 @@ __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) 
                 bool ab = (bnd >> w) & 1u;
                 int n = W.nact[o];
                 if (n > 0 && !ab) {
-                    if (rget<kNW>(tnext, w) != t) continue;   // mid-step
+                    if (rget<KW>(tnext, w) != t) continue;   // mid-step
                     W.stm[o] = W.nxs[o];                 // join boundary exactly at t
                     ab = true;
                 }
