@@ -43,6 +43,15 @@ struct DevModel {
     const double* ltab;                // [ncap][max_db] decode step latency, n = 1..max_db
 };
 
+// Prefetch (to L2) of the timing-wheel head of a decode worker's next finish
+// bucket, issued when that bucket becomes known and read at the next leave.
+// A/B on one box (tools/run_ab.sh): cfg 4 785 -> 770 ms/step; an L1 prefetch
+// (773 ms), keeping the head in registers (807 ms) and deciding the TPOT tests
+// without the FP64 division (814 ms) were no better.
+__device__ __forceinline__ void pf_head(const void* p) {
+    asm volatile("prefetch.global.L2 [%0];" :: "l"(p));
+}
+
 // Decode segment boundaries (A14; A40 with context growth): boundary k of a
 // segment that started at ts0 with first-step latency L and per-step growth dL.
 __device__ __forceinline__ double seg_bnd(double ts0, double L, double dL, int k, bool growth) {

@@ -526,6 +526,7 @@ struct JReplay {
             }
             W.mfin[o] = mf;
             W.b1[o] = mf;
+            pf_head(hw + (size_t)(mf & Wm) * 32);
             set_tnext(g, bnd(o, mf));
         } else {
             W.mfin[o] = kIntMax;

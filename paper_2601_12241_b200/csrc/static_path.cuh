@@ -758,6 +758,7 @@ __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) 
                     }
                     W.mfin[o] = mf;
                     W.nxs[o] = mf;
+                    pf_head(hw + (mf & Wm));
                     set_tnext(w, seg_bnd(ts0, L, dL, mf - s0, gr));
                 } else {
                     W.mfin[o] = 0x7fffffff;
