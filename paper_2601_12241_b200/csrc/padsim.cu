@@ -578,7 +578,14 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
         F.a_warp_bytes = off;
         // small stage-A workloads (e.g. cfg 2: 12k replays) use 32-thread CTAs so every SM
         // gets some of the latency-bound replays; large ones use 128-thread CTAs
-        const int tb = GQS >= (long long)ctx->n_sm * 2 * kThreads ? kThreads : 32;
+        // large ones use 256-thread CTAs: the staged trace is shared by 8 warps
+        // and shared memory then holds 16 resident warps per SM instead of 12
+        int tb = GQS >= (long long)ctx->n_sm * 2 * kThreads ? kThreads : 32;
+        if (tb == kThreads && GQS >= (long long)ctx->n_sm * 2 * 256) tb = kATbBig;
+        if (const char* e = getenv("PADSIM_A_TB")) {       // experiment knob: 32 / 128 / 256
+            const int v = atoi(e);
+            if (v == 32 || v == kThreads || v == kATbBig) tb = v;
+        }
         ctx->fA_tb = tb;
         F.a_blocks_per_trace = (int)(((long long)Q * G + tb - 1) / tb);
         const long long ctas = (long long)F.a_blocks_per_trace * S;
@@ -588,11 +595,13 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
         ctx->fA_grid = (int)ctas;
         const size_t Rp = (Rm + 15) & ~(size_t)15;
         const size_t tb_bytes = Rp * (8 + 8 + 4);
-        const size_t wbytes = tb == kThreads ? a_work_bytes<kThreads>() + a_slot_bytes<kThreads>()
+        const size_t wbytes = tb == kATbBig ? a_work_bytes<kATbBig>() + a_slot_bytes<kATbBig>()
+                            : tb == kThreads ? a_work_bytes<kThreads>() + a_slot_bytes<kThreads>()
                                              : a_work_bytes<32>() + a_slot_bytes<32>();
         F.a_smem_trace = wbytes + tb_bytes <= 200 * 1024 ? 1 : 0;
         ctx->fA_smem = wbytes + (F.a_smem_trace ? tb_bytes : 0);
-        const void* fa = tb == kThreads ? (const void*)stageA_kernel<kThreads> : (const void*)stageA_kernel<32>;
+        const void* fa = tb == kATbBig ? (const void*)stageA_kernel<kATbBig>
+                       : tb == kThreads ? (const void*)stageA_kernel<kThreads> : (const void*)stageA_kernel<32>;
         CK(cudaFuncSetAttribute(fa, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->fA_smem));
     }
     // stage C: CTAs bound to one trace each (staged in smem by TMA bulk copies),
@@ -1156,7 +1165,8 @@ int padsim_run(padsim_ctx* ctx, void* stream) {
         F.s_begin = 0;
         F.s_count = ctx->S;
         const int ga = F.a_blocks_per_trace * F.s_count;
-        if (ctx->fA_tb == kThreads) stageA_kernel<kThreads><<<ga, kThreads, ctx->fA_smem, st>>>(F);
+        if (ctx->fA_tb == kATbBig) stageA_kernel<kATbBig><<<ga, kATbBig, ctx->fA_smem, st>>>(F);
+        else if (ctx->fA_tb == kThreads) stageA_kernel<kThreads><<<ga, kThreads, ctx->fA_smem, st>>>(F);
         else stageA_kernel<32><<<ga, 32, ctx->fA_smem, st>>>(F);
         CK(cudaGetLastError());
     }

@@ -156,6 +156,7 @@ __host__ __device__ constexpr size_t a_slot_bytes() {   // KV slots kept in smem
     return TB == 32 ? (size_t)PADSIM_MAX_SLOTS * TB * (2 * sizeof(double) + sizeof(int)) : 0;
 }
 constexpr int kPre = 8;    // ids fetched per batch of independent loads
+constexpr int kATbBig = 256;   // stage A CTA size for large workloads
 
 template <int TB>
 __global__ void __launch_bounds__(TB) stageA_kernel(const __grid_constant__ FPlan P) {
