@@ -119,6 +119,7 @@ struct padsim_ctx {
     // stage C decode-pool classes (static_path.cuh kc_class): cc range, grid, smem
     int kc_base[kNumKC] = {0, 0, 0}, kc_n[kNumKC] = {0, 0, 0}, kc_grid[kNumKC] = {0, 0, 0};
     size_t kc_smem[kNumKC] = {0, 0, 0}, kc_off_sdec[kNumKC] = {0, 0, 0};
+    int kc_bits_smem[kNumKC] = {1, 1, 1};
     char* kc_scr[kNumKC] = {nullptr, nullptr, nullptr};
     int fA_tb = kThreads;
     bool fC_idx16 = false;
@@ -646,7 +647,12 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
             const int KWc = kc_kw(kc);
             const size_t wbytes = (size_t)KWc * kThreads * (kCWorkSlotBytes + (ctxm ? kCWorkCtxSlotBytes : 0));
             const size_t bbytes = (size_t)KWc * (wheel / 32) * kThreads * sizeof(unsigned);
-            ctx->kc_off_sdec[kc] = wbytes + (F.bits_in_smem ? bbytes : 0);
+            int bsm = F.bits_in_smem;
+            // experiment knob: the largest class keeps its wheel bitmaps in global
+            // memory so more of its warps fit in shared memory
+            if (kc == kNumKC - 1 && getenv("PADSIM_BITS_GLOBAL_BIG")) bsm = 0;
+            ctx->kc_bits_smem[kc] = bsm;
+            ctx->kc_off_sdec[kc] = wbytes + (bsm ? bbytes : 0);
             ctx->kc_smem[kc] = ctx->kc_off_sdec[kc] + (size_t)F.m.ncap * sizeof(double);
             const void* fn = stagec_fn(ctxm, idx16, kc);
             CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->kc_smem[kc]));
@@ -1222,6 +1228,7 @@ int padsim_run(padsim_ctx* ctx, void* stream) {
             F.n_cc = ctx->kc_n[kc];
             F.work = ctx->d_workC + (size_t)kc * ctx->S;
             F.c_off_sdec = ctx->kc_off_sdec[kc];
+            F.bits_in_smem = ctx->kc_bits_smem[kc];
             F.scrC = ctx->kc_scr[kc];
             stagec_launch(cm, ctx->fC_idx16, kc, ctx->kc_grid[kc], ctx->kc_smem[kc], cs, F);
             CK(cudaGetLastError());
