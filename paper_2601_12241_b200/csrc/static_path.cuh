@@ -155,6 +155,9 @@ template <int TB>
 __host__ __device__ constexpr size_t a_slot_bytes() {   // KV slots kept in smem for small CTAs
     return TB == 32 ? (size_t)PADSIM_MAX_SLOTS * TB * (2 * sizeof(double) + sizeof(int)) : 0;
 }
+#ifndef PADSIM_EAGER
+#define PADSIM_EAGER 1     // stage C eager joins (see the transfer-end handler)
+#endif
 constexpr int kPre = 8;    // ids fetched per batch of independent loads
 constexpr int kATbBig = 256;   // stage A CTA size for large workloads
 
@@ -666,14 +669,69 @@ __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) 
 #pragma unroll
                 for (int w = 1; w < KW; w++) if (ld[w] < bl) { bl = ld[w]; best = w; }
                 radd<KW, int>(ld, best, 1);
-                ck1 = ck0; cm1 = cm0; ck0 = kk; cm0 = hc.meta;
                 const int o = best * kThreads;
                 const int qn = W.ql[o];
+                const int na = W.nact[o];
+                if (PADSIM_EAGER && na > 0 && !((bnd >> best) & 1u) && na < max_db && qn == 0) {
+                    // Eager join: the request joins at the first boundary sj ≥ t of
+                    // the running segment (A14).  When sj precedes the worker's next
+                    // leave, nothing else happens to this worker until sj (routing
+                    // only reads active + pending, unchanged by the join), so the
+                    // dispatch the boundary instant would run is done now: the new
+                    // segment starts at sj (time bnd(sj)) with the joiner admitted.
+                    // A later transfer end at or before bnd(sj) finds sj again as its
+                    // first boundary and joins the same not-yet-started segment.
+                    // Saves the join-only instant; same state as the DES at bnd(sj).
+                    const double ts0 = W.tseg[o], L = W.Ls[o];
+                    const double dL = CTX ? W.dL[o] : 0.0;
+                    const int s0 = W.st0[o];
+                    const int sj = seg_first_ge(ts0, L, dL, s0, W.stm[o], t, gr);
+                    int mf = W.mfin[o];
+                    if (sj < mf) {
+                        const double tj = seg_bnd(ts0, L, dL, sj - s0, gr);
+                        const int out = hc.meta & 0x7fffffff;
+                        if (P.c_prefetch) asm volatile("prefetch.global.L2 [%0];" :: "l"(recs + kk));
+                        const int fin = sj + (out - 1);
+                        const int b = fin & Wm;
+                        IDX* hw = heads + (size_t)best * Wh;
+                        unsigned* wp = bits + (size_t)best * nwords * bstride + (size_t)(b >> 5) * bstride;
+                        const unsigned bit = 1u << (b & 31);
+                        const unsigned old = *wp;
+                        if (old & bit) {
+                            link[(size_t)kk * 32] = hw[b];
+                            hw[b] = (IDX)((unsigned)kk | kMulti);
+                        } else {
+                            hw[b] = (IDX)kk;
+                            *wp = old | bit;
+                        }
+                        const int n = na + 1;
+                        W.nact[o] = n;
+                        if (CTX) { W.ctx[o] += itk[hc.id]; W.sj[o] += sj; }
+                        mf = fin < mf ? fin : mf;
+                        const int cix = (int)((dcx >> (9 * best)) & 511u);
+                        double xv = P.m.dec_fixed + P.m.dec_per_seq * (double)n;
+                        if (CTX) {
+                            long long cc = W.ctx[o];
+                            if (gr) cc += (long long)n * (sj + 1) - W.sj[o];
+                            xv = xv + P.m.dec_per_ctx * (double)cc;
+                        }
+                        const double L2 = xv / sdt[cix];
+                        const double dL2 = (CTX && gr) ? (P.m.dec_per_ctx * (double)n) / sdt[cix] : 0.0;
+                        W.tseg[o] = tj; W.st0[o] = sj; W.Ls[o] = L2;
+                        if (CTX) W.dL[o] = dL2;
+                        W.stm[o] = sj - 1;           // boundaries ≥ sj belong to the new segment
+                        W.mfin[o] = mf;
+                        W.nxs[o] = mf;
+                        set_tnext(best, seg_bnd(tj, L2, dL2, mf - sj, gr));
+                        pf_head(hw + (mf & Wm));
+                        continue;
+                    }
+                }
+                ck1 = ck0; cm1 = cm0; ck0 = kk; cm0 = hc.meta;
                 if (qn == 0) W.qh[o] = kk; else link[(size_t)W.qt[o] * 32] = (IDX)kk;
                 W.qt[o] = kk;
                 W.ql[o] = qn + 1;
                 touched |= 1u << best;
-                const int na = W.nact[o];
                 if (na > 0 && !((bnd >> best) & 1u) && na < max_db && qn == 0) {
                     const double ts0 = W.tseg[o], L = W.Ls[o];
                     const double dL = CTX ? W.dL[o] : 0.0;
