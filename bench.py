@@ -41,7 +41,11 @@ from workloads.configs import dynamic_candidates  # noqa: E402
 
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 TRAFFIC_PATH = os.path.join(ROOT, "profiles", "ncu_traffic.json")   # dram bytes/launch per kernel
-OPS_PER_EVENT = 32          # DESIGN.md §6: algorithmic ALU ops of one DES event handler
+OPS_PER_EVENT = 32          # DESIGN.md §5: algorithmic ALU ops of one DES event handler
+# algorithmic DES events per simulated request: stage A
+# arrival+routing, batch share, KV transfer end; stage C transfer-end routing, join,
+# leave+scoring; the joint replay all six (controller ticks not counted)
+EV_PER_REQ = {"stageA_kernel": 3, "stageC_kernel": 3, "joint_kernel": 6}
 LANES_PER_SM = 128          # INT32/FP32 lanes per SM (4 SMSP x 32)
 
 
@@ -119,6 +123,13 @@ def ncu_traffic(workload: str, kernel: str):
     `workload`, from the committed ncu --set full capture (profiles/), or None."""
     try:
         return json.load(open(TRAFFIC_PATH)).get(workload, {}).get(kernel, {}).get("bytes")
+    except Exception:
+        return None
+
+
+def ncu_field(workload: str, kernel: str, key: str):
+    try:
+        return json.load(open(TRAFFIC_PATH)).get(workload, {}).get(kernel, {}).get(key)
     except Exception:
         return None
 
@@ -299,6 +310,14 @@ def main():
         ev_dyn += ev_static
         ev_static = 0
     events_per_launch = ev_a + ev_static + ev_dyn
+    # simulated requests each kernel processes per launch (the roofline unit)
+    r_sum = sum(int(t["s_unit"].size) for t in traces)
+    static_idx = [c for c in range(C) if pols[c]["kind"] == 0]
+    groups = {tuple(int(v) for v in cap[c][role[c] == 0]) for c in static_idx}
+    fact = ev_a > 0                       # the factorized static path ran (N <= 8)
+    req_k = {"stageA_kernel": len(groups) * Q * r_sum if fact else 0,
+             "stageC_kernel": len(static_idx) * Q * r_sum if fact else 0,
+             "joint_kernel": (C - len(static_idx) + (0 if fact else len(static_idx))) * Q * r_sum}
 
     # e2e: the public one-shot C-ABI call with host buffers
     e2e_times = []
@@ -328,11 +347,12 @@ def main():
         km = np.mean(np.array(kern_ms), axis=0) if kern_ms else np.zeros(3)
         names = ["stageA_kernel", "stageC_kernel", "joint_kernel"]
         evs = [ev_a, ev_static, ev_dyn]
-        # dominant kernel = the one doing most of the algorithmic work (DES
-        # instants); kernels overlap on two streams, so the longest event span is
-        # not necessarily the one the step is made of
-        dom = int(np.argmax(evs))
-        achieved = evs[dom] * OPS_PER_EVENT / (km[dom] / 1e3) / 1e12 if km[dom] > 0 else float("nan")
+        # dominant kernel = the one doing most of the algorithmic work (simulated
+        # requests × events per request); kernels overlap on several streams, so
+        # the longest event span is not necessarily the one the step is made of
+        ops = [req_k[n] * EV_PER_REQ[n] * OPS_PER_EVENT for n in names]
+        dom = int(np.argmax(ops))
+        achieved = ops[dom] / (km[dom] / 1e3) / 1e12 if km[dom] > 0 else float("nan")
         peak = 148 * LANES_PER_SM * f_mhz * 1e6 / 1e12
         cfg4 = get_config("cfg4")
         cfg4_replays = (955 + 21) * len(cfg4["qps"]) * cfg4["seeds"]
@@ -351,7 +371,11 @@ def main():
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tops/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(cfg["name"], names[dom]),
                          "kernel": names[dom], "kernel_ms": float(km[dom]),
-                         "events_per_launch": evs[dom], "ops_per_event": OPS_PER_EVENT,
+                         "unit_basis": "simulated requests x events/request x ops/event",
+                         "requests_per_launch": req_k[names[dom]],
+                         "events_per_request": EV_PER_REQ[names[dom]], "ops_per_event": OPS_PER_EVENT,
+                         "des_instants_per_launch": evs[dom],
+                         "ncu_issue_active": ncu_field(cfg["name"], names[dom], "issue_active"),
                          "peak_basis": f"148 SM x 128 lanes x {f_mhz:.0f} MHz (sampled clock)",
                          "kernels_ms": {n: float(v) for n, v in zip(names, km)},
                          "kernels_events": {n: int(v) for n, v in zip(names, evs)},
