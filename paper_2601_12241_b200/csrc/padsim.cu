@@ -120,6 +120,10 @@ struct padsim_ctx {
     int kc_base[kNumKC] = {0, 0, 0}, kc_n[kNumKC] = {0, 0, 0}, kc_grid[kNumKC] = {0, 0, 0};
     size_t kc_smem[kNumKC] = {0, 0, 0}, kc_off_sdec[kNumKC] = {0, 0, 0};
     int kc_bits_smem[kNumKC] = {1, 1, 1};
+    int kc_ltab[kNumKC] = {0, 0, 0};
+    int kc_hca[kNumKC] = {0, 0, 0};
+    size_t kc_off_hca[kNumKC] = {0, 0, 0};
+    size_t kc_off_ltab[kNumKC] = {0, 0, 0};
     char* kc_scr[kNumKC] = {nullptr, nullptr, nullptr};
     int fA_tb = kThreads;
     bool fC_idx16 = false;
@@ -523,6 +527,16 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
         cc_cand[k] = ccs[k].cand; cc_group[k] = ccs[k].group; cc_y[k] = ccs[k].y;
         for (int w = 0; w < kNW; w++) cc_dcap[(size_t)k * kNW + w] = ccs[k].dcap[w];
     }
+    // rows of the shared-memory decode step table: the distinct decode caps in use
+    std::vector<int> lsl, cc_dslot((size_t)NC * kNW, 0);
+    {
+        std::map<int, int> row;
+        for (int k = 0; k < NC; k++)
+            for (int w = 0; w < kNW; w++) row.emplace(cc_dcap[(size_t)k * kNW + w], 0);
+        int r = 0;
+        for (auto& kv : row) { kv.second = r++; lsl.push_back(kv.first - model->min_w); }
+        for (size_t i = 0; i < cc_dcap.size(); i++) cc_dslot[i] = row[cc_dcap[i]];
+    }
     FPlan& F = ctx->fplan;
     std::memset(&F, 0, sizeof(F));
     F.m.min_w = model->min_w; F.m.max_w = model->max_w; F.m.ncap = model->max_w - model->min_w + 1;
@@ -553,6 +567,11 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
 #define AL(p, n) do { int r_ = dalloc(ctx, &(p), (size_t)(n)); if (r_) return r_; } while (0)
     AL(d_gx, G); AL(d_gcap, (size_t)G * kNW); AL(d_ccc, NC); AL(d_ccg, NC); AL(d_ccy, NC);
     AL(d_ccd, (size_t)NC * kNW);
+    int *d_lsl, *d_ccsl;
+    AL(d_lsl, std::max<size_t>(lsl.size(), 1)); AL(d_ccsl, (size_t)NC * kNW);
+    CK(cudaMemcpy(d_lsl, lsl.data(), sizeof(int) * lsl.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_ccsl, cc_dslot.data(), sizeof(int) * NC * kNW, cudaMemcpyHostToDevice));
+    F.lsl = d_lsl; F.cc_dslot = d_ccsl; F.c_lslots = (int)lsl.size();
     AL(d_rec, GQS * Rm); AL(d_hot, GQS * Rm); AL(d_pe, GQS * Rm); AL(d_evA, GQS);
     AL(d_asq, GQS); AL(d_ase, GQS);
     CK(cudaMemcpy(d_gx, gx.data(), sizeof(int) * G, cudaMemcpyHostToDevice));
@@ -654,6 +673,16 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
             ctx->kc_bits_smem[kc] = bsm;
             ctx->kc_off_sdec[kc] = wbytes + (bsm ? bbytes : 0);
             ctx->kc_smem[kc] = ctx->kc_off_sdec[kc] + (size_t)F.m.ncap * sizeof(double);
+            // decode step table in shared memory for the classes with headroom (the
+            // KW = 7 class is shared-memory bound: it keeps the in-place division)
+            const size_t lbytes = (size_t)F.c_lslots * F.m.max_db * sizeof(double);
+            ctx->kc_ltab[kc] = !ctxm && kc < kNumKC - 1 && F.c_lslots <= kLtabRows && !getenv("PADSIM_NO_LTAB");
+            ctx->kc_off_ltab[kc] = ctx->kc_smem[kc];
+            if (ctx->kc_ltab[kc]) ctx->kc_smem[kc] += lbytes;
+            // async head cache for the KW ≤ 4 classes ([KW][kThreads] words)
+            ctx->kc_hca[kc] = kc < kNumKC - 1 && !getenv("PADSIM_NO_HCA");
+            ctx->kc_off_hca[kc] = ctx->kc_smem[kc];
+            if (ctx->kc_hca[kc]) ctx->kc_smem[kc] += (size_t)KWc * kThreads * sizeof(unsigned);
             const void* fn = stagec_fn(ctxm, idx16, kc);
             CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->kc_smem[kc]));
             int occ = 0;
@@ -1228,6 +1257,10 @@ int padsim_run(padsim_ctx* ctx, void* stream) {
             F.n_cc = ctx->kc_n[kc];
             F.work = ctx->d_workC + (size_t)kc * ctx->S;
             F.c_off_sdec = ctx->kc_off_sdec[kc];
+            F.c_ltab_on = ctx->kc_ltab[kc];
+            F.c_hca_on = ctx->kc_hca[kc];
+            F.c_off_hca = ctx->kc_off_hca[kc];
+            F.c_off_ltab = ctx->kc_off_ltab[kc];
             F.bits_in_smem = ctx->kc_bits_smem[kc];
             F.scrC = ctx->kc_scr[kc];
             stagec_launch(cm, ctx->fC_idx16, kc, ctx->kc_grid[kc], ctx->kc_smem[kc], cs, F);

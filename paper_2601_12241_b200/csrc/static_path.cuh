@@ -124,6 +124,15 @@ struct FPlan {
     int wheel;              // decode timing wheel size (power of 2 ≥ max out_tok, ≥ 32)
     int bits_in_smem;       // wheel occupancy bitmap in shared memory (wheel ≤ 256)
     size_t c_off_sdec;      // byte offset of the s_dec(w) table in shared memory
+    // decode step latency L[slot][n-1] in shared memory for the caps the candidates
+    // use (a3 table; per_ctx = 0 only, small decode-pool classes with smem headroom)
+    int c_hca_on;           // async head cache in shared memory (KW ≤ 4 classes)
+    size_t c_off_hca;       // its byte offset: [KW][kThreads] 32-bit words
+    int c_ltab_on;          // this launch reads L from the table (else xv / s_dec)
+    int c_lslots;           // distinct decode caps (table rows)
+    size_t c_off_ltab;      // byte offset of the table in shared memory
+    const int* lsl;         // [c_lslots] cap index (cap - min_w) of each row
+    const int* cc_dslot;    // [n_cc][kNW] row of each decode worker's cap
     int c_prefetch;         // prefetch the completion record into L2 at decode join
     float sync_win;         // lane clock window in mean inter-arrival times (0 = off)
     int smem_trace;
@@ -159,6 +168,7 @@ __host__ __device__ constexpr size_t a_slot_bytes() {   // KV slots kept in smem
 #define PADSIM_EAGER 1     // stage C eager joins (see the transfer-end handler)
 #endif
 constexpr int kPre = 8;    // ids fetched per batch of independent loads
+constexpr int kLtabRows = 16;  // max distinct decode caps of the shared-memory step table
 constexpr int kATbBig = 256;   // stage A CTA size for large workloads
 
 template <int TB>
@@ -449,6 +459,17 @@ constexpr size_t kCWorkCtxSlotBytes = 2 * sizeof(long long) + sizeof(double);
 // smaller register arrays / shared-memory SoA (fewer instructions per event,
 // more resident warps).  168 registers: shared memory caps KW = 7 at 3 CTAs/SM,
 // which 168 registers still allow; launched with kThreads threads.
+// Async head cache (cp.async, 4 bytes global → shared): the head of a decode
+// worker's next finish bucket is copied into shared memory when the bucket
+// becomes known and read at the next leave, so the leave does not wait for a
+// dependent global load; the copy is asynchronous, so no register waits on it.
+__device__ __forceinline__ void hca_issue(unsigned* sdst, const void* gsrc) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+    const unsigned long long ga = (unsigned long long)__cvta_generic_to_global(gsrc) & ~3ull;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n\tcp.async.commit_group;" :: "r"(sa), "l"(ga) : "memory");
+}
+__device__ __forceinline__ void hca_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 template <bool CTX, typename IDX, int KW>
 __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) {
     constexpr unsigned kMulti = sizeof(IDX) == 2 ? 0x8000u : 0x80000000u;
@@ -489,6 +510,13 @@ __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) 
     // a3 table, so bit-identical) instead of a dependent global table load
     double* sdt = (double*)(smem + P.c_off_sdec);
     for (int i = tid; i < P.m.ncap; i += kThreads) sdt[i] = P.m.sdec[i];
+    double* lts = (double*)(smem + P.c_off_ltab);
+    const bool hca = KW <= 4 && P.c_hca_on;
+    unsigned* hcs = (unsigned*)(smem + P.c_off_hca) + tid;     // [w * kThreads]
+    const bool ltab_on = !CTX && P.c_ltab_on;
+    if (ltab_on)
+        for (int i = tid; i < P.c_lslots * P.m.max_db; i += kThreads)
+            lts[i] = P.m.ltab[(size_t)P.lsl[i / P.m.max_db] * P.m.max_db + i % P.m.max_db];
     __syncthreads();
     const int s = P.s_begin + blockIdx.x % P.s_count;
     const long long off = P.toff[s];
@@ -518,7 +546,8 @@ __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) 
         unsigned long long dcx = 0ull;
 #pragma unroll
         for (int w = 0; w < KW; w++)
-            dcx |= (unsigned long long)(P.cc_dcap[cc * kNW + w] - P.m.min_w) << (9 * w);
+            dcx |= (unsigned long long)(ltab_on ? P.cc_dslot[cc * kNW + w]      // table row
+                                                : P.cc_dcap[cc * kNW + w] - P.m.min_w) << (9 * w);
         double tnext[KW];
         int ld[KW];                        // routing load: active + pending (A13)
 #pragma unroll
@@ -600,7 +629,14 @@ __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) 
                 W.stm[o] = sN;               // tnext[w] is rewritten by this instant's dispatch
                 if (sN == W.mfin[o]) {
                     const int b = sN & Wm;
-                    unsigned cur = (unsigned)heads[(size_t)w * Wh + b];
+                    unsigned cur;
+                    if (hca) {
+                        hca_wait();
+                        const unsigned wd = hcs[w * kThreads];
+                        cur = sizeof(IDX) == 2 ? ((b & 1) ? (wd >> 16) : (wd & 0xffffu)) : wd;
+                    } else {
+                        cur = (unsigned)heads[(size_t)w * Wh + b];
+                    }
                     int left = 0;
                     for (;;) {
                         const int kk = (int)(cur & ~kMulti);
@@ -704,6 +740,11 @@ __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) 
                             hw[b] = (IDX)kk;
                             *wp = old | bit;
                         }
+                        if (hca && fin <= mf) {          // it heads the earliest bucket now
+                            const unsigned hv = (old & bit) ? ((unsigned)kk | kMulti) : (unsigned)kk;
+                            hca_wait();
+                            hcs[best * kThreads] = (sizeof(IDX) == 2 && (b & 1)) ? (hv << 16) : hv;
+                        }
                         const int n = na + 1;
                         W.nact[o] = n;
                         if (CTX) { W.ctx[o] += itk[hc.id]; W.sj[o] += sj; }
@@ -715,7 +756,7 @@ __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) 
                             if (gr) cc += (long long)n * (sj + 1) - W.sj[o];
                             xv = xv + P.m.dec_per_ctx * (double)cc;
                         }
-                        const double L2 = xv / sdt[cix];
+                        const double L2 = ltab_on ? lts[cix * max_db + n - 1] : xv / sdt[cix];
                         const double dL2 = (CTX && gr) ? (P.m.dec_per_ctx * (double)n) / sdt[cix] : 0.0;
                         W.tseg[o] = tj; W.st0[o] = sj; W.Ls[o] = L2;
                         if (CTX) W.dL[o] = dL2;
@@ -723,7 +764,7 @@ __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) 
                         W.mfin[o] = mf;
                         W.nxs[o] = mf;
                         set_tnext(best, seg_bnd(tj, L2, dL2, mf - sj, gr));
-                        pf_head(hw + (mf & Wm));
+                        if (!hca) pf_head(hw + (mf & Wm));
                         continue;
                     }
                 }
@@ -758,6 +799,9 @@ __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) 
                 if (!ab && qn == 0) continue;
                 const bool was_idle = !ab;
                 bool joined = false;
+                bool hset = false;
+                unsigned hv = 0u;
+                int hb = 0;
                 const int step = W.stm[o];
                 int mf = W.mfin[o];
                 int h = W.qh[o];
@@ -786,6 +830,11 @@ __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) 
                         hw[b] = (IDX)kk;
                         *wp = old | bit;
                     }
+                    if (fin <= mf) {                     // head of the earliest bucket
+                        hv = (old & bit) ? ((unsigned)kk | kMulti) : (unsigned)kk;
+                        hb = b;
+                        hset = true;
+                    }
                     n++;
                     if (CTX) { W.ctx[o] += itk[hots[kk].id]; W.sj[o] += step; }
                     mf = fin < mf ? fin : mf;
@@ -808,7 +857,7 @@ __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) 
                             if (gr) cc += (long long)n * (step + 1) - W.sj[o];
                             xv = xv + P.m.dec_per_ctx * (double)cc;
                         }
-                        L = xv / sdt[cix];
+                        L = ltab_on ? lts[cix * max_db + n - 1] : xv / sdt[cix];
                         W.tseg[o] = ts0; W.st0[o] = s0; W.Ls[o] = L;
                         if (CTX) {
                             dL = gr ? (P.m.dec_per_ctx * (double)n) / sdt[cix] : 0.0;
@@ -817,7 +866,16 @@ __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) 
                     }
                     W.mfin[o] = mf;
                     W.nxs[o] = mf;
-                    pf_head(hw + (mf & Wm));
+                    if (hca) {
+                        if (hset) {
+                            hca_wait();
+                            hcs[w * kThreads] = (sizeof(IDX) == 2 && (hb & 1)) ? (hv << 16) : hv;
+                        } else if ((touched >> (w + 16)) & 1u) {   // after a leave: copy it in
+                            hca_issue(hcs + w * kThreads, hw + (mf & Wm));
+                        }
+                    } else {
+                        pf_head(hw + (mf & Wm));
+                    }
                     set_tnext(w, seg_bnd(ts0, L, dL, mf - s0, gr));
                 } else {
                     W.mfin[o] = 0x7fffffff;
