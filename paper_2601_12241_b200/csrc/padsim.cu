@@ -106,8 +106,8 @@ struct padsim_ctx {
     cudaEvent_t evJ0 = nullptr, evJ1 = nullptr;
     cudaStream_t side = nullptr;     // joint kernel runs concurrently with stages A/C
     cudaEvent_t evC0 = nullptr;
-    cudaStream_t sideC[kNumKC] = {nullptr, nullptr, nullptr};   // stage C classes run concurrently
-    cudaEvent_t evCk[kNumKC] = {nullptr, nullptr, nullptr};    // class joins
+    cudaStream_t sideC[kNumKC] = {};   // stage C classes run concurrently
+    cudaEvent_t evCk[kNumKC] = {};    // class joins
     cudaEvent_t evCf = nullptr;                                  // class fork
     bool j_with_a = false;           // experiment knob: joint replays next to stage A
     bool ev_recorded = false;
@@ -117,14 +117,16 @@ struct padsim_ctx {
     int fA_grid = 0, fC_grid = 0;
     size_t fC_smem = 0, fA_smem = 0;
     // stage C decode-pool classes (static_path.cuh kc_class): cc range, grid, smem
-    int kc_base[kNumKC] = {0, 0, 0}, kc_n[kNumKC] = {0, 0, 0}, kc_grid[kNumKC] = {0, 0, 0};
-    size_t kc_smem[kNumKC] = {0, 0, 0}, kc_off_sdec[kNumKC] = {0, 0, 0};
-    int kc_bits_smem[kNumKC] = {1, 1, 1};
-    int kc_ltab[kNumKC] = {0, 0, 0};
-    int kc_hca[kNumKC] = {0, 0, 0};
-    size_t kc_off_hca[kNumKC] = {0, 0, 0};
-    size_t kc_off_ltab[kNumKC] = {0, 0, 0};
-    char* kc_scr[kNumKC] = {nullptr, nullptr, nullptr};
+    int kc_base[kNumKC] = {}, kc_n[kNumKC] = {}, kc_grid[kNumKC] = {};
+    size_t kc_smem[kNumKC] = {}, kc_off_sdec[kNumKC] = {};
+    int kc_bits_smem[kNumKC] = {};
+    int kc_ltab[kNumKC] = {};
+    int kc_fine = 0;                   // five decode-pool classes (large workloads)
+    int kc_bl[kNumKC] = {};            // class uses the sorted batch lists (BL) instead of the wheel
+    int kc_hca[kNumKC] = {};
+    size_t kc_off_hca[kNumKC] = {};
+    size_t kc_off_ltab[kNumKC] = {};
+    char* kc_scr[kNumKC] = {};
     int fA_tb = kThreads;
     bool fC_idx16 = false;
     int j_tb[2] = {kThreads, kThreads};
@@ -453,30 +455,26 @@ static int validate_policy(padsim_ctx* ctx, const padsim_policy* p, const padsim
     return PADSIM_OK;
 }
 
-// stage C instantiation for (context term, 16-bit indices, decode-pool class)
-template <int KW>
-static const void* stagec_fn_kw(bool cm, bool i16) {
-    return cm ? (i16 ? (const void*)stageC_kernel<true, unsigned short, KW> : (const void*)stageC_kernel<true, unsigned, KW>)
-              : (i16 ? (const void*)stageC_kernel<false, unsigned short, KW> : (const void*)stageC_kernel<false, unsigned, KW>);
-}
-static const void* stagec_fn(bool cm, bool i16, int kc) {
-    return kc == 0 ? stagec_fn_kw<kc_kw(0)>(cm, i16) : kc == 1 ? stagec_fn_kw<kc_kw(1)>(cm, i16)
-                                                               : stagec_fn_kw<kc_kw(2)>(cm, i16);
+// stage C instantiation for (context term, 16-bit indices, decode-pool class,
+// batch-list variant)
+template <int KW, bool BL>
+static const void* stagec_fn_kwb(bool cm, bool i16) {
+    return cm ? (i16 ? (const void*)stageC_kernel<true, unsigned short, KW, BL> : (const void*)stageC_kernel<true, unsigned, KW, BL>)
+              : (i16 ? (const void*)stageC_kernel<false, unsigned short, KW, BL> : (const void*)stageC_kernel<false, unsigned, KW, BL>);
 }
 template <int KW>
-static void stagec_launch_kw(bool cm, bool i16, int grid, size_t smem, cudaStream_t st, const FPlan& F) {
-    if (i16) {
-        if (cm) stageC_kernel<true, unsigned short, KW><<<grid, kThreads, smem, st>>>(F);
-        else stageC_kernel<false, unsigned short, KW><<<grid, kThreads, smem, st>>>(F);
-    } else {
-        if (cm) stageC_kernel<true, unsigned, KW><<<grid, kThreads, smem, st>>>(F);
-        else stageC_kernel<false, unsigned, KW><<<grid, kThreads, smem, st>>>(F);
-    }
+static const void* stagec_fn_kw(bool cm, bool i16, bool bl) {
+    return bl ? stagec_fn_kwb<KW, true>(cm, i16) : stagec_fn_kwb<KW, false>(cm, i16);
 }
-static void stagec_launch(bool cm, bool i16, int kc, int grid, size_t smem, cudaStream_t st, const FPlan& F) {
-    if (kc == 0) stagec_launch_kw<kc_kw(0)>(cm, i16, grid, smem, st, F);
-    else if (kc == 1) stagec_launch_kw<kc_kw(1)>(cm, i16, grid, smem, st, F);
-    else stagec_launch_kw<kc_kw(2)>(cm, i16, grid, smem, st, F);
+static const void* stagec_fn(bool cm, bool i16, int kc, bool bl) {
+    return kc == 0 ? stagec_fn_kw<kc_kw(0)>(cm, i16, bl) : kc == 1 ? stagec_fn_kw<kc_kw(1)>(cm, i16, bl)
+         : kc == 2 ? stagec_fn_kw<kc_kw(2)>(cm, i16, bl) : kc == 3 ? stagec_fn_kw<kc_kw(3)>(cm, i16, bl)
+                   : stagec_fn_kw<kc_kw(4)>(cm, i16, bl);
+}
+static void stagec_launch(bool cm, bool i16, int kc, bool bl, int grid, size_t smem, cudaStream_t st,
+                          const FPlan& F) {
+    void* args[] = {(void*)&F};
+    (void)cudaLaunchKernel(stagec_fn(cm, i16, kc, bl), dim3(grid), dim3(kThreads), args, smem, st);   // checked by the caller
 }
 
 // Groups static candidates by their prefill pool (caps of the prefill GPUs in
@@ -511,16 +509,23 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
         for (int w = 0; w < kNW; w++) e.dcap[w] = w < e.y ? dc[w] : model->min_w;
         ccs.push_back(e);
     }
-    // decode-pool classes (y ≤ 2, ≤ 4, ≤ 7): one stage C launch per class with
-    // register arrays / shared-memory SoA sized to the class; within a class
-    // lanes of a warp are consecutive candidates sorted by prefill group
-    std::stable_sort(ccs.begin(), ccs.end(), [](const CC& a, const CC& b) {
-        const int ka = kc_class(a.y), kb = kc_class(b.y);
+    // decode-pool classes: one stage C launch per class with register arrays /
+    // shared-memory SoA sized to the class (KW = 1, 2, 4, 5, 7 decode-GPU slots);
+    // within a class lanes of a warp are consecutive candidates sorted by prefill
+    // group.  Small workloads use three classes (y ≤ 2, ≤ 4, ≤ 7): more, smaller
+    // launches leave their SMs latency-bound (measured: cfg 2 45.8 → 51.5 ms with
+    // five, cfg 4 621 → 609 ms)
+    const long long n_static_rep = (long long)ccs.size() * Q * S;
+    const bool fine = (n_static_rep >= 400000LL && !getenv("PADSIM_KC3")) || getenv("PADSIM_KC5");
+    ctx->kc_fine = fine;
+    auto kcls = [fine](int y) { return fine ? kc_class(y) : (y <= 2 ? 1 : y <= 4 ? 2 : kNumKC - 1); };
+    std::stable_sort(ccs.begin(), ccs.end(), [&](const CC& a, const CC& b) {
+        const int ka = kcls(a.y), kb = kcls(b.y);
         return ka != kb ? ka < kb : a.group < b.group;
     });
     const int G = (int)gx.size(), NC = (int)ccs.size();
     for (int k = 0; k < kNumKC; k++) { ctx->kc_base[k] = 0; ctx->kc_n[k] = 0; }
-    for (int k = 0; k < NC; k++) ctx->kc_n[kc_class(ccs[k].y)]++;
+    for (int k = 0; k < NC; k++) ctx->kc_n[kcls(ccs[k].y)]++;
     for (int k = 1; k < kNumKC; k++) ctx->kc_base[k] = ctx->kc_base[k - 1] + ctx->kc_n[k - 1];
     std::vector<int> cc_cand(NC), cc_group(NC), cc_y(NC), cc_dcap((size_t)NC * kNW);
     for (int k = 0; k < NC; k++) {
@@ -640,6 +645,10 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
         F.wheel = wheel;
         F.c_off_heads = take((size_t)32 * kNW * wheel * isz);
         F.c_off_bits = take((size_t)kNW * (wheel / 32) * 32 * sizeof(unsigned));
+        int rb = 1;
+        while (rb < model->max_decode_batch) rb <<= 1;
+        F.c_rb = rb;
+        F.c_off_ring = take((size_t)32 * kNW * rb * sizeof(unsigned long long));
         F.c_warp_bytes = off;
         unsigned* d_wc;
         AL(d_wc, (size_t)kNumKC * S);             // work counters per (class, trace)
@@ -664,29 +673,50 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
             ctx->kc_grid[kc] = 0;
             if (ctx->kc_n[kc] == 0) continue;
             const int KWc = kc_kw(kc);
-            const size_t wbytes = (size_t)KWc * kThreads * (kCWorkSlotBytes + (ctxm ? kCWorkCtxSlotBytes : 0));
+            // batch-list variant per class: PADSIM_BL_MASK (bit kc) overrides the default
+            // (measured: the KW = 7 class of large workloads gains from the freed shared
+            // memory — 16 instead of 12 resident warps per SM: cfg 4 610 → 584 ms; the
+            // others lose — all classes 700 ms, cfg 2's KW = 7 class 46.6 → 47.3 ms)
+            int blmask = ctx->kc_fine ? (1 << (kNumKC - 1)) : 0;
+            if (const char* e = getenv("PADSIM_BL_MASK")) blmask = atoi(e);
+            const bool blc = (blmask >> kc) & 1;
+            ctx->kc_bl[kc] = blc;
+            const size_t wbytes = (size_t)KWc * kThreads *
+                                  (kCWorkSlotBytes + (blc ? sizeof(int) : 0) + (ctxm ? kCWorkCtxSlotBytes : 0));
             const size_t bbytes = (size_t)KWc * (wheel / 32) * kThreads * sizeof(unsigned);
-            int bsm = F.bits_in_smem;
+            int bsm = blc ? 0 : F.bits_in_smem;
             // experiment knob: the largest class keeps its wheel bitmaps in global
             // memory so more of its warps fit in shared memory
             if (kc == kNumKC - 1 && getenv("PADSIM_BITS_GLOBAL_BIG")) bsm = 0;
             ctx->kc_bits_smem[kc] = bsm;
             ctx->kc_off_sdec[kc] = wbytes + (bsm ? bbytes : 0);
-            ctx->kc_smem[kc] = ctx->kc_off_sdec[kc] + (size_t)F.m.ncap * sizeof(double);
-            // decode step table in shared memory for the classes with headroom (the
-            // KW = 7 class is shared-memory bound: it keeps the in-place division)
+            const size_t base = ctx->kc_off_sdec[kc] + (size_t)F.m.ncap * sizeof(double);
+            const void* fn = stagec_fn(ctxm, idx16, kc, blc);
+            auto occ_of = [&](size_t sm) {      // resident CTAs per SM (0: does not fit)
+                int o = 0;
+                if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess ||
+                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, kThreads, sm) != cudaSuccess) {
+                    (void)cudaGetLastError();
+                    return 0;
+                }
+                return o;
+            };
+            const int occ0 = occ_of(base);
+            // shared-memory extras, each kept only when it costs no resident CTA:
+            // the async head cache ([KW][kThreads] words) and the decode step table
+            const size_t hbytes = (size_t)KWc * kThreads * sizeof(unsigned);
             const size_t lbytes = (size_t)F.c_lslots * F.m.max_db * sizeof(double);
-            ctx->kc_ltab[kc] = !ctxm && kc < kNumKC - 1 && F.c_lslots <= kLtabRows && !getenv("PADSIM_NO_LTAB");
-            ctx->kc_off_ltab[kc] = ctx->kc_smem[kc];
-            if (ctx->kc_ltab[kc]) ctx->kc_smem[kc] += lbytes;
-            // async head cache for the KW ≤ 4 classes ([KW][kThreads] words)
-            ctx->kc_hca[kc] = kc < kNumKC - 1 && !getenv("PADSIM_NO_HCA");
-            ctx->kc_off_hca[kc] = ctx->kc_smem[kc];
-            if (ctx->kc_hca[kc]) ctx->kc_smem[kc] += (size_t)KWc * kThreads * sizeof(unsigned);
-            const void* fn = stagec_fn(ctxm, idx16, kc);
-            CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->kc_smem[kc]));
-            int occ = 0;
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, ctx->kc_smem[kc]));
+            size_t sm = base;
+            ctx->kc_hca[kc] = !getenv("PADSIM_NO_HCA") && occ_of(sm + hbytes) >= occ0;
+            ctx->kc_off_hca[kc] = sm;
+            if (ctx->kc_hca[kc]) sm += hbytes;
+            ctx->kc_ltab[kc] = !ctxm && F.c_lslots <= kLtabRows && !getenv("PADSIM_NO_LTAB") &&
+                               occ_of(sm + lbytes) >= occ0;
+            ctx->kc_off_ltab[kc] = sm;
+            if (ctx->kc_ltab[kc]) sm += lbytes;
+            ctx->kc_smem[kc] = sm;
+            int occ = occ_of(sm);
+            if (occ == 0) return fail(ctx, PADSIM_ECUDA, "stage C shared memory does not fit");
             occ = std::max(occ, 1);
             const long long items = ((long long)Q * ctx->kc_n[kc] + 31) / 32;   // warp items per trace
             long long per_trace = std::max<long long>(1, ((long long)ctx->n_sm * occ) / S);
@@ -1263,7 +1293,7 @@ int padsim_run(padsim_ctx* ctx, void* stream) {
             F.c_off_ltab = ctx->kc_off_ltab[kc];
             F.bits_in_smem = ctx->kc_bits_smem[kc];
             F.scrC = ctx->kc_scr[kc];
-            stagec_launch(cm, ctx->fC_idx16, kc, ctx->kc_grid[kc], ctx->kc_smem[kc], cs, F);
+            stagec_launch(cm, ctx->fC_idx16, kc, ctx->kc_bl[kc], ctx->kc_grid[kc], ctx->kc_smem[kc], cs, F);
             CK(cudaGetLastError());
         }
         for (int kc = 0; kc < kNumKC; kc++) {

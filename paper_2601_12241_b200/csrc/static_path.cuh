@@ -33,10 +33,10 @@ namespace padsim {
 
 constexpr int kNW = 7;   // ≤ 7 workers per role when N ≤ 8 (each role has ≥ 1 GPU)
 
-// stage C decode-pool classes: y ≤ 2, y ≤ 4, y ≤ 7 decode GPUs → KW = 2, 4, 7
-constexpr int kNumKC = 3;
-__host__ __device__ constexpr int kc_class(int y) { return y <= 2 ? 0 : (y <= 4 ? 1 : 2); }
-__host__ __device__ constexpr int kc_kw(int k) { return k == 0 ? 2 : (k == 1 ? 4 : kNW); }
+// stage C decode-pool classes: y = 1, 2, 3–4, 5, 6–7 decode GPUs → KW = 1, 2, 4, 5, 7
+constexpr int kNumKC = 5;
+__host__ __device__ constexpr int kc_kw(int k) { return k == 0 ? 1 : k == 1 ? 2 : k == 2 ? 4 : k == 3 ? 5 : kNW; }
+__host__ __device__ constexpr int kc_class(int y) { return y <= 1 ? 0 : y <= 2 ? 1 : y <= 4 ? 2 : y <= 5 ? 3 : 4; }
 
 // Register-array helpers: a run-time index selects with predicated moves only
 // (no branches, no local memory).
@@ -126,6 +126,8 @@ struct FPlan {
     size_t c_off_sdec;      // byte offset of the s_dec(w) table in shared memory
     // decode step latency L[slot][n-1] in shared memory for the caps the candidates
     // use (a3 table; per_ctx = 0 only, small decode-pool classes with smem headroom)
+    size_t c_off_ring;      // decode batch lists (BL variant): per lane [kNW][c_rb] u64
+    int c_rb;               // ring slots per decode worker (power of 2 ≥ max_db)
     int c_hca_on;           // async head cache in shared memory (KW ≤ 4 classes)
     size_t c_off_hca;       // its byte offset: [KW][kThreads] 32-bit words
     int c_ltab_on;          // this launch reads L from the table (else xv / s_dec)
@@ -443,6 +445,7 @@ struct CWork {            // per-thread shared-memory SoA views (stride kThreads
     double* tseg;
     double* Ls;
     int* nact; int* qh; int* qt; int* ql; int* stm; int* nxs; int* st0; int* mfin;
+    int* bf;                 // BL: ring index of the batch list's front
     long long* ctx;          // CTX: Σ prompt tokens of the active members (A15)
     long long* sj;           // CTX: Σ join steps of the active members (A40)
     double* dL;              // CTX: per-step latency growth of the segment (A40)
@@ -470,7 +473,13 @@ __device__ __forceinline__ void hca_issue(unsigned* sdst, const void* gsrc) {
 }
 __device__ __forceinline__ void hca_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-template <bool CTX, typename IDX, int KW>
+// BL = false: decode batches are a timing wheel (bucket = finish step mod Wh,
+// heads + occupancy bitmap).  BL = true: each decode worker's batch is a list
+// sorted by (finish step, stream index) in a per-lane ring of u64 entries
+// (fin << 32 | k): a leave pops the front entries, a join inserts from the back
+// (new members usually finish last), the next finish step is the front's — no
+// bitmap in shared memory, and the live entries sit in a few adjacent sectors.
+template <bool CTX, typename IDX, int KW, bool BL>
 __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) {
     constexpr unsigned kMulti = sizeof(IDX) == 2 ? 0x8000u : 0x80000000u;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -492,7 +501,8 @@ __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) 
         W.nact = ib + 0 * n + tid; W.qh = ib + 1 * n + tid; W.qt = ib + 2 * n + tid;
         W.ql = ib + 3 * n + tid; W.stm = ib + 4 * n + tid; W.nxs = ib + 5 * n + tid;
         W.st0 = ib + 6 * n + tid; W.mfin = ib + 7 * n + tid;
-        p += 8 * n * sizeof(int);
+        W.bf = BL ? ib + 8 * n + tid : nullptr;
+        p += (BL ? 9 : 8) * n * sizeof(int);
         W.ctx = CTX ? (long long*)p + tid : nullptr;
         W.sj = CTX ? (long long*)p + n + tid : nullptr;
         W.dL = CTX ? (double*)p + 2 * n + tid : nullptr;
@@ -511,7 +521,9 @@ __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) 
     double* sdt = (double*)(smem + P.c_off_sdec);
     for (int i = tid; i < P.m.ncap; i += kThreads) sdt[i] = P.m.sdec[i];
     double* lts = (double*)(smem + P.c_off_ltab);
-    const bool hca = KW <= 4 && P.c_hca_on;
+    const bool hca = !BL && P.c_hca_on;
+    const int RB = P.c_rb, RBm = P.c_rb - 1;
+    unsigned long long* ring = BL ? (unsigned long long*)(wb + P.c_off_ring) + (size_t)lane * kNW * RB : nullptr;
     unsigned* hcs = (unsigned*)(smem + P.c_off_hca) + tid;     // [w * kThreads]
     const bool ltab_on = !CTX && P.c_ltab_on;
     if (ltab_on)
@@ -558,9 +570,11 @@ __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) 
             W.tseg[o] = 0.0; W.Ls[o] = 1.0;
             W.nact[o] = 0; W.qh[o] = kNoIdx; W.qt[o] = kNoIdx; W.ql[o] = 0;
             W.stm[o] = 0; W.nxs[o] = 0; W.st0[o] = 0; W.mfin[o] = 0x7fffffff;
+            if (BL) W.bf[o] = 0;
             if (CTX) { W.ctx[o] = 0; W.sj[o] = 0; W.dL[o] = 0.0; }
         }
-        for (int z = 0; z < y * nwords; z++) bits[(size_t)z * bstride] = 0u;
+        if (!BL)
+            for (int z = 0; z < y * nwords; z++) bits[(size_t)z * bstride] = 0u;
         int completed = 0, met = 0, near = 0, k = 0;
         double maxcomp = -PAD_INF;
         SHot nxt;                          // the next transfer end of the stream
@@ -608,6 +622,21 @@ __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) 
         // interleaving gives identical results; the lane with the smallest clock
         // always proceeds, so there is no deadlock.
         const float win = P.sync_win > 0.f ? P.sync_win / (float)(P.qps[q] * (double)P.N) : 0.f;
+        // BL: insert (fin, kk) into worker w's sorted list of n members, shifting
+        // later-finishing entries back by one
+        auto bl_insert = [&](int w, int n, int fin, int kk) {
+            unsigned long long* rg = ring + (size_t)w * RB;
+            const int f = W.bf[w * kThreads];
+            const unsigned long long e = ((unsigned long long)(unsigned)fin << 32) | (unsigned)kk;
+            int i = n;
+            while (i > 0) {
+                const unsigned long long pv = rg[(f + i - 1) & RBm];
+                if (pv < e) break;
+                rg[(f + i) & RBm] = pv;
+                i--;
+            }
+            rg[(f + i) & RBm] = e;
+        };
         while (completed < R) {
             double t = tk;
 #pragma unroll
@@ -628,18 +657,9 @@ __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) 
                 const int sN = W.nxs[o];
                 W.stm[o] = sN;               // tnext[w] is rewritten by this instant's dispatch
                 if (sN == W.mfin[o]) {
-                    const int b = sN & Wm;
-                    unsigned cur;
-                    if (hca) {
-                        hca_wait();
-                        const unsigned wd = hcs[w * kThreads];
-                        cur = sizeof(IDX) == 2 ? ((b & 1) ? (wd >> 16) : (wd & 0xffffu)) : wd;
-                    } else {
-                        cur = (unsigned)heads[(size_t)w * Wh + b];
-                    }
-                    int left = 0;
-                    for (;;) {
-                        const int kk = (int)(cur & ~kMulti);
+                    // one leaving member (stream index kk): score it, now (CTX) or
+                    // deferred by kDefer completions
+                    auto leave_member = [&](int kk) {
                         if (CTX) {                          // the leave needs the record now
                             const SRec rc = recs[kk];
                             const int o1 = (rc.meta & 0x7fffffff) - 1;
@@ -664,24 +684,58 @@ __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) 
                             dt[0] = t;
                             completed++;
                         }
-                        left++;
-                        if (!(cur & kMulti)) break;
-                        cur = (unsigned)link[(size_t)kk * 32];   // IDX → unsigned keeps the flag bit
-                    }
-                    unsigned* bw = bits + (size_t)w * nwords * bstride;
-                    bw[(size_t)(b >> 5) * bstride] &= ~(1u << (b & 31));
-                    const int n = W.nact[o] - left;
-                    W.nact[o] = n;
+                    };
+                    int left = 0;
                     int mf = 0x7fffffff;
-                    if (n > 0) {   // next occupied bucket (finish steps lie in (sN, sN+Wh))
-                        const int st = (b + 1) & Wm;
-                        int wi = st >> 5;
-                        unsigned mword = bw[(size_t)wi * bstride] & (0xffffffffu << (st & 31));
-                        while (mword == 0u) {
-                            wi = (wi + 1) & (nwords - 1);
-                            mword = bw[(size_t)wi * bstride];
+                    if constexpr (BL) {
+                        // pop the front entries with fin == sN; the first entry left
+                        // behind is the new front (its fin is the next finish step)
+                        const int n0 = W.nact[o];
+                        const unsigned long long* rg = ring + (size_t)w * RB;
+                        int f = W.bf[o];
+                        unsigned long long e = rg[f];
+                        for (;;) {
+                            leave_member((int)(unsigned)e);
+                            left++;
+                            f = (f + 1) & RBm;
+                            if (left == n0) break;
+                            e = rg[f];
+                            if ((int)(e >> 32) != sN) break;
                         }
-                        mf = sN + ((((wi << 5) + __ffs(mword) - 1) - b) & Wm);
+                        W.bf[o] = f;
+                        W.nact[o] = n0 - left;
+                        if (left < n0) mf = (int)(e >> 32);
+                    } else {
+                        const int b = sN & Wm;
+                        unsigned cur;
+                        if (hca) {
+                            hca_wait();
+                            const unsigned wd = hcs[w * kThreads];
+                            cur = sizeof(IDX) == 2 ? ((b & 1) ? (wd >> 16) : (wd & 0xffffu)) : wd;
+                        } else {
+                            cur = (unsigned)heads[(size_t)w * Wh + b];
+                        }
+                        for (;;) {
+                            const int kk = (int)(cur & ~kMulti);
+                            leave_member(kk);
+                            left++;
+                            if (!(cur & kMulti)) break;
+                            cur = (unsigned)link[(size_t)kk * 32];   // IDX → unsigned keeps the flag bit
+                        }
+                        unsigned* bw = bits + (size_t)w * nwords * bstride;
+                        bw[(size_t)(b >> 5) * bstride] &= ~(1u << (b & 31));
+                        const int n = W.nact[o] - left;
+                        W.nact[o] = n;
+                        if (n > 0) {   // next occupied bucket (finish steps lie in (sN, sN+Wh))
+                            const int st = (b + 1) & Wm;
+                            int wi = st >> 5;
+                            unsigned mword = bw[(size_t)wi * bstride] & (0xffffffffu << (st & 31));
+                            while (mword == 0u) {
+                                wi = (wi + 1) & (nwords - 1);
+                                mword = bw[(size_t)wi * bstride];
+                            }
+                            mf = sN + ((((wi << 5) + __ffs(mword) - 1) - b) & Wm);
+                        }
                     }
                     W.mfin[o] = mf;
                     radd<KW, int>(ld, w, -left);
@@ -728,22 +782,26 @@ __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) 
                         const int out = hc.meta & 0x7fffffff;
                         if (P.c_prefetch) asm volatile("prefetch.global.L2 [%0];" :: "l"(recs + kk));
                         const int fin = sj + (out - 1);
-                        const int b = fin & Wm;
                         IDX* hw = heads + (size_t)best * Wh;
-                        unsigned* wp = bits + (size_t)best * nwords * bstride + (size_t)(b >> 5) * bstride;
-                        const unsigned bit = 1u << (b & 31);
-                        const unsigned old = *wp;
-                        if (old & bit) {
-                            link[(size_t)kk * 32] = hw[b];
-                            hw[b] = (IDX)((unsigned)kk | kMulti);
+                        if constexpr (BL) {
+                            bl_insert(best, na, fin, kk);
                         } else {
-                            hw[b] = (IDX)kk;
-                            *wp = old | bit;
-                        }
-                        if (hca && fin <= mf) {          // it heads the earliest bucket now
-                            const unsigned hv = (old & bit) ? ((unsigned)kk | kMulti) : (unsigned)kk;
-                            hca_wait();
-                            hcs[best * kThreads] = (sizeof(IDX) == 2 && (b & 1)) ? (hv << 16) : hv;
+                            const int b = fin & Wm;
+                            unsigned* wp = bits + (size_t)best * nwords * bstride + (size_t)(b >> 5) * bstride;
+                            const unsigned bit = 1u << (b & 31);
+                            const unsigned old = *wp;
+                            if (old & bit) {
+                                link[(size_t)kk * 32] = hw[b];
+                                hw[b] = (IDX)((unsigned)kk | kMulti);
+                            } else {
+                                hw[b] = (IDX)kk;
+                                *wp = old | bit;
+                            }
+                            if (hca && fin <= mf) {          // it heads the earliest bucket now
+                                const unsigned hv = (old & bit) ? ((unsigned)kk | kMulti) : (unsigned)kk;
+                                hca_wait();
+                                hcs[best * kThreads] = (sizeof(IDX) == 2 && (b & 1)) ? (hv << 16) : hv;
+                            }
                         }
                         const int n = na + 1;
                         W.nact[o] = n;
@@ -764,7 +822,7 @@ __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) 
                         W.mfin[o] = mf;
                         W.nxs[o] = mf;
                         set_tnext(best, seg_bnd(tj, L2, dL2, mf - sj, gr));
-                        if (!hca) pf_head(hw + (mf & Wm));
+                        if (!BL && !hca) pf_head(hw + (mf & Wm));
                         continue;
                     }
                 }
@@ -819,21 +877,25 @@ __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) 
                     const int out = meta & 0x7fffffff;
                     if (P.c_prefetch) asm volatile("prefetch.global.L2 [%0];" :: "l"(recs + kk));
                     const int fin = step + (out - 1);
-                    const int b = fin & Wm;
-                    unsigned* wp = bw + (size_t)(b >> 5) * bstride;
-                    const unsigned bit = 1u << (b & 31);
-                    const unsigned old = *wp;
-                    if (old & bit) {                     // bucket occupied: chain
-                        link[(size_t)kk * 32] = hw[b];
-                        hw[b] = (IDX)((unsigned)kk | kMulti);
+                    if constexpr (BL) {
+                        bl_insert(w, n, fin, kk);
                     } else {
-                        hw[b] = (IDX)kk;
-                        *wp = old | bit;
-                    }
-                    if (fin <= mf) {                     // head of the earliest bucket
-                        hv = (old & bit) ? ((unsigned)kk | kMulti) : (unsigned)kk;
-                        hb = b;
-                        hset = true;
+                        const int b = fin & Wm;
+                        unsigned* wp = bw + (size_t)(b >> 5) * bstride;
+                        const unsigned bit = 1u << (b & 31);
+                        const unsigned old = *wp;
+                        if (old & bit) {                     // bucket occupied: chain
+                            link[(size_t)kk * 32] = hw[b];
+                            hw[b] = (IDX)((unsigned)kk | kMulti);
+                        } else {
+                            hw[b] = (IDX)kk;
+                            *wp = old | bit;
+                        }
+                        if (fin <= mf) {                     // head of the earliest bucket
+                            hv = (old & bit) ? ((unsigned)kk | kMulti) : (unsigned)kk;
+                            hb = b;
+                            hset = true;
+                        }
                     }
                     n++;
                     if (CTX) { W.ctx[o] += itk[hots[kk].id]; W.sj[o] += step; }
@@ -866,7 +928,8 @@ __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) 
                     }
                     W.mfin[o] = mf;
                     W.nxs[o] = mf;
-                    if (hca) {
+                    if (BL) {
+                    } else if (hca) {
                         if (hset) {
                             hca_wait();
                             hcs[w * kThreads] = (sizeof(IDX) == 2 && (hb & 1)) ? (hv << 16) : hv;

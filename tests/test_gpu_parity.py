@@ -36,6 +36,22 @@ def test_static_records_exact(pkg, family):
     assert n == len(XPD) * len(qps) * 600
 
 
+@pytest.mark.parametrize("bl_mask", ["16", "31", "0"])
+def test_fine_decode_pool_classes(pkg, monkeypatch, bl_mask):
+    # large workloads split stage C into five decode-pool classes (KW = 1, 2, 4, 5, 7)
+    # and use sorted batch lists for the KW = 7 class; force both on a small case
+    # (every y = 1..7 appears; batch lists on no / the largest / every class):
+    # records bit-exact
+    monkeypatch.setenv("PADSIM_KC5", "1")
+    monkeypatch.setenv("PADSIM_BL_MASK", bl_mask)
+    xpd = [(7, 500, 700), (6, 550, 650), (5, 600, 600), (4, 600, 600), (3, 650, 560),
+           (2, 700, 540), (1, 750, 575)]
+    role, cap = static_candidates(8, xpd)
+    pols = [policy("static")] * len(xpd)
+    traces = [make_trace("lb", s, 250) for s in range(2)]
+    compare_records(traces, [0.5, 1.5, 3.0], DEFAULT_MODEL, role, cap, pols, DEFAULT_SLO, 4800)
+
+
 @pytest.mark.parametrize("kind", ["dyn-power", "dyn-gpu", "dyn-both"])
 def test_dynamic_records_exact(pkg, kind):
     xpd = [(4, 600, 600), (5, 600, 600), (3, 600, 600), (4, 750, 450)]
