@@ -122,6 +122,8 @@ struct Plan {
     size_t off_heads, off_bits;        // decode timing wheel (joint8 kernel)
     size_t off_wts, off_wtf;           // TTFT window: stamps + flags (joint kernel)
     size_t off_jw;                     // per-GPU SoA in global scratch (joint kernel, NG = 64)
+    size_t off_ring;                   // decode batch lists (joint kernel, PADSIM_JBL): per lane [NG][ring_slots] u64
+    int ring_slots;                    // power of 2 ≥ max_decode_batch
     int wheel;                         // wheel size: power of 2 ≥ max out_tok, ≥ 32
     size_t warp_bytes;
     int smem_trace;                    // stage the trace in shared memory (TMA bulk)

@@ -25,6 +25,13 @@
 #include "controller.cuh"
 #include "replay.cuh"
 
+// Decode batches of the joint replay: PADSIM_JBL = 1 sorted per-GPU batch lists
+// in a per-lane ring of u64 (fin << 32 | id) entries (as stageC_kernel<BL>), 0 =
+// the timing wheel (bucket heads + occupancy bitmap in global scratch).
+#ifndef PADSIM_JBL
+#define PADSIM_JBL 1
+#endif
+
 namespace padsim {
 
 constexpr int kJG = 8;     // GPU slots of the small-node variant (N ≤ 8)
@@ -178,10 +185,11 @@ struct JWork {
     int* b0;    // P: batch head | D: last materialised step
     int* b1;    // P: batch size | D: next boundary to materialise
     int* st0; int* mfin; int* eff; int* cmd; int* rse; int* ctx;
+    int* bf;    // D: ring index of the batch list's front (PADSIM_JBL)
     unsigned char* fl;
 };
 template <int TB>
-__host__ __device__ constexpr size_t j_work_bytes() { return (size_t)kJG * TB * (4 * sizeof(double) + 13 * sizeof(int) + 1); }
+__host__ __device__ constexpr size_t j_work_bytes() { return (size_t)kJG * TB * (4 * sizeof(double) + 14 * sizeof(int) + 1); }
 
 enum : unsigned char { JF_DRAIN = 1, JF_DIRTY = 2 };
 
@@ -233,6 +241,8 @@ struct JReplay {
     int* tti;
     int* heads;          // [(g*wheel + b)*32]
     unsigned* bits;      // [(g*wheel/32 + k)*32]
+    unsigned long long* ring;   // PADSIM_JBL: per-lane [g][RB] batch lists
+    int RB, RBm;
     double* wts;         // TTFT window stamps [k], per-lane contiguous (FIFO walk)
     unsigned char* wtf;  // TTFT window flags (≤ SLO, < SLO) [k]
     int Wh, Wm, nwords;
@@ -391,31 +401,52 @@ struct JReplay {
         W.b0[o] = s;
         set_tnext(g, PAD_INF);
         if (s != W.mfin[o]) return false;
-        const int b = s & Wm;
-        int id = heads[((size_t)g * Wh + b) * 32];
         int left = 0;
-        while (id != kNoIdx) {
-            const int nx = LNK(id);
+        auto leave = [&](int id) {
             complete(id, t, (t - PE(id)) / (double)(T.out_tok[id] - 1));
             W.ctx[o] -= T.in_tok[id];
             if (gr) W.sj[o] -= s - (T.out_tok[id] - 1);      // its join step (A40)
             left++;
-            id = nx;
-        }
-        unsigned* bw = bits + (size_t)g * nwords * 32;
-        bw[(size_t)(b >> 5) * 32] &= ~(1u << (b & 31));
-        const int n = W.a0[o] - left;
-        W.a0[o] = n;
+        };
         int mf = kIntMax;
-        if (n > 0) {
-            const int st = (b + 1) & Wm;
-            int wi = st >> 5;
-            unsigned mword = bw[(size_t)wi * 32] & (0xffffffffu << (st & 31));
-            while (mword == 0u) {
-                wi = (wi + 1) & (nwords - 1);
-                mword = bw[(size_t)wi * 32];
+        if (PADSIM_JBL) {
+            // pop the front entries with fin == s; the first one left is the new front
+            const int n0 = W.a0[o];
+            const unsigned long long* rg = ring + (size_t)g * RB;
+            int f = W.bf[o];
+            unsigned long long e = rg[f];
+            for (;;) {
+                leave((int)(unsigned)e);
+                f = (f + 1) & RBm;
+                if (left == n0) break;
+                e = rg[f];
+                if ((int)(e >> 32) != s) break;
             }
-            mf = s + ((((wi << 5) + __ffs(mword) - 1) - b) & Wm);
+            W.bf[o] = f;
+            W.a0[o] = n0 - left;
+            if (left < n0) mf = (int)(e >> 32);
+        } else {
+            const int b = s & Wm;
+            int id = heads[((size_t)g * Wh + b) * 32];
+            while (id != kNoIdx) {
+                const int nx = LNK(id);
+                leave(id);
+                id = nx;
+            }
+            unsigned* bw = bits + (size_t)g * nwords * 32;
+            bw[(size_t)(b >> 5) * 32] &= ~(1u << (b & 31));
+            const int n = W.a0[o] - left;
+            W.a0[o] = n;
+            if (n > 0) {
+                const int st = (b + 1) & Wm;
+                int wi = st >> 5;
+                unsigned mword = bw[(size_t)wi * 32] & (0xffffffffu << (st & 31));
+                while (mword == 0u) {
+                    wi = (wi + 1) & (nwords - 1);
+                    mword = bw[(size_t)wi * 32];
+                }
+                mf = s + ((((wi << 5) + __ffs(mword) - 1) - b) & Wm);
+            }
         }
         W.mfin[o] = mf;
         if (!(W.fl[o] & JF_DRAIN)) add_kd(g, -left);
@@ -490,13 +521,28 @@ struct JReplay {
             qn--;
             if (qn > 0) h = LNK(i);
             const int fin = step + (T.out_tok[i] - 1);
-            const int b = fin & Wm;
-            unsigned* wp = bw + (size_t)(b >> 5) * 32;
-            const unsigned bit = 1u << (b & 31);
-            const unsigned old = *wp;
-            LNK(i) = (old & bit) ? hw[(size_t)b * 32] : kNoIdx;
-            hw[(size_t)b * 32] = i;
-            *wp = old | bit;
+            if (PADSIM_JBL) {
+                // insert (fin, i) into the sorted list of n members from the back
+                unsigned long long* rg = ring + (size_t)g * RB;
+                const int f = W.bf[o];
+                const unsigned long long e = ((unsigned long long)(unsigned)fin << 32) | (unsigned)i;
+                int z = n;
+                while (z > 0) {
+                    const unsigned long long pv = rg[(f + z - 1) & RBm];
+                    if (pv < e) break;
+                    rg[(f + z) & RBm] = pv;
+                    z--;
+                }
+                rg[(f + z) & RBm] = e;
+            } else {
+                const int b = fin & Wm;
+                unsigned* wp = bw + (size_t)(b >> 5) * 32;
+                const unsigned bit = 1u << (b & 31);
+                const unsigned old = *wp;
+                LNK(i) = (old & bit) ? hw[(size_t)b * 32] : kNoIdx;
+                hw[(size_t)b * 32] = i;
+                *wp = old | bit;
+            }
             n++;
             W.ctx[o] += T.in_tok[i];
             if (gr) W.sj[o] += step;
@@ -526,7 +572,7 @@ struct JReplay {
             }
             W.mfin[o] = mf;
             W.b1[o] = mf;
-            pf_head(hw + (size_t)(mf & Wm) * 32);
+            if (!PADSIM_JBL) pf_head(hw + (size_t)(mf & Wm) * 32);
             set_tnext(g, bnd(o, mf));
         } else {
             W.mfin[o] = kIntMax;
@@ -570,7 +616,7 @@ struct JReplay {
         dmask ^= ((Mask)1) << g;
         W.fl[o] = 0;
         W.a0[o] = 0; W.ql[o] = 0; W.b0[o] = 0; W.b1[o] = 0; W.st0[o] = 0;
-        W.mfin[o] = kIntMax; W.ctx[o] = 0; W.sj[o] = 0;
+        W.mfin[o] = kIntMax; W.ctx[o] = 0; W.sj[o] = 0; W.bf[o] = 0;
         set_tnext(g, PAD_INF);
         tab.set_p(g, to_p ? 0 : kIntMax);
         tab.set_d(g, to_p ? kIntMax : 0);
@@ -721,10 +767,11 @@ struct JReplay {
             W.a0[o] = 0; W.qh[o] = kNoIdx; W.qt[o] = kNoIdx; W.ql[o] = 0;
             W.b0[o] = 0; W.b1[o] = 0; W.st0[o] = 0; W.mfin[o] = kIntMax;
             W.eff[o] = W.cmd[o] = on ? ccap[g] : P.m.min_w;
-            W.rse[o] = 0; W.ctx[o] = 0; W.fl[o] = 0;
+            W.rse[o] = 0; W.ctx[o] = 0; W.fl[o] = 0; W.bf[o] = 0;
         }
         Wh = P.wheel; Wm = Wh - 1; nwords = Wh >> 5;
-        for (int z = 0; z < N * nwords; z++) bits[(size_t)z * 32] = 0u;
+        if (!PADSIM_JBL)
+            for (int z = 0; z < N * nwords; z++) bits[(size_t)z * 32] = 0u;
         tbusy = 0; mk = 0; mid = 0; twh = twt = kNoIdx; twl = 0;
         mte = PAD_INF;
         completed = 0; met = 0; near = 0;
@@ -849,7 +896,8 @@ __global__ void __launch_bounds__(TB) __maxnreg__(MR) joint_kernel(const __grid_
         W.ql = ib + 3 * n + tid; W.b0 = ib + 4 * n + tid; W.b1 = ib + 5 * n + tid;
         W.st0 = ib + 6 * n + tid; W.mfin = ib + 7 * n + tid; W.eff = ib + 8 * n + tid;
         W.cmd = ib + 9 * n + tid; W.rse = ib + 10 * n + tid; W.ctx = ib + 11 * n + tid;
-        p += 13 * n * sizeof(int);
+        W.bf = ib + 13 * n + tid;
+        p += 14 * n * sizeof(int);
         W.fl = p + tid;
         ws = TB;
     } else {                 // per-GPU SoA in lane-interleaved global scratch
@@ -864,7 +912,8 @@ __global__ void __launch_bounds__(TB) __maxnreg__(MR) joint_kernel(const __grid_
         W.ql = ib + 3 * n + lane; W.b0 = ib + 4 * n + lane; W.b1 = ib + 5 * n + lane;
         W.st0 = ib + 6 * n + lane; W.mfin = ib + 7 * n + lane; W.eff = ib + 8 * n + lane;
         W.cmd = ib + 9 * n + lane; W.rse = ib + 10 * n + lane; W.ctx = ib + 11 * n + lane;
-        p += 13 * n * sizeof(int);
+        W.bf = ib + 13 * n + lane;
+        p += 14 * n * sizeof(int);
         W.fl = (unsigned char*)p + lane;
         ws = 32;
     }
@@ -911,6 +960,9 @@ __global__ void __launch_bounds__(TB) __maxnreg__(MR) joint_kernel(const __grid_
         rp.tti = tti;
         rp.heads = (int*)(wbase + P.off_heads) + lane;
         rp.bits = (unsigned*)(wbase + P.off_bits) + lane;
+        rp.RB = P.ring_slots;
+        rp.RBm = P.ring_slots - 1;
+        rp.ring = (unsigned long long*)(wbase + P.off_ring) + (size_t)lane * NG * P.ring_slots;
         rp.wts = DYN ? (double*)(wbase + P.off_wts) + (size_t)lane * P.Rmax : nullptr;
         rp.wtf = DYN ? (unsigned char*)(wbase + P.off_wtf) + (size_t)lane * P.Rmax : nullptr;
         const ReplayResult res = rp.run(c, q, P.rec_ttft ? r * P.Rmax : -1);
@@ -929,7 +981,7 @@ __global__ void __launch_bounds__(TB) __maxnreg__(MR) joint_kernel(const __grid_
 }
 
 constexpr size_t joint_global_bytes_per_warp(int NG) {   // per-GPU SoA for NG = 64
-    return NG == 8 ? 0 : (size_t)NG * 32 * (4 * sizeof(double) + 13 * sizeof(int) + 1);
+    return NG == 8 ? 0 : (size_t)NG * 32 * (4 * sizeof(double) + 14 * sizeof(int) + 1);
 }
 
 }  // namespace padsim

@@ -1080,8 +1080,14 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
         int wheel = 32;
         while (wheel < maxo) wheel <<= 1;
         P.wheel = wheel;
-        P.off_heads = take((size_t)NG * wheel * 32 * sizeof(int));
-        P.off_bits = take((size_t)NG * (wheel / 32) * 32 * sizeof(unsigned));
+        if (!PADSIM_JBL) {       // timing wheel
+            P.off_heads = take((size_t)NG * wheel * 32 * sizeof(int));
+            P.off_bits = take((size_t)NG * (wheel / 32) * 32 * sizeof(unsigned));
+        }
+        int rslots = 1;
+        while (rslots < model->max_decode_batch) rslots <<= 1;
+        P.ring_slots = rslots;
+        if (PADSIM_JBL) P.off_ring = take((size_t)32 * NG * rslots * sizeof(unsigned long long));
         if (NG == 64) P.off_jw = take(joint_global_bytes_per_warp(64));
         P.warp_bytes = off;
         ctx->j8[dyn] = true;
@@ -1114,6 +1120,7 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
         int occj = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occj, fnj, tbj, jb));
         occj = std::max(occj, 1);
+        if (const char* e = getenv("PADSIM_J_OCC")) occj = std::max(1, std::min(occj, atoi(e)));   // knob
         // replays per warp item: 32, or fewer when the joint workload would leave
         // the SMs with fewer than ~4 latency-bound warps each (measured on cfg 3,
         // 13.4k replays: 32 lanes 464 ms, 16 lanes 387 ms, 8 lanes 452 ms)
