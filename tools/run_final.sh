@@ -1,0 +1,18 @@
+# Round-end evidence on one box: bash tools/run_final.sh <tag>
+tag=$1
+D=gpurun_out/$tag
+mkdir -p $D
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,driver_version --format=csv > $D/gpu.txt
+timeout 1200 python -m pytest tests -m gpu -q 2>&1 | tail -5 > $D/gpu_tests.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $D/smoke.log 2>&1
+for c in cfg4 cfg2 cfg3 cfg1; do
+  timeout 900 python bench.py --config $c > $D/bench_$c.log 2>&1
+done
+timeout 600 python bench.py --impl reference --steps 2 --warmup 3 > $D/bench_ref.log 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $D/launches_cfg4.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 > $D/ncu_bench.log 2>&1
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:stageC -c 5 -o $D/stageC_cfg4 python tools/prof_run.py --config cfg4 --runs 1 > $D/ncu_C.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:stageA -c 1 -o $D/stageA_cfg4 python tools/prof_run.py --config cfg4 --runs 1 > $D/ncu_A.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:joint -c 1 -o $D/joint_cfg4 python tools/prof_run.py --config cfg4 --runs 1 > $D/ncu_J4.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:joint -c 1 -o $D/joint_cfg3 python tools/prof_run.py --config cfg3 --runs 1 > $D/ncu_J3.log 2>&1
+timeout 2400 python bench.py --config cfg5 --steps 1 --warmup 3 --e2e-steps 1 --cpu-seconds 20 > $D/bench_cfg5.log 2>&1
+ls -la $D
