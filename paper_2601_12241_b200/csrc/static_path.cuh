@@ -582,10 +582,12 @@ __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) 
         double tk = nxt.te;
         long long inst = 0;
         auto set_tnext = [&](int wd, double v) { rset<KW>(tnext, wd, v); };
-        int metk[kMaxSloSweep];
-#pragma unroll
-        for (int z = 0; z < kMaxSloSweep; z++) metk[z] = 0;
+        // SLO-sweep met counts (§8(f) row 1): counted in this replay's global slots
+        // (rolled loops; nothing to do when no sweep is set, as in the bench)
         const int nk = P.sw.n;
+        int* metk = P.sw.rep_met + r * kMaxSloSweep;
+#pragma unroll 1
+        for (int z = 0; z < nk; z++) metk[z] = 0;
         int ck0 = -1, cm0 = 0, ck1 = -1, cm1 = 0;   // last two routed (stream index, meta)
         // deferred completions (non-CTX): a kDefer-deep FIFO in registers, shifted
         // with static indices; an entry is scored kDefer completions after its
@@ -598,12 +600,10 @@ __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) 
         auto complete = [&](const SRec& rc, double t, double tpot) {
             const double ts = (rc.meta < 0) ? P.tpot_slo1 : P.tpot_slo0;
             met += ((rc.fl & 1u) && tpot <= ts) ? 1 : 0;
-#pragma unroll
-            for (int z = 0; z < kMaxSloSweep; z++) {
-                if (z < nk) {
-                    const double tz = (rc.meta < 0) ? P.sw.tpot1[z] : P.sw.tpot0[z];
-                    metk[z] += (((rc.fl >> (2 + z)) & 1u) && tpot <= tz) ? 1 : 0;
-                }
+#pragma unroll 1
+            for (int z = 0; z < nk; z++) {
+                const double tz = (rc.meta < 0) ? P.sw.tpot1[z] : P.sw.tpot0[z];
+                if (((rc.fl >> (2 + z)) & 1u) && tpot <= tz) metk[z]++;
             }
             near += ((rc.fl & 2u) || fabs(tpot - ts) <= 1e-9 * ts) ? 1 : 0;
             maxcomp = fmax(maxcomp, t);
@@ -966,9 +966,6 @@ __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) 
             const double cs = (double)P.sw.capsum[c];
             const double acc = R > 0 ? cs * dur : 0.0;
             P.sw.rep_watts[r] = dur > 0 ? acc / dur : cs;
-#pragma unroll
-            for (int z = 0; z < kMaxSloSweep; z++)
-                if (z < nk) P.sw.rep_met[r * kMaxSloSweep + z] = metk[z];
         }
     }
 }
