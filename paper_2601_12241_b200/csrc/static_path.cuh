@@ -647,7 +647,7 @@ __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) 
                 if (tf > __uint_as_float(mn) + win) continue;
             }
             inst++;
-            unsigned bnd = 0, touched = 0;
+            unsigned bnd = 0, touched = 0, eag = 0;
 #pragma unroll
             for (int w = 0; w < KW; w++) if (tnext[w] == t) bnd |= 1u << w;
             // kind 3: materialised step boundaries, worker order
@@ -762,70 +762,6 @@ __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) 
                 const int o = best * kThreads;
                 const int qn = W.ql[o];
                 const int na = W.nact[o];
-                if (PADSIM_EAGER && na > 0 && !((bnd >> best) & 1u) && na < max_db && qn == 0) {
-                    // Eager join: the request joins at the first boundary sj ≥ t of
-                    // the running segment (A14).  When sj precedes the worker's next
-                    // leave, nothing else happens to this worker until sj (routing
-                    // only reads active + pending, unchanged by the join), so the
-                    // dispatch the boundary instant would run is done now: the new
-                    // segment starts at sj (time bnd(sj)) with the joiner admitted.
-                    // A later transfer end at or before bnd(sj) finds sj again as its
-                    // first boundary and joins the same not-yet-started segment.
-                    // Saves the join-only instant; same state as the DES at bnd(sj).
-                    const double ts0 = W.tseg[o], L = W.Ls[o];
-                    const double dL = CTX ? W.dL[o] : 0.0;
-                    const int s0 = W.st0[o];
-                    const int sj = seg_first_ge(ts0, L, dL, s0, W.stm[o], t, gr);
-                    int mf = W.mfin[o];
-                    if (sj < mf) {
-                        const double tj = seg_bnd(ts0, L, dL, sj - s0, gr);
-                        const int out = hc.meta & 0x7fffffff;
-                        if (P.c_prefetch) asm volatile("prefetch.global.L2 [%0];" :: "l"(recs + kk));
-                        const int fin = sj + (out - 1);
-                        IDX* hw = heads + (size_t)best * Wh;
-                        if constexpr (BL) {
-                            bl_insert(best, na, fin, kk);
-                        } else {
-                            const int b = fin & Wm;
-                            unsigned* wp = bits + (size_t)best * nwords * bstride + (size_t)(b >> 5) * bstride;
-                            const unsigned bit = 1u << (b & 31);
-                            const unsigned old = *wp;
-                            if (old & bit) {
-                                link[(size_t)kk * 32] = hw[b];
-                                hw[b] = (IDX)((unsigned)kk | kMulti);
-                            } else {
-                                hw[b] = (IDX)kk;
-                                *wp = old | bit;
-                            }
-                            if (hca && fin <= mf) {          // it heads the earliest bucket now
-                                const unsigned hv = (old & bit) ? ((unsigned)kk | kMulti) : (unsigned)kk;
-                                hca_wait();
-                                hcs[best * kThreads] = (sizeof(IDX) == 2 && (b & 1)) ? (hv << 16) : hv;
-                            }
-                        }
-                        const int n = na + 1;
-                        W.nact[o] = n;
-                        if (CTX) { W.ctx[o] += itk[hc.id]; W.sj[o] += sj; }
-                        mf = fin < mf ? fin : mf;
-                        const int cix = (int)((dcx >> (9 * best)) & 511u);
-                        double xv = P.m.dec_fixed + P.m.dec_per_seq * (double)n;
-                        if (CTX) {
-                            long long cc = W.ctx[o];
-                            if (gr) cc += (long long)n * (sj + 1) - W.sj[o];
-                            xv = xv + P.m.dec_per_ctx * (double)cc;
-                        }
-                        const double L2 = ltab_on ? lts[cix * max_db + n - 1] : xv / sdt[cix];
-                        const double dL2 = (CTX && gr) ? (P.m.dec_per_ctx * (double)n) / sdt[cix] : 0.0;
-                        W.tseg[o] = tj; W.st0[o] = sj; W.Ls[o] = L2;
-                        if (CTX) W.dL[o] = dL2;
-                        W.stm[o] = sj - 1;           // boundaries ≥ sj belong to the new segment
-                        W.mfin[o] = mf;
-                        W.nxs[o] = mf;
-                        set_tnext(best, seg_bnd(tj, L2, dL2, mf - sj, gr));
-                        if (!BL && !hca) pf_head(hw + (mf & Wm));
-                        continue;
-                    }
-                }
                 ck1 = ck0; cm1 = cm0; ck0 = kk; cm0 = hc.meta;
                 if (qn == 0) W.qh[o] = kk; else link[(size_t)W.qt[o] * 32] = (IDX)kk;
                 W.qt[o] = kk;
@@ -836,7 +772,19 @@ __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) 
                     const double dL = CTX ? W.dL[o] : 0.0;
                     const int s0 = W.st0[o];
                     const int sj = seg_first_ge(ts0, L, dL, s0, W.stm[o], t, gr);
-                    if (sj < W.nxs[o]) {
+                    if (PADSIM_EAGER && sj < W.mfin[o]) {
+                        // Eager join: the request joins at the first boundary sj ≥ t
+                        // of the running segment (A14).  When sj precedes the worker's
+                        // next leave, nothing else happens to this worker until sj
+                        // (routing only reads active + pending, unchanged by a join),
+                        // so this instant's dispatch admits it as the boundary instant
+                        // would: the new segment starts at sj (time bnd(sj)).  A later
+                        // transfer end at or before bnd(sj) finds sj again as its first
+                        // boundary and joins the same not-yet-started segment.  Saves
+                        // the join-only instant; same state as the DES at bnd(sj).
+                        W.nxs[o] = sj;
+                        eag |= 1u << best;
+                    } else if (sj < W.nxs[o]) {
                         W.nxs[o] = sj;
                         set_tnext(best, seg_bnd(ts0, L, dL, sj - s0, gr));
                     }
@@ -847,12 +795,14 @@ __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) 
                 const int w = __ffs(m) - 1;
                 const int o = w * kThreads;
                 bool ab = (bnd >> w) & 1u;
+                const bool eg = (eag >> w) & 1u;         // eager join at boundary W.nxs
                 int n = W.nact[o];
-                if (n > 0 && !ab) {
+                if (n > 0 && !ab && !eg) {
                     if (rget<KW>(tnext, w) != t) continue;   // mid-step
                     W.stm[o] = W.nxs[o];                 // join boundary exactly at t
                     ab = true;
                 }
+                ab = ab || eg;
                 int qn = W.ql[o];
                 if (!ab && qn == 0) continue;
                 const bool was_idle = !ab;
@@ -860,7 +810,7 @@ __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) 
                 bool hset = false;
                 unsigned hv = 0u;
                 int hb = 0;
-                const int step = W.stm[o];
+                const int step = eg ? W.nxs[o] : W.stm[o];
                 int mf = W.mfin[o];
                 int h = W.qh[o];
                 IDX* hw = heads + (size_t)w * Wh;
@@ -910,7 +860,10 @@ __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) 
                     double dL = CTX ? W.dL[o] : 0.0;
                     int s0 = W.st0[o];
                     if (was_idle || joined || ((touched >> (w + 16)) & 1u)) {
-                        ts0 = t;
+                        // the new segment starts at this instant, or for an eager join
+                        // at boundary `step` of the running segment (time bnd(step))
+                        ts0 = eg ? seg_bnd(ts0, L, dL, step - s0, gr) : t;
+                        if (eg) W.stm[o] = step - 1;         // boundaries ≥ step: new segment
                         s0 = step;
                         const int cix = (int)((dcx >> (9 * w)) & 511u);
                         double xv = P.m.dec_fixed + P.m.dec_per_seq * (double)n;
