@@ -42,6 +42,7 @@ __device__ __forceinline__ int ctl_step(const padsim_policy& pol, int min_w, int
     const int ceil_to = to == 0 ? max_w : pol.decode_ceiling_w;
     int n_don = 0, n_rec = 0;
     bool rec_ceil = true, don_floor = true;
+#pragma unroll 1
     for (int g = 0; g < N; g++) {
         if (v.draining(g)) continue;
         const int r = v.role(g);
@@ -56,6 +57,7 @@ __device__ __forceinline__ int ctl_step(const padsim_policy& pol, int min_w, int
         // MovePower: donors −min(step, cap−floor), F = Σ, recipients
         // +min(⌊F/|rec|⌋, ceiling−cap), leftover unallocated.
         long long F = 0;
+#pragma unroll 1
         for (int g = 0; g < N; g++) {
             const int c = v.target(g);
             new_cap[g] = c;
@@ -67,6 +69,7 @@ __device__ __forceinline__ int ctl_step(const padsim_policy& pol, int min_w, int
             F += r;
         }
         const long long share = n_rec > 0 ? F / n_rec : 0;
+#pragma unroll 1
         for (int g = 0; g < N; g++) {
             if (v.draining(g) || v.role(g) != to) continue;
             const int c = v.target(g);
@@ -81,6 +84,7 @@ __device__ __forceinline__ int ctl_step(const padsim_policy& pol, int min_w, int
         // MoveGPU: least outstanding work, lowest id; then uniform caps
         int best = -1;
         long long bl = 0;
+#pragma unroll 1
         for (int g = 0; g < N; g++) {
             if (v.draining(g) || v.role(g) != from) continue;
             const long long l = v.load(g);
@@ -89,6 +93,7 @@ __device__ __forceinline__ int ctl_step(const padsim_policy& pol, int min_w, int
         int u = budget / N;                                     // DistributeUniformPower
         u = u < min_w ? min_w : u;
         u = u > max_w ? max_w : u;
+#pragma unroll 1
         for (int g = 0; g < N; g++) new_cap[g] = u;
         *out_gpu = best;
         return ACT_MOVE_GPU;

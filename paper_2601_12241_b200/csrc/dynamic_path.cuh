@@ -290,6 +290,7 @@ struct JReplay {
         met += (ttft <= P.ttft_slo && tpot <= ts) ? 1 : 0;
         near += (fabs(ttft - P.ttft_slo) <= 1e-9 * P.ttft_slo || fabs(tpot - ts) <= 1e-9 * ts) ? 1 : 0;
         maxcomp = fmax(maxcomp, t);
+#pragma unroll 1
         for (int z = 0; z < nk; z++) {
             const double tz = T.phase[i] ? P.sw.tpot1[z] : P.sw.tpot0[z];
             if (ttft <= P.sw.ttft[z] && tpot <= tz) metk[z]++;
@@ -582,6 +583,7 @@ struct JReplay {
 
     // ---- dynamic ---------------------------------------------------------
     __device__ void settle(double t) {
+#pragma unroll 1
         for (int g = 0; g < N; g++) {
             const int o = g * ws;
             bool changed = false;
@@ -605,6 +607,7 @@ struct JReplay {
             w_prev = t;
         }
         long long wsum_ = 0;
+#pragma unroll 1
         for (int g = 0; g < N; g++) wsum_ += W.eff[g * ws];
         w_sum = wsum_;
     }
@@ -685,6 +688,7 @@ struct JReplay {
                         }
                     }
                 }
+#pragma unroll 1
                 for (int g = 0; g < N; g++) {
                     const int o = g * ws;
                     const int tg = newcap[g];
@@ -789,6 +793,7 @@ struct JReplay {
             tick_t = settle_t = flip_t = PAD_INF;
         }
         nk = P.sw.n;
+#pragma unroll 1
         for (int z = 0; z < nk; z++) metk[z] = 0;
         gr = P.m.ctx_growth != 0 && P.m.dec_per_ctx != 0.0;
         w_sum = P.sw.capsum[c];
