@@ -68,3 +68,16 @@ def test_enumeration_matches_oracle(lib, N, B, step, exact):
     a = pkg.enumerate_pool_uniform(N, B, 400, 750, step, exact)
     b = oracle.enumerate_pool_uniform(N, B, 400, 750, step, exact)
     assert np.array_equal(a, b)
+
+
+def test_smoke_inputs_valid():
+    # __graft_entry__.smoke() runs on the GPU box only: its inputs must pass the
+    # library's validation (every candidate within the node budget) — the
+    # oracle evaluates the same case here
+    import __graft_entry__ as ge
+    import oracle
+    from workloads import DEFAULT_MODEL, DEFAULT_SLO
+    role, cap, pols, traces, qps = ge.smoke_inputs()
+    assert (cap.sum(axis=1) <= ge.SMOKE_BUDGET_W).all()
+    ref = oracle.evaluate(DEFAULT_MODEL, role, cap, pols, ge.SMOKE_BUDGET_W, DEFAULT_SLO, traces, qps)
+    assert ref["met"].shape == (role.shape[0], len(qps))
