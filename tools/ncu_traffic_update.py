@@ -45,8 +45,12 @@ def rows(path):
 def main():
     wl, tag, reps = sys.argv[1], sys.argv[2], sys.argv[3:]
     agg = defaultdict(lambda: defaultdict(float))
+    missing = defaultdict(int)
     for p in reps:
         for d in rows(p):
+            if any(d[k] != d[k] for k in ("rd", "wr", "iss")):     # NaN: ncu did not collect
+                missing[d["name"]] += 1
+                continue
             a = agg[d["name"]]
             a["launches"] += 1
             a["read"] += d["rd"]
@@ -63,7 +67,8 @@ def main():
         w[n] = {"bytes": a["read"] + a["write"], "read": a["read"], "write": a["write"],
                 "launches": int(a["launches"]), "ncu_ms": a["dur"] * 1e3,
                 "issue_active": a["iss"] / a["dur"] / 100, "simt_threads": a["simt"] / a["dur"],
-                "warps_active": a["warps"] / a["dur"] / 100, "profile": tag}
+                "warps_active": a["warps"] / a["dur"] / 100, "profile": tag,
+                "launches_not_collected": missing.get(n, 0)}
     json.dump(data, open(OUT, "w"), indent=1)
     print(json.dumps(w, indent=1))
 
