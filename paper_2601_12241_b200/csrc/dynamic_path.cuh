@@ -224,7 +224,10 @@ struct JCtlView {
     }
 };
 
-template <bool DYN, int TB, int NG>
+// CX: the decode step has a context term (decode_per_ctx_tok_s != 0, A15/A40);
+// without it the per-GPU context sums are not kept (no in_tok loads at joins and
+// leaves) and the growth code is compiled out
+template <bool DYN, int TB, int NG, bool CX>
 struct JReplay {
     using Mask = typename MaskT<NG>::type;
     const Plan& P;
@@ -405,7 +408,7 @@ struct JReplay {
         int left = 0;
         auto leave = [&](int id) {
             complete(id, t, (t - PE(id)) / (double)(T.out_tok[id] - 1));
-            W.ctx[o] -= T.in_tok[id];
+            if (CX) W.ctx[o] -= T.in_tok[id];
             if (gr) W.sj[o] -= s - (T.out_tok[id] - 1);      // its join step (A40)
             left++;
         };
@@ -545,7 +548,7 @@ struct JReplay {
                 *wp = old | bit;
             }
             n++;
-            W.ctx[o] += T.in_tok[i];
+            if (CX) W.ctx[o] += T.in_tok[i];
             if (gr) W.sj[o] += step;
             mf = fin < mf ? fin : mf;
             joined = true;
@@ -559,7 +562,7 @@ struct JReplay {
                 W.tseg[o] = t;
                 W.st0[o] = step;
                 const int ci = W.eff[o] - P.m.min_w;
-                if (P.m.dec_per_ctx == 0.0) {
+                if (!CX) {
                     W.L[o] = P.m.ltab[(size_t)ci * max_db + (n - 1)];
                 } else {            // A15 / A40 context of the segment's first step
                     double xv = P.m.dec_fixed + P.m.dec_per_seq * (double)n;
@@ -795,7 +798,7 @@ struct JReplay {
         nk = P.sw.n;
 #pragma unroll 1
         for (int z = 0; z < nk; z++) metk[z] = 0;
-        gr = P.m.ctx_growth != 0 && P.m.dec_per_ctx != 0.0;
+        gr = CX && P.m.ctx_growth != 0 && P.m.dec_per_ctx != 0.0;
         w_sum = P.sw.capsum[c];
         a0t = R > 0 ? arr(0) : 0.0;
         w_acc = 0.0;
@@ -882,7 +885,7 @@ struct JReplay {
 // CTAs bound to one trace (s = blockIdx.x mod S); warps pull 32-replay items.
 // MR: register cap — 232 for one-warp CTAs (no spills; measured on cfg 3/4: a
 // 168-register variant that fits more warps next to stage C was not faster).
-template <bool DYN, int TB, int NG, int MR = (TB == 32 ? 232 : 168)>
+template <bool DYN, int TB, int NG, bool CX, int MR = (TB == 32 ? 232 : 168)>
 __global__ void __launch_bounds__(TB) __maxnreg__(MR) joint_kernel(const __grid_constant__ Plan P) {
     extern __shared__ __align__(128) unsigned char smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -952,7 +955,7 @@ __global__ void __launch_bounds__(TB) __maxnreg__(MR) joint_kernel(const __grid_
         const int q = u / P.n_clist;
         const int c = P.clist[u - q * P.n_clist];
         const long long r = ((long long)c * P.Q + q) * P.S + s;
-        JReplay<DYN, TB, NG> rp(P, T, X, W);
+        JReplay<DYN, TB, NG, CX> rp(P, T, X, W);
         rp.ws = ws;
         if constexpr (NG == 64) {        // next-event / routing keys: shared memory
             rp.tab.tn = (double*)smem + tid;

@@ -122,6 +122,7 @@ struct padsim_ctx {
     int kc_bits_smem[kNumKC] = {};
     int kc_ltab[kNumKC] = {};
     int kc_fine = 0;                   // five decode-pool classes (large workloads)
+    bool j_cx = false;                 // joint kernel instantiated with the context term
     int kc_bl[kNumKC] = {};            // class uses the sorted batch lists (BL) instead of the wheel
     int kc_hca[kNumKC] = {};
     size_t kc_off_hca[kNumKC] = {};
@@ -475,6 +476,17 @@ static void stagec_launch(bool cm, bool i16, int kc, bool bl, int grid, size_t s
                           const FPlan& F) {
     void* args[] = {(void*)&F};
     (void)cudaLaunchKernel(stagec_fn(cm, i16, kc, bl), dim3(grid), dim3(kThreads), args, smem, st);   // checked by the caller
+}
+
+// joint replay instantiation for (dynamic, CTA size, GPU slots, context term)
+template <bool D, int TB, int NG>
+static const void* joint_fn_t(bool cx) {
+    return cx ? (const void*)joint_kernel<D, TB, NG, true> : (const void*)joint_kernel<D, TB, NG, false>;
+}
+static const void* joint_fn(bool dyn, int tb, int ng, bool cx) {
+    if (ng == 64) return dyn ? joint_fn_t<true, 32, 64>(cx) : joint_fn_t<false, 32, 64>(cx);
+    if (tb == kThreads) return dyn ? joint_fn_t<true, kThreads, 8>(cx) : joint_fn_t<false, kThreads, 8>(cx);
+    return dyn ? joint_fn_t<true, 32, 8>(cx) : joint_fn_t<false, 32, 8>(cx);
 }
 
 // Groups static candidates by their prefill pool (caps of the prefill GPUs in
@@ -1106,15 +1118,11 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
         ctx->j_tb[dyn] = tbj;
         const void* fnj;
         size_t jb;
-        if (NG == 8) {
-            jb = tbj == kThreads ? joint_smem_bytes<8, kThreads>() : joint_smem_bytes<8, 32>();
-            fnj = tbj == kThreads
-                ? (dyn ? (const void*)joint_kernel<true, kThreads, 8> : (const void*)joint_kernel<false, kThreads, 8>)
-                : (dyn ? (const void*)joint_kernel<true, 32, 8> : (const void*)joint_kernel<false, 32, 8>);
-        } else {
-            jb = joint_smem_bytes<64, 32>();
-            fnj = dyn ? (const void*)joint_kernel<true, 32, 64> : (const void*)joint_kernel<false, 32, 64>;
-        }
+        const bool cx = model->decode_per_ctx_tok_s != 0.0;
+        ctx->j_cx = cx;
+        if (NG == 8) jb = tbj == kThreads ? joint_smem_bytes<8, kThreads>() : joint_smem_bytes<8, 32>();
+        else jb = joint_smem_bytes<64, 32>();
+        fnj = joint_fn(dyn, tbj, NG, cx);
         P.smem_trace_bytes = jb;
         CK(cudaFuncSetAttribute(fnj, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jb));
         int occj = 0;
@@ -1254,15 +1262,10 @@ int padsim_run(padsim_ctx* ctx, void* stream) {
         const int grid = dyn ? ctx->grid_dyn : ctx->grid_static;
         const size_t smem = dyn ? ctx->smem_dyn : ctx->smem_static;
         CK(cudaMemsetAsync(ctx->d_workJ[dyn], 0, (size_t)ctx->S * sizeof(unsigned), js));
-        if (ctx->j_ng == 64) {
-            if (dyn) joint_kernel<true, 32, 64><<<grid, 32, smem, js>>>(P);
-            else joint_kernel<false, 32, 64><<<grid, 32, smem, js>>>(P);
-        } else if (ctx->j_tb[dyn] == kThreads) {
-            if (dyn) joint_kernel<true, kThreads, 8><<<grid, kThreads, smem, js>>>(P);
-            else joint_kernel<false, kThreads, 8><<<grid, kThreads, smem, js>>>(P);
-        } else {
-            if (dyn) joint_kernel<true, 32, 8><<<grid, 32, smem, js>>>(P);
-            else joint_kernel<false, 32, 8><<<grid, 32, smem, js>>>(P);
+        {
+            const int tbl = ctx->j_ng == 64 ? 32 : ctx->j_tb[dyn];
+            void* args[] = {(void*)&P};
+            CK(cudaLaunchKernel(joint_fn(dyn != 0, tbl, ctx->j_ng, ctx->j_cx), dim3(grid), dim3(tbl), args, smem, js));
         }
         CK(cudaGetLastError());
     }
