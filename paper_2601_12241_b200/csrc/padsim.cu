@@ -123,6 +123,7 @@ struct padsim_ctx {
     int kc_ltab[kNumKC] = {};
     int kc_fine = 0;                   // five decode-pool classes (large workloads)
     bool j_cx = false;                 // joint kernel instantiated with the context term
+    bool j_r168 = false;               // joint kernel: 168-register one-warp-CTA variant
     int kc_bl[kNumKC] = {};            // class uses the sorted batch lists (BL) instead of the wheel
     int kc_hca[kNumKC] = {};
     size_t kc_off_hca[kNumKC] = {};
@@ -483,9 +484,12 @@ template <bool D, int TB, int NG>
 static const void* joint_fn_t(bool cx) {
     return cx ? (const void*)joint_kernel<D, TB, NG, true> : (const void*)joint_kernel<D, TB, NG, false>;
 }
-static const void* joint_fn(bool dyn, int tb, int ng, bool cx) {
+static const void* joint_fn(bool dyn, int tb, int ng, bool cx, bool r168 = false) {
     if (ng == 64) return dyn ? joint_fn_t<true, 32, 64>(cx) : joint_fn_t<false, 32, 64>(cx);
     if (tb == kThreads) return dyn ? joint_fn_t<true, kThreads, 8>(cx) : joint_fn_t<false, kThreads, 8>(cx);
+    if (r168)        // one-warp CTAs capped at 168 registers: 10 instead of 8 resident warps per SM
+        return dyn ? (cx ? (const void*)joint_kernel<true, 32, 8, true, 168> : (const void*)joint_kernel<true, 32, 8, false, 168>)
+                   : (cx ? (const void*)joint_kernel<false, 32, 8, true, 168> : (const void*)joint_kernel<false, 32, 8, false, 168>);
     return dyn ? joint_fn_t<true, 32, 8>(cx) : joint_fn_t<false, 32, 8>(cx);
 }
 
@@ -1122,7 +1126,13 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
         ctx->j_cx = cx;
         if (NG == 8) jb = tbj == kThreads ? joint_smem_bytes<8, kThreads>() : joint_smem_bytes<8, 32>();
         else jb = joint_smem_bytes<64, 32>();
-        fnj = joint_fn(dyn, tbj, NG, cx);
+        // next to a large stage C workload the joint replays run as one-warp CTAs
+        // capped at 168 registers so they leave registers to stage C (cfg 4 536 →
+        // 522 ms); when they are the bulk of the step (cfg 3) the 232-register
+        // variant is faster (327 vs 357 ms).  PADSIM_J_R168=0/1 overrides.
+        ctx->j_r168 = ctx->fact && ctx->kc_fine && NG == 8 && tbj == 32;
+        if (const char* e = getenv("PADSIM_J_R168")) ctx->j_r168 = atoi(e) != 0;
+        fnj = joint_fn(dyn, tbj, NG, cx, ctx->j_r168);
         P.smem_trace_bytes = jb;
         CK(cudaFuncSetAttribute(fnj, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jb));
         int occj = 0;
@@ -1265,7 +1275,8 @@ int padsim_run(padsim_ctx* ctx, void* stream) {
         {
             const int tbl = ctx->j_ng == 64 ? 32 : ctx->j_tb[dyn];
             void* args[] = {(void*)&P};
-            CK(cudaLaunchKernel(joint_fn(dyn != 0, tbl, ctx->j_ng, ctx->j_cx), dim3(grid), dim3(tbl), args, smem, js));
+            CK(cudaLaunchKernel(joint_fn(dyn != 0, tbl, ctx->j_ng, ctx->j_cx, ctx->j_r168), dim3(grid), dim3(tbl), args,
+                                smem, js));
         }
         CK(cudaGetLastError());
     }

@@ -44,10 +44,12 @@ def test_fine_decode_pool_classes(pkg, monkeypatch, bl_mask):
     # records bit-exact
     monkeypatch.setenv("PADSIM_KC5", "1")
     monkeypatch.setenv("PADSIM_BL_MASK", bl_mask)
+    # (with five classes the dynamic replays next to them use the 168-register
+    # joint variant: two dynamic candidates exercise it)
     xpd = [(7, 500, 700), (6, 550, 650), (5, 600, 600), (4, 600, 600), (3, 650, 560),
-           (2, 700, 540), (1, 750, 575)]
+           (2, 700, 540), (1, 750, 575), (4, 600, 600), (5, 600, 600)]
     role, cap = static_candidates(8, xpd)
-    pols = [policy("static")] * len(xpd)
+    pols = [policy("static")] * 7 + [policy("dyn-both", cooldown_s=2.0), policy("dyn-power")]
     traces = [make_trace("lb", s, 250) for s in range(2)]
     compare_records(traces, [0.5, 1.5, 3.0], DEFAULT_MODEL, role, cap, pols, DEFAULT_SLO, 4800)
 
