@@ -14,5 +14,6 @@ timeout 1200 ncu --set full --clock-control none --import-source on -k regex:sta
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:stageA -c 1 -o $D/stageA_cfg4 python tools/prof_run.py --config cfg4 --runs 1 > $D/ncu_A.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:joint -c 1 -o $D/joint_cfg4 python tools/prof_run.py --config cfg4 --runs 1 > $D/ncu_J4.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:joint -c 1 -o $D/joint_cfg3 python tools/prof_run.py --config cfg3 --runs 1 > $D/ncu_J3.log 2>&1
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29517 bench.py --gpus 2 --backend gloo --same-device --config cfg2 --steps 2 --warmup 3 --no-cpu-baseline > $D/bench_cfg2_2rank_gloo.log 2>&1
 timeout 2400 python bench.py --config cfg5 --steps 1 --warmup 3 --e2e-steps 1 --cpu-seconds 20 > $D/bench_cfg5.log 2>&1
 ls -la $D
