@@ -1298,7 +1298,9 @@ int padsim_run(padsim_ctx* ctx, void* stream) {
         // class's tail overlaps the others (they share nothing but the stream
         // records written by stage A and the scratch — each class gets its own
         // scratch slice)
-        for (int kc = 0; kc < kNumKC; kc++) {
+        const bool rev = getenv("PADSIM_KC_REV") != nullptr;      // experiment knob: launch order
+        for (int kq = 0; kq < kNumKC; kq++) {
+            const int kc = rev ? kNumKC - 1 - kq : kq;
             if (ctx->kc_n[kc] == 0) continue;
             cudaStream_t cs = ctx->sideC[kc];
             CK(cudaStreamWaitEvent(cs, ctx->evCf, 0));
