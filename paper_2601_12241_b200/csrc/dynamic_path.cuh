@@ -638,16 +638,22 @@ struct JReplay {
         if ((t - last_move) > pol.cooldown_s) {
             acted = 1;
             const double lo = t - pol.window_s;
-            while (w_tlo < w_th && wts[w_tlo] < lo) {
-                const unsigned char f = wtf[w_tlo];
-                w_tle -= f & 1;
-                w_tlt -= f >> 1;
-                w_tlo++;
-            }
-            while (w_plo < w_ph && X.tst[w_plo] < lo) {
-                const unsigned char f = X.tfl[w_plo];
-                w_ple0 -= f & 1; w_plt0 -= (f >> 1) & 1; w_ple1 -= (f >> 2) & 1; w_plt1 -= (f >> 3) & 1;
-                w_plo++;
+            // expire samples older than the window from both FIFOs in one walk: the
+            // next stamp (and flags) of each are loaded together, one round trip per
+            // step instead of one per FIFO
+            for (;;) {
+                const bool ct = w_tlo < w_th, cp = w_plo < w_ph;
+                const double a = ct ? wts[w_tlo] : PAD_INF;
+                const double b = cp ? X.tst[w_plo] : PAD_INF;
+                const unsigned char fa = ct ? wtf[w_tlo] : 0;
+                const unsigned char fb = cp ? X.tfl[w_plo] : 0;
+                const bool pa = a < lo, pb = b < lo;
+                if (!pa && !pb) break;
+                if (pa) { w_tle -= fa & 1; w_tlt -= fa >> 1; w_tlo++; }
+                if (pb) {
+                    w_ple0 -= fb & 1; w_plt0 -= (fb >> 1) & 1; w_ple1 -= (fb >> 2) & 1; w_plt1 -= (fb >> 3) & 1;
+                    w_plo++;
+                }
             }
             const int nt = w_th - w_tlo, np = w_ph - w_plo;
             const int kt = (90 * nt + 99) / 100, kq = (90 * np + 99) / 100;

@@ -16,4 +16,14 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:join
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:joint -c 1 -o $D/joint_cfg3 python tools/prof_run.py --config cfg3 --runs 1 > $D/ncu_J3.log 2>&1
 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29517 bench.py --gpus 2 --backend gloo --same-device --config cfg2 --steps 2 --warmup 3 --no-cpu-baseline > $D/bench_cfg2_2rank_gloo.log 2>&1
 timeout 2400 python bench.py --config cfg5 --steps 1 --warmup 3 --e2e-steps 1 --cpu-seconds 20 > $D/bench_cfg5.log 2>&1
+# summaries on the box (the .ncu-rep files would exceed gpurun's 64 MiB copy-back)
+{ python tools/ncu_summary.py full $D/stageC_cfg4.ncu-rep; python tools/ncu_hot.py $D/stageC_cfg4.ncu-rep 25; } > $D/sum_stageC_cfg4.txt 2>&1
+{ python tools/ncu_summary.py full $D/stageA_cfg4.ncu-rep; python tools/ncu_hot.py $D/stageA_cfg4.ncu-rep 20; } > $D/sum_stageA_cfg4.txt 2>&1
+{ python tools/ncu_summary.py full $D/joint_cfg4.ncu-rep; python tools/ncu_hot.py $D/joint_cfg4.ncu-rep 20; } > $D/sum_joint_cfg4.txt 2>&1
+{ python tools/ncu_summary.py full $D/joint_cfg3.ncu-rep; python tools/ncu_hot.py $D/joint_cfg3.ncu-rep 20; } > $D/sum_joint_cfg3.txt 2>&1
+echo '{}' > profiles/ncu_traffic.json
+python tools/ncu_traffic_update.py cfg4 $tag $D/stageC_cfg4.ncu-rep $D/stageA_cfg4.ncu-rep $D/joint_cfg4.ncu-rep > /dev/null 2>&1
+python tools/ncu_traffic_update.py cfg3 $tag $D/joint_cfg3.ncu-rep > /dev/null 2>&1
+cp profiles/ncu_traffic.json $D/ncu_traffic.json
+mkdir -p /tmp/ncu_keep && mv $D/*.ncu-rep /tmp/ncu_keep/ 2>/dev/null
 ls -la $D
