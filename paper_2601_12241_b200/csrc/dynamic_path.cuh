@@ -260,6 +260,7 @@ struct JReplay {
     long long tick_k;
     int flip_g, drain_pending, phase2;
     int w_th, w_tlo, w_tle, w_tlt, w_ph, w_plo, w_ple0, w_plt0, w_ple1, w_plt1;
+    double wh_t, wh_p;   // oldest TTFT / TPOT window stamps, as of the last window walk
     Mask touched;
     // SLO sweep + provisioned power (time-weighted Σ effective caps)
     int* metk;            // this replay's sweep counters (global, kMaxSloSweep)
@@ -469,11 +470,20 @@ struct JReplay {
             tti[tbusy * 32] = j;
             tbusy++;
         }
+        // earliest (te, id) in flight: slots read four at a time (independent loads)
         mte = PAD_INF;
-        for (int z = 0; z < tbusy; z++) {
-            const double e = tte[z * 32];
-            const int d = tti[z * 32];
-            if (e < mte || (e == mte && d < mid)) { mte = e; mid = d; mk = z; }
+        for (int z0 = 0; z0 < tbusy; z0 += 4) {
+            double ev[4];
+            int dv[4];
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                const bool ok = z0 + j < tbusy;
+                ev[j] = ok ? tte[(z0 + j) * 32] : PAD_INF;
+                dv[j] = ok ? tti[(z0 + j) * 32] : 0x7fffffff;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; j++)
+                if (ev[j] < mte || (ev[j] == mte && dv[j] < mid)) { mte = ev[j]; mid = dv[j]; mk = z0 + j; }
         }
         if (rec_base >= 0) P.rec_te[rec_base + i] = t;
         if (T.out_tok[i] == 1) complete(i, t, 0.0);
@@ -648,7 +658,7 @@ struct JReplay {
                 const unsigned char fa = ct ? wtf[w_tlo] : 0;
                 const unsigned char fb = cp ? X.tfl[w_plo] : 0;
                 const bool pa = a < lo, pb = b < lo;
-                if (!pa && !pb) break;
+                if (!pa && !pb) { wh_t = a; wh_p = b; break; }   // the heads, for skip_ticks
                 if (pa) { w_tle -= fa & 1; w_tlt -= fa >> 1; w_tlo++; }
                 if (pb) {
                     w_ple0 -= fb & 1; w_plt0 -= (fb >> 1) & 1; w_ple1 -= (fb >> 2) & 1; w_plt1 -= (fb >> 3) & 1;
@@ -750,8 +760,10 @@ struct JReplay {
             k = cooldown_tick(k0);           // no tick before it can act, whatever happens
         } else {
             k = tick_at_or_after(next_event, k0);
-            if (w_tlo < w_th) k = min(k, expiry_tick(wts[w_tlo], k0));
-            if (w_plo < w_ph) k = min(k, expiry_tick(X.tst[w_plo], k0));
+            // the oldest stamps were read by this tick's window walk (no sample is
+            // added or expired between the tick and here)
+            if (w_tlo < w_th) k = min(k, expiry_tick(wh_t, k0));
+            if (w_plo < w_ph) k = min(k, expiry_tick(wh_p, k0));
         }
         if (k > k0 && k != 0x7fffffffffffffffLL) {
             tick_k = k;

@@ -352,11 +352,20 @@ __global__ void __launch_bounds__(TB) stageA_kernel(const __grid_constant__ FPla
                 tpe[tbusy * ss] = P.st_pe[sb + j];
                 tbusy++;
             }
+            // earliest (te, id) in flight: slots read four at a time (independent loads)
             mte = PAD_INF;
-            for (int z = 0; z < tbusy; z++) {
-                const double e = tte[z * ss];
-                const int d = tidb[z * ss];
-                if (e < mte || (e == mte && d < mid)) { mte = e; mid = d; mk = z; }
+            for (int z0 = 0; z0 < tbusy; z0 += 4) {
+                double ev[4];
+                int dv[4];
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    const bool ok = z0 + j < tbusy;
+                    ev[j] = ok ? tte[(z0 + j) * ss] : PAD_INF;
+                    dv[j] = ok ? tidb[(z0 + j) * ss] : 0x7fffffff;
+                }
+#pragma unroll
+                for (int j = 0; j < 4; j++)
+                    if (ev[j] < mte || (ev[j] == mte && dv[j] < mid)) { mte = ev[j]; mid = dv[j]; mk = z0 + j; }
             }
         }
         // kind 5: arrivals → least outstanding prefill worker, lowest id (A8)
