@@ -124,6 +124,8 @@ struct Plan {
     size_t off_jw;                     // per-GPU SoA in global scratch (joint kernel, NG = 64)
     size_t off_ring;                   // decode batch lists (joint kernel, PADSIM_JBL): per lane [NG][ring_slots] u64
     int ring_slots;                    // power of 2 ≥ max_decode_batch
+    int j_kglob;                       // joint kernel, N > 8: next-event / routing keys in global scratch
+    size_t off_keys;                   // their per-warp offset (lane-interleaved [NG][32] f64, i32, i32)
     int wheel;                         // wheel size: power of 2 ≥ max out_tok, ≥ 32
     size_t warp_bytes;
     int smem_trace;                    // stage the trace in shared memory (TMA bulk)

@@ -245,6 +245,7 @@ struct JReplay {
     int* heads;          // [(g*wheel + b)*32]
     unsigned* bits;      // [(g*wheel/32 + k)*32]
     unsigned long long* ring;   // PADSIM_JBL: per-lane [g][RB] batch lists
+    size_t accoff;              // byte offset of the Fig. 6 accumulators in shared memory
     int RB, RBm;
     double* wts;         // TTFT window stamps [k], per-lane contiguous (FIFO walk)
     unsigned char* wtf;  // TTFT window flags (≤ SLO, < SLO) [k]
@@ -386,7 +387,7 @@ struct JReplay {
             i = nx;
         }
         {   // per-thread accumulators in shared memory (no extra registers)
-            double* acc = (double*)(joint_dyn_smem + ((joint_smem_base<NG, TB>() + 15) & ~(size_t)15)) +
+            double* acc = (double*)(joint_dyn_smem + accoff) +
                           threadIdx.x;
             acc[0] = acc[0] + bq;
             acc[TB] = acc[TB] + be;
@@ -822,7 +823,7 @@ struct JReplay {
         w_acc = 0.0;
         w_prev = a0t;
         {
-            double* acc = (double*)(joint_dyn_smem + ((joint_smem_base<NG, TB>() + 15) & ~(size_t)15)) +
+            double* acc = (double*)(joint_dyn_smem + accoff) +
                           threadIdx.x;
             acc[0] = 0.0;
             acc[TB] = 0.0;
@@ -908,6 +909,7 @@ __global__ void __launch_bounds__(TB) __maxnreg__(MR) joint_kernel(const __grid_
     extern __shared__ __align__(128) unsigned char smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     char* wbase = P.scratch + ((size_t)blockIdx.x * (TB / 32) + warp) * P.warp_bytes;
+    const size_t accoff = (NG == 64 && P.j_kglob) ? 0 : ((joint_smem_base<NG, TB>() + 15) & ~(size_t)15);
     JWork W;
     int ws;
     if (NG == 8) {           // per-GPU SoA in shared memory
@@ -975,11 +977,19 @@ __global__ void __launch_bounds__(TB) __maxnreg__(MR) joint_kernel(const __grid_
         const long long r = ((long long)c * P.Q + q) * P.S + s;
         JReplay<DYN, TB, NG, CX> rp(P, T, X, W);
         rp.ws = ws;
-        if constexpr (NG == 64) {        // next-event / routing keys: shared memory
-            rp.tab.tn = (double*)smem + tid;
-            rp.tab.kp = (int*)(smem + (size_t)NG * TB * sizeof(double)) + tid;
-            rp.tab.kd = rp.tab.kp + NG * TB;
-            rp.tab.st = TB;
+        rp.accoff = accoff;
+        if constexpr (NG == 64) {        // next-event / routing keys
+            if (P.j_kglob) {             // lane-interleaved global scratch (frees shared memory)
+                rp.tab.tn = (double*)(wbase + P.off_keys) + lane;
+                rp.tab.kp = (int*)(wbase + P.off_keys + (size_t)NG * 32 * sizeof(double)) + lane;
+                rp.tab.kd = rp.tab.kp + NG * 32;
+                rp.tab.st = 32;
+            } else {                     // shared memory
+                rp.tab.tn = (double*)smem + tid;
+                rp.tab.kp = (int*)(smem + (size_t)NG * TB * sizeof(double)) + tid;
+                rp.tab.kd = rp.tab.kp + NG * TB;
+                rp.tab.st = TB;
+            }
         }
         rp.metk = P.sw.rep_met + r * kMaxSloSweep;
         rp.tte = tte;
@@ -999,7 +1009,7 @@ __global__ void __launch_bounds__(TB) __maxnreg__(MR) joint_kernel(const __grid_
         P.rep_events[r] = res.events;
         P.sw.rep_watts[r] = res.watts;
         {
-            const double* acc = (const double*)(smem + ((joint_smem_base<NG, TB>() + 15) & ~(size_t)15)) + tid;
+            const double* acc = (const double*)(smem + accoff) + tid;
             P.sw.rep_sq[r] = acc[0];
             P.sw.rep_se[r] = acc[TB];
         }

@@ -1106,6 +1106,11 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
         P.ring_slots = rslots;
         if (PADSIM_JBL) P.off_ring = take((size_t)32 * NG * rslots * sizeof(unsigned long long));
         if (NG == 64) P.off_jw = take(joint_global_bytes_per_warp(64));
+        // N > 8: the per-GPU next-event / routing keys in global scratch instead of
+        // 32 KB of shared memory per warp, so registers (11 warps/SM) instead of shared
+        // memory (7) bound the occupancy: cfg 5 subset (65 k replays) 27.7 -> 23.3 s
+        P.j_kglob = NG == 64 && getenv("PADSIM_J64_KSMEM") == nullptr;   // knob: keep them in smem
+        if (P.j_kglob) P.off_keys = take((size_t)NG * 32 * (sizeof(double) + 2 * sizeof(int)));
         P.warp_bytes = off;
         ctx->j8[dyn] = true;
         ctx->j_ng = NG;
@@ -1126,7 +1131,7 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
         const bool cx = model->decode_per_ctx_tok_s != 0.0;
         ctx->j_cx = cx;
         if (NG == 8) jb = tbj == kThreads ? joint_smem_bytes<8, kThreads>() : joint_smem_bytes<8, 32>();
-        else jb = joint_smem_bytes<64, 32>();
+        else jb = P.j_kglob ? 2 * 32 * sizeof(double) : joint_smem_bytes<64, 32>();
         // next to a large stage C workload the joint replays run as one-warp CTAs
         // capped at 168 registers so they leave registers to stage C (cfg 4 536 →
         // 522 ms); when they are the bulk of the step (cfg 3) the 232-register
