@@ -1163,7 +1163,10 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
         P.scratch_per_cta = per_cta;
         size_t frj = 0, tmj = 0;
         CK(cudaMemGetInfo(&frj, &tmj));
-        const long long cap_ctas = std::max<long long>(n_traces, (long long)((tmj * 3 / 10) / per_cta));
+        // scratch cap: a fraction of device memory (knob PADSIM_J_MEMFRAC, default 0.3)
+        double mfr = 0.3;
+        if (const char* e = getenv("PADSIM_J_MEMFRAC")) mfr = std::min(0.8, std::max(0.05, atof(e)));
+        const long long cap_ctas = std::max<long long>(n_traces, (long long)((double)tmj * mfr / (double)per_cta));
         long long gridj = std::min<long long>(per_trace * n_traces, (cap_ctas / n_traces) * n_traces);
         gridj = std::max<long long>(gridj, n_traces);
         char* scrj = nullptr;
