@@ -169,7 +169,10 @@ __host__ __device__ constexpr size_t a_slot_bytes() {   // KV slots kept in smem
 #ifndef PADSIM_EAGER
 #define PADSIM_EAGER 1     // stage C eager joins (see the transfer-end handler)
 #endif
-constexpr int kPre = 8;    // ids fetched per batch of independent loads
+#ifndef PADSIM_KPRE
+#define PADSIM_KPRE 4
+#endif
+constexpr int kPre = PADSIM_KPRE;    // ids fetched per batch of independent loads
 constexpr int kLtabRows = 16;  // max distinct decode caps of the shared-memory step table
 constexpr int kATbBig = 256;   // stage A CTA size for large workloads
 
