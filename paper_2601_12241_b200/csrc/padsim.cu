@@ -1121,7 +1121,9 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
         P.smem_trace = 0;
         // measured (cfg 3): a 16-inter-arrival lane clock window speeds the joint
         // replays up 15 % (622 -> 529 ms/step): lanes read the same trace lines
-        P.sync_win = 16.f;
+        // (round end, with batch lists and the merged window walk: 8 inter-arrivals
+        // cfg 3 315 -> 308 ms, 32: 328 ms; cfg 4 unchanged)
+        P.sync_win = 8.f;
         if (const char* e = getenv("PADSIM_SYNC_WIN")) P.sync_win = (float)atof(e);   // experiment knob
         const long long UJ = (long long)n_traces * n_qps * P.n_clist;
         const int tbj = (NG == 8 && UJ >= (long long)ctx->n_sm * 3 * kThreads) ? kThreads : 32;
