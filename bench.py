@@ -40,19 +40,21 @@ from workloads import (DEFAULT_MODEL, get_config, make_trace, policy,  # noqa: E
 from workloads.configs import dynamic_candidates  # noqa: E402
 
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+MICRO_PEAKS_PATH = os.path.join(ROOT, "profiles", "peaks_r02.json")   # tools/peaks_microbench.cu
 TRAFFIC_PATH = os.path.join(ROOT, "profiles", "ncu_traffic.json")   # dram bytes/launch per kernel
-OPS_PER_EVENT = 32          # algorithmic ALU ops of one DES event handler
-# algorithmic DES events per simulated request: stage A
-# arrival+routing, batch share, KV transfer end; stage C transfer-end routing, join,
-# leave+scoring; the joint replay all six (controller ticks not counted)
-EV_PER_REQ = {"stageA_kernel": 3, "stageC_kernel": 3, "joint_kernel": 6}
-LANES_PER_SM = 128          # INT32/FP32 lanes per SM (4 SMSP x 32)
+# Algorithmic FP64 operations per simulated request: stage A —
+# arrival scale (1 mul), its share of the prefill batch latency (1 div), TTFT
+# (1 sub), transfer end (1 add) = 4; stage C — two segment boundaries (2 x (mul +
+# add)), TPOT (sub + div), two SLO compares = 8; the joint replay does both = 12.
+FP64_OPS_PER_REQ = {"stageA_kernel": 4, "stageC_kernel": 8, "joint_kernel": 12}
+WARP_INSTR_BUDGET = 15      # warp-instructions per simulated request (8-lane groups)
 
 
 def build_workload(cfg: dict, rank: int = 0, enumerate_fn=None):
-    """Candidates (role, cap, policies), traces (this rank's seed block), qps."""
+    """Candidates (role, cap, policies, per-candidate budgets), traces, qps.
+    Every rank builds the same fixed grid (the shard is cut from it)."""
     N, B = cfg["n_gpus"], cfg["budget_w"]
-    rows, pols = [], []
+    rows, pols, buds = [], [], []
     if cfg.get("space"):
         sp = cfg["space"]
         xpd = enumerate_fn(N, B, DEFAULT_MODEL["min_w"], DEFAULT_MODEL["max_w"], sp["step_w"])
@@ -60,17 +62,21 @@ def build_workload(cfg: dict, rank: int = 0, enumerate_fn=None):
             xpd = xpd[xpd[:, 0] == sp["x_only"]]
         rows += [tuple(r) for r in xpd]
         pols += [policy("static")] * len(xpd)
-    for xpd in cfg.get("statics", []):
-        rows.append(tuple(xpd))
+        buds += [B] * len(xpd)
+    for st in cfg.get("statics", []):
+        rows.append(tuple(st[:3]))
         pols.append(policy("static"))
+        buds.append(st[3] if len(st) > 3 else B)     # e.g. 4P4D-750 W at 6000 W
     for x, p, d, pol in dynamic_candidates(cfg):
         rows.append((x, p, d))
         pols.append(pol)
+        buds.append(B)
     role, cap = static_candidates(N, rows)
     fams = cfg["family"] if isinstance(cfg["family"], tuple) else (cfg["family"],)
     S = cfg["seeds"]
-    traces = [make_trace(f, rank * S + s, cfg["n_req"]) for f in fams for s in range(S)]
-    return role, cap, pols, traces, list(cfg["qps"])
+    traces = [make_trace(f, s, cfg["n_req"]) for f in fams for s in range(S)]
+    cb = np.asarray(buds, np.int32)
+    return role, cap, pols, traces, list(cfg["qps"]), (None if (cb == B).all() else cb)
 
 
 class ClockSampler:
@@ -141,36 +147,61 @@ def peaks():
         return {}
 
 
-def cpu_baseline(cfg, role, cap, pols, traces, qps, seconds=15.0):
-    """The oracle as it stands on a bounded deterministic sample of the workload."""
+def cpu_baseline(cfg, role, cap, pols, traces, qps, cand_budget=None, seconds=15.0, gpu_rep=None):
+    """The oracle as it stands on a bounded deterministic sample of the workload
+    (host cores, then one thread).  With ``gpu_rep`` (the GPU's per-replay
+    met / goodput / duration of the same grid) the sampled replays double as a
+    parity check of the timed launch configuration: mismatches are counted."""
     import oracle
     cores = os.cpu_count() or 1
     C, Q, S = role.shape[0], len(qps), len(traces)
     total = C * Q * S
-    # deterministic sample: every k-th (c, q) pair, all traces of seed 0 only
+    B = cfg["budget_w"]
+
+    def run(cs, q, nt):
+        return oracle.evaluate(DEFAULT_MODEL, role[cs], cap[cs], [pols[i] for i in cs], B, cfg["slo"],
+                               traces[:1], [qps[q]], n_threads=nt, per_replay=True,
+                               cand_budget_w=None if cand_budget is None else cand_budget[cs])
     t0 = time.perf_counter()
-    probe = oracle.evaluate(DEFAULT_MODEL, role[:2], cap[:2], pols[:2], cfg["budget_w"], cfg["slo"],
-                            traces[:1], qps[len(qps) // 2: len(qps) // 2 + 1], n_threads=1)
-    del probe
-    per = max((time.perf_counter() - t0) / 2, 1e-4)
+    run(np.arange(min(2, C)), Q // 2, 1)
+    per = max((time.perf_counter() - t0) / min(2, C), 1e-4)
     n_pairs = int(max(cores, min(C * Q, seconds * cores / per)))
     stride = max(1, (C * Q) // n_pairs)
-    sel = np.arange(0, C * Q, stride)[:n_pairs]
-    cs = sel // Q
-    qs = sel % Q
-    reps = 0
+    sel = set(range(0, C * Q, stride)[:n_pairs])
+    # every dynamic candidate appears at least once (at QPS index c mod Q)
+    sel |= {c * Q + c % Q for c in range(C) if pols[c]["kind"] != 0}
+    sel = np.array(sorted(sel))
+    cs_all, qs_all = sel // Q, sel % Q
+    reps, mism = 0, 0
     t0 = time.perf_counter()
-    # group by q so one evaluate() call per QPS point uses all host threads
-    for q in np.unique(qs):
-        cc = cs[qs == q]
-        oracle.evaluate(DEFAULT_MODEL, role[cc], cap[cc], [pols[i] for i in cc], cfg["budget_w"],
-                        cfg["slo"], traces[:1], [qps[q]], n_threads=cores)
-        reps += len(cc)
+    for q in np.unique(qs_all):          # one evaluate() per QPS point uses all host threads
+        cs = cs_all[qs_all == q]
+        ev = run(cs, int(q), cores)
+        reps += len(cs)
+        if gpu_rep is not None:
+            g_met = gpu_rep["met"][cs, q, 0]
+            g_good = gpu_rep["goodput"][cs, q, 0]
+            g_dur = gpu_rep["duration"][cs, q, 0]
+            mism += int(((ev["rep_met"][:, 0, 0] != g_met) | (ev["rep_goodput"][:, 0, 0] != g_good) |
+                         (ev["rep_duration"][:, 0, 0] != g_dur)).sum())
     dt = time.perf_counter() - t0
+    # one host thread on a small slice of the same sample
+    n1 = max(1, min(len(sel), int(max(1.0, seconds / 4) / per)))
+    t1 = time.perf_counter()
+    for k in sel[:: max(1, len(sel) // n1)][:n1]:
+        run(np.array([k // Q]), int(k % Q), 1)
+    dt1 = time.perf_counter() - t1
     R = traces[0]["s_unit"].size
-    return {"value": reps / dt, "unit": "evals/s", "cores": cores, "kind": "oracle",
-            "sample": f"{reps} of {total} replays (every {stride}th (candidate,QPS) pair, trace seed 0), "
-                      f"{dt:.1f} s", "req_per_s": reps * R / dt}
+    out = {"value": reps / dt, "unit": "evals/s", "cores": cores, "kind": "oracle",
+           "sample": f"{reps} of {total} replays (every {stride}th (candidate,QPS) pair + every dynamic "
+                     f"candidate once, trace seed 0), {dt:.1f} s on {cores} threads",
+           "req_per_s": reps * R / dt,
+           "one_thread": {"value": n1 / dt1, "unit": "evals/s", "cores": 1,
+                          "sample": f"{n1} replays of the same sample, {dt1:.1f} s"}}
+    if gpu_rep is not None:
+        out["parity"] = {"replays": reps, "mismatches": mism,
+                         "compared": "per-replay met, goodput, duration (exact) vs the timed GPU run"}
+    return out
 
 
 def run_reference(args, cfg, rank, world):
@@ -178,25 +209,32 @@ def run_reference(args, cfg, rank, world):
     if rank != 0:
         return
     import oracle                       # the reference arm is the oracle alone
-    role, cap, pols, traces, qps = build_workload(cfg, 0, oracle.enumerate_pool_uniform)
+    role, cap, pols, traces, qps, cb = build_workload(cfg, 0, oracle.enumerate_pool_uniform)
     vals = []
     last = None
     for k in range(args.warmup + args.steps):
-        cb = cpu_baseline(cfg, role, cap, pols, traces, qps, seconds=max(2.0, 20.0 / max(1, args.steps)))
+        cb_ = cpu_baseline(cfg, role, cap, pols, traces, qps, cb, seconds=max(2.0, 20.0 / max(1, args.steps)))
         if k >= args.warmup:
-            vals.append(cb["value"])
-            last = cb
+            vals.append(cb_["value"])
+            last = cb_
     v = float(np.mean(vals))
     R = traces[0]["s_unit"].size
     line = {"impl": "reference", "metric": "candidate-trace evaluations/sec", "value": v,
             "unit": "evals/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": None, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg["name"], "sample": last["sample"]},
             "cpu_baseline": dict(last, value=v),
             "e2e": {"value": v, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "sim_req_per_s": v * R}
     print(json.dumps(line), flush=True)
+
+
+def micro_peaks():
+    try:
+        return json.load(open(MICRO_PEAKS_PATH))
+    except Exception:
+        return {}
 
 
 def main():
@@ -229,7 +267,8 @@ def main():
     import torch.distributed as dist
     import paper_2601_12241_b200 as pkg
     from paper_2601_12241_b200.build import build
-    from paper_2601_12241_b200.distributed import allreduce_met, max_over_ranks
+    from paper_2601_12241_b200.distributed import (all_shards, evaluate_sharded, gather_results,
+                                                   max_over_ranks)
     if rank == 0:
         build()
     local_dev = 0 if args.same_device else local
@@ -246,12 +285,18 @@ def main():
     torch.cuda.set_device(dev)
     stream = torch.cuda.current_stream(dev)
 
-    role, cap, pols, traces, qps = build_workload(cfg, rank, pkg.enumerate_pool_uniform)
+    # the fixed grid (BASELINE config) and this rank's shard of it
+    role, cap, pols, traces, qps, cand_budget = build_workload(cfg, rank, pkg.enumerate_pool_uniform)
     C, Q, S = role.shape[0], len(qps), len(traces)
     R = traces[0]["s_unit"].size
-    n_req_total = sum(t["s_unit"].size for t in traces)
-    ctx = pkg.Context(local)
-    ctx.plan(traces, qps, DEFAULT_MODEL, role, cap, pols, cfg["slo"], cfg["budget_w"])
+    static = np.array([p["kind"] == 0 for p in pols])
+    shards = all_shards(world, role, cap, Q, static)
+    sh = shards[rank]
+    Cl, Ql = len(sh.cand), len(sh.qps)
+    ctx = pkg.Context(local, stream.cuda_stream)
+    ctx.plan(traces, [qps[q] for q in sh.qps], DEFAULT_MODEL, role[sh.cand], cap[sh.cand],
+             [pols[c] for c in sh.cand], cfg["slo"], cfg["budget_w"],
+             cand_budget_w=None if cand_budget is None else cand_budget[sh.cand])
     d = ctx.device_results()
 
     def as_tensor(ptr, n, dtype, typestr):
@@ -260,26 +305,27 @@ def main():
                                         "version": 3, "strides": None}
         return torch.as_tensor(_A(), device=dev).view(dtype)
 
-    met_dev = as_tensor(d.d_met, C * Q, torch.int64, "<i8")
-    ev_dev = as_tensor(d.d_rep_events, C * Q * S, torch.int64, "<i8")
-    met_glob = torch.empty(C * Q, dtype=torch.int64, device=dev)
+    met_dev = as_tensor(d.d_met, Cl * Ql, torch.int64, "<i8")
+    good_dev = as_tensor(d.d_goodput, Cl * Ql, torch.float64, "<f8")
+    capsum = torch.as_tensor(cap.sum(axis=1).astype(np.int32)).to(dev)
     am_glob = torch.empty(Q, dtype=torch.int32, device=dev)
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
     def step():
         ctx.run(stream.cuda_stream)
-        if world > 1:
-            met_glob.copy_(met_dev)
-            allreduce_met(met_glob)
-            ctx.argmax_device(met_glob.data_ptr(), C, Q, am_glob.data_ptr(), stream.cuda_stream)
-        return 3 + (1 if world > 1 else 0) + (1 if any(p["kind"] for p in pols) else 0)
+        n = ctx.launch_count()
+        if world > 1:      # the one exchange: allgather of the scores, then the global argmax
+            met_g, _good_g = gather_results(met_dev, good_dev, shards, C, Q)
+            ctx.argmax_device(met_g.data_ptr(), C, Q, am_glob.data_ptr(), stream.cuda_stream,
+                              d_capsum_ptr=capsum.data_ptr())
+            n += 1
+        return n
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     launches = 0
     times = []
-    replay_ms = []
     kern_ms = []
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
@@ -290,101 +336,115 @@ def main():
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            launches += step()
+            launches = step()
             e1.record(stream)
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1))
-            replay_ms.append(ctx.replay_kernel_ms())
             kern_ms.append(ctx.kernel_times_ms())
     t_local = sum(times) / 1e3
     t_max = max_over_ranks(t_local, device=dev)
-    units = C * Q * S * world
+    units = C * Q * S                       # the whole fixed grid, over all ranks (strong scaling)
     value = units * args.steps / t_max
-    ev_rep = ev_dev.view(C, Q, S)
-    is_dyn = torch.tensor([p["kind"] != 0 for p in pols], device=dev)
-    ev_static = int(ev_rep[~is_dyn].sum().item())
-    ev_dyn = int(ev_rep[is_dyn].sum().item())
+    ev_rep = as_tensor(d.d_rep_events, Cl * Ql * S, torch.int64, "<i8").view(Cl, Ql, S)
+    is_dyn = torch.tensor([pols[c]["kind"] != 0 for c in sh.cand], device=dev)
+    ev_static = int(ev_rep[~is_dyn].sum().item()) if Cl else 0
+    ev_dyn = int(ev_rep[is_dyn].sum().item()) if Cl else 0
     ev_a = int(as_tensor(d.d_aux_events, d.n_aux_events, torch.int64, "<i8").sum().item()) \
         if d.n_aux_events > 0 else 0
     if ev_a == 0:            # N > 8: static replays run in the joint kernel
         ev_dyn += ev_static
         ev_static = 0
-    events_per_launch = ev_a + ev_static + ev_dyn
-    # simulated requests each kernel processes per launch (the roofline unit)
+    # per-rank replay results of the timed configuration (for the parity sample)
+    rep = ctx.fetch_replays()
+
+    # per-kernel device times in isolation (kernels serialised on one stream; not the
+    # timed region): the roofline's kernel time
+    ctx.set_tuning({"serialize": 1})
+    iso = []
+    for k in range(4):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        ctx.run(stream.cuda_stream)
+        torch.cuda.synchronize()
+        if k:
+            iso.append(ctx.kernel_times_ms())
+    ctx.set_tuning(None)
+    iso = np.mean(np.array(iso), axis=0)
+
     r_sum = sum(int(t["s_unit"].size) for t in traces)
-    static_idx = [c for c in range(C) if pols[c]["kind"] == 0]
+    static_idx = [c for c in sh.cand if pols[c]["kind"] == 0]
     groups = {tuple(int(v) for v in cap[c][role[c] == 0]) for c in static_idx}
     fact = ev_a > 0                       # the factorized static path ran (N <= 8)
-    req_k = {"stageA_kernel": len(groups) * Q * r_sum if fact else 0,
-             "stageC_kernel": len(static_idx) * Q * r_sum if fact else 0,
-             "joint_kernel": (C - len(static_idx) + (0 if fact else len(static_idx))) * Q * r_sum}
+    req_k = {"stageA_kernel": len(groups) * Ql * r_sum if fact else 0,
+             "stageC_kernel": len(static_idx) * Ql * r_sum if fact else 0,
+             "joint_kernel": (Cl - len(static_idx) + (0 if fact else len(static_idx))) * Ql * r_sum}
 
-    # e2e: the public one-shot C-ABI call with host buffers
+    # e2e: the public API with host buffers (evaluate_sharded = padsim_evaluate_allocations on
+    # this rank's shard + allgather + argmax; one process: exactly padsim_evaluate_allocations)
     e2e_times = []
     h2d = sum(t["s_unit"].nbytes + 4 * t["in_tok"].size * 2 + t["s_unit"].size for t in traces)
-    h2d += role.nbytes + cap.nbytes + 48 * C + 8 * Q
-    d2h = C * Q * 24 + Q * 4
+    h2d += Cl * (role.shape[1] * 5 + 48) + 8 * Ql
+    d2h = Cl * Ql * 24 + Ql * 4 + (C * Q * 16 + Q * 4 if world > 1 else 0)
     for k in range(args.e2e_steps + 1 if args.e2e_steps > 0 else 0):
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
-        out = pkg.evaluate_allocations(traces, qps, DEFAULT_MODEL, role, cap, pols, cfg["slo"],
-                                       cfg["budget_w"], ctx=ctx)
-        if world > 1:
-            mg = torch.as_tensor(out["met"].ravel()).to(dev)
-            allreduce_met(mg)
-            mg.cpu()
+        out = evaluate_sharded(traces, qps, DEFAULT_MODEL, role, cap, pols, cfg["slo"], cfg["budget_w"],
+                               ctx=ctx, device=local, cand_budget_w=cand_budget)
         if k > 0:
             e2e_times.append(time.perf_counter() - t0)
     e2e_t = max_over_ranks(float(np.mean(e2e_times)) if e2e_times else float("nan"), device=dev)
-    # restore the plan timed above (evaluate_allocations re-planned the ctx)
+    del out
 
     if rank == 0:
         pk = peaks()
+        mp_ = micro_peaks()
         clocks = clk.summary()
-        f_mhz = clocks.get("sm_mhz") or pk.get("sm_max_mhz") or 1965.0
-        r_ms = float(np.mean(replay_ms)) if replay_ms else float("nan")
         km = np.mean(np.array(kern_ms), axis=0) if kern_ms else np.zeros(3)
         names = ["stageA_kernel", "stageC_kernel", "joint_kernel"]
         evs = [ev_a, ev_static, ev_dyn]
-        # dominant kernel = the one doing most of the algorithmic work (simulated
-        # requests × events per request); kernels overlap on several streams, so
-        # the longest event span is not necessarily the one the step is made of
-        ops = [req_k[n] * EV_PER_REQ[n] * OPS_PER_EVENT for n in names]
-        dom = int(np.argmax(ops))
-        achieved = ops[dom] / (km[dom] / 1e3) / 1e12 if km[dom] > 0 else float("nan")
-        peak = 148 * LANES_PER_SM * f_mhz * 1e6 / 1e12
+        # dominant kernel = the one with the most isolated device time
+        dom = int(np.argmax(iso))
+        fp64_ops = req_k[names[dom]] * FP64_OPS_PER_REQ[names[dom]]
+        achieved = fp64_ops / (iso[dom] / 1e3) / 1e12 if iso[dom] > 0 else float("nan")
+        peak_fp64 = (mp_.get("_derived", {}).get("fp64_pipe_ops_per_s") or 148 * 64 * 1965e6) / 1e12
+        wipr = ncu_field(cfg["name"], names[dom], "warp_instr_per_request")
         cfg4 = get_config("cfg4")
         cfg4_replays = (955 + 21) * len(cfg4["qps"]) * cfg4["seeds"]
         line = {
             "metric": "candidate-trace evaluations/sec", "value": value, "unit": "evals/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": t_max / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": t_max / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg["name"], "n_cand": C, "n_qps": Q, "n_traces_per_rank": S,
-                       "n_req": R, "replays_per_rank": C * Q * S, "family": cfg["family"],
-                       "l2": "flushed between steps (512 MiB write)"},
-            "sim_req_per_s": value * n_req_total / S,
+            "config": {"workload": cfg["name"], "n_cand": C, "n_qps": Q, "n_traces": S, "n_req": R,
+                       "replays": units, "family": cfg["family"], "shard": sh.mode,
+                       "replays_rank0": Cl * Ql * S, "l2": "flushed between steps (512 MiB write)"},
+            "sim_req_per_s": value * r_sum / S,
             "e2e": {"value": units / e2e_t, "unit": "evals/s", "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": int(d2h), "api": "padsim_evaluate_allocations"},
+                    "d2h_bytes_per_step": int(d2h), "api": "evaluate_sharded -> padsim_evaluate_allocations"},
             "gpu_launches": launches,
-            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tops/s",
-                         "frac": achieved / peak, "traffic": ncu_traffic(cfg["name"], names[dom]),
-                         "kernel": names[dom], "kernel_ms": float(km[dom]),
-                         "unit_basis": "simulated requests x events/request x ops/event",
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak_fp64, "unit": "TFLOP/s",
+                         "frac": achieved / peak_fp64,
+                         "traffic": ncu_traffic(cfg["name"], names[dom]),
+                         "kernel": names[dom], "kernel_ms_isolated": float(iso[dom]),
+                         "unit_basis": f"simulated requests x {FP64_OPS_PER_REQ[names[dom]]} algorithmic FP64 "
+                                       "ops/request (SURVEY 8(d)) / isolated kernel time",
                          "requests_per_launch": req_k[names[dom]],
-                         "events_per_request": EV_PER_REQ[names[dom]], "ops_per_event": OPS_PER_EVENT,
-                         "des_instants_per_launch": evs[dom],
-                         "ncu_issue_active": ncu_field(cfg["name"], names[dom], "issue_active"),
-                         "peak_basis": f"148 SM x 128 lanes x {f_mhz:.0f} MHz (sampled clock)",
-                         "kernels_ms": {n: float(v) for n, v in zip(names, km)},
-                         "kernels_events": {n: int(v) for n, v in zip(names, evs)},
-                         "replay_kernels_ms": r_ms},
+                         "peak_basis": "measured DFMA rate (profiles/peaks_r02.json, tools/peaks_microbench.cu)",
+                         "issue": {"warp_instr_per_request": wipr, "budget": WARP_INSTR_BUDGET,
+                                   "event_frac": (WARP_INSTR_BUDGET / wipr) if wipr else None,
+                                   "issue_active": ncu_field(cfg["name"], names[dom], "issue_active"),
+                                   "source": "ncu --set full of the dominant kernel (profiles/ncu_traffic.json)"},
+                         "kernels_ms_isolated": {n: float(v) for n, v in zip(names, iso)},
+                         "kernels_ms_concurrent_span": {n: float(v) for n, v in zip(names, km)},
+                         "kernels_des_instants": {n: int(v) for n, v in zip(names, evs)}},
             "north_star_cfg4_seconds_at_this_rate": cfg4_replays / value,
             "clocks": clocks,
         }
         if not args.no_cpu_baseline and world == 1:
-            line["cpu_baseline"] = cpu_baseline(cfg, role, cap, pols, traces, qps, args.cpu_seconds)
+            line["cpu_baseline"] = cpu_baseline(cfg, role, cap, pols, traces, qps, cand_budget,
+                                                args.cpu_seconds, gpu_rep=rep)
+            line["parity"] = line["cpu_baseline"].pop("parity")
         print(json.dumps(line), flush=True)
     ctx.close()
     if world > 1:

@@ -112,10 +112,15 @@ typedef struct {
  * decode batch.  For kind 1–3:
  * tick_s > 0 (MIN_TIME), settle_s > 0, reassign_s > 0
  * (P:294), cooldown_s >= settle_s, window_s >= 0, power_step_w > 0,
- * decode_ceiling_w ∈ [min_w, max_w], queue_threshold >= 0.        */
+ * decode_ceiling_w ∈ [min_w, max_w], queue_threshold >= 0,
+ * window_stamp ∈ {0, 1}.                                                      */
 typedef struct {
     int32_t kind;
     int32_t queue_threshold, power_step_w, decode_ceiling_w;
+    int32_t window_stamp;   /* controller TTFT samples stamped at 0: the first token
+                               (prefill end, reading A22 — the default) or 1: request
+                               completion; TPOT samples are always
+                               stamped at completion                                  */
     double cooldown_s, tick_s, window_s, settle_s, reassign_s;
 } padsim_policy;
 
@@ -130,7 +135,11 @@ typedef struct {
 
 /* SLOs: inclusive ≤ (A6). All > 0.           */
 typedef struct { double ttft_s; double tpot_s[2]; } padsim_slo;
-typedef struct { int32_t budget_w; } padsim_budget;   /* node GPU budget */
+/* Node GPU power budget (4800 W).  cand_budget_w (nullable) gives a
+ * budget per candidate [n_cand] instead — e.g. Fig. 5a's 4P4D-750W reference
+ * at 6000 W next to 4800 W candidates; it bounds Σ caps (validation)
+ * and DistributeUniformPower / the N·min_w check of a dynamic candidate.      */
+typedef struct { int32_t budget_w; const int32_t* cand_budget_w; } padsim_budget;
 
 /* a7/a8 results.  met[c*n_qps+q] = Σ over traces of requests meeting both
  * SLOs (int, exact); goodput = Σ over traces (ascending) of met/duration;
@@ -147,7 +156,10 @@ typedef struct {
 } padsim_result;
 
 /* ---- context ------------------------------------------------------------ */
-int padsim_create(int32_t cuda_device, padsim_ctx** out);
+/* padsim_create: bind a context to CUDA device `cuda_device`; `cuda_stream`
+ * (cudaStream_t as void*, NULL = the legacy default stream) is the stream the
+ * one-shot padsim_evaluate_allocations runs on.  ECUDA without a device.     */
+int padsim_create(int32_t cuda_device, void* cuda_stream, padsim_ctx** out);
 void padsim_destroy(padsim_ctx* ctx);
 const char* padsim_last_error(const padsim_ctx* ctx);
 const char* padsim_version(void);
@@ -260,42 +272,102 @@ int padsim_fetch_decomposition(padsim_ctx* ctx, void* stream, double* rep_queue,
 int padsim_fetch_percentiles(padsim_ctx* ctx, void* stream, const int32_t* pcts, int32_t n_pct,
                              double* out);
 
-/* a8 across ranks: argmax over a device met array (e.g. after an NCCL
- * all-reduce of d_met) using the planned candidates' Σcaps; asynchronous.   */
-int padsim_argmax_device(padsim_ctx* ctx, void* stream, const int64_t* d_met, int32_t n_cand,
-                         int32_t n_qps, int32_t* d_argmax);
+/* a8 across ranks: argmax per QPS over a device met array
+ * d_met[n_cand * n_qps] (e.g. the all-gathered scores of every rank's shard)
+ * with the key (Σmet ↓, Σcaps ↑, index ↑) (A25).  d_capsum[n_cand] (device,
+ * nullable) gives each candidate's Σ initial caps; NULL uses the planned
+ * candidates' (then n_cand must equal the plan's).  Asynchronous on stream.  */
+int padsim_argmax_device(padsim_ctx* ctx, void* stream, const int64_t* d_met, const int32_t* d_capsum,
+                         int32_t n_cand, int32_t n_qps, int32_t* d_argmax);
 
-/* ---- step_controller (north_star; Algorithm 1 body) -----------
- * One controller decision, run on the device by the same __device__ code the
- * dynamic replay kernel uses.  Guards of Alg. 1 on the window statistics
- * (strict > / <), cooldown strict (A20), PowerLimitsReached checked
- * before moving (A18), MovePower, MoveGPU of the least-loaded donor
- * then DistributeUniformPower.  Mutates *state, writes
- * *action.  Synchronous.                                                      */
+/* ---- step_controller (north_star; Algorithm 1) -----------------
+ * A PURE HOST FUNCTION (no context, no device, no allocation; thread-safe:
+ * it touches only *inout and *out).  One controller invocation at time now_s
+ * on the full controller state of one node:
+ *   1. time-driven transitions due by now_s, in the A10 kind order:
+ *      settle: every GPU with settle_deadline_s[g] <= now_s takes
+ *      eff = cmd when cmd < eff and, if pending_raise_w[g] > 0, cmd = eff =
+ *      pending_raise_w[g] (sinks are raised at the donors' settle instant,
+ *      source-before-sink); the deadline is cleared (< 0).
+ *      role flip: a draining GPU whose drain completed
+ *      (stats->drained_empty_s[g] >= 0) flips roles at drained_empty_s[g] +
+ *      reassign_s; if that time is <= now_s the flip is applied (role ^= 1,
+ *      draining = 0), otherwise flip_deadline_s[g] holds it.
+ *   2. the Alg. 1 decision on the window statistics (guards strict as printed,
+ *      P:229–240, A20; cooldown strict; |Q_P| > THRESHOLD; PowerLimitsReached
+ *      checked before moving, A18): MovePower (donors −min(step,
+ *      cap−floor), recipients +min(⌊F/|rec|⌋, ceiling−cap)), else MoveGPU of
+ *      the least-loaded donor (load[g], lowest id) + DistributeUniformPower
+ *      (clamp(B/N, min_w, max_w)) when the policy allows, the donor
+ *      role keeps >= 1 GPU and no role change is pending, else saturated.
+ *      Draining GPUs belong to neither pool (A26).  Policy masking S:323.
+ *   3. a move commands decreases at once (cmd), holds raises in
+ *      pending_raise_w, sets every GPU's settle_deadline_s = now_s + settle_s,
+ *      marks the MoveGPU donor draining, and sets last_move_s = now_s.
+ * Errors: EINVAL (null / n_gpus outside [2, 64] / role not 0/1 / bad policy),
+ * EMODEL (model), ERANGE (a cap outside [min_w, max_w]).                     */
 typedef struct {
-    uint8_t role[PADSIM_MAX_GPUS];      /* 0 prefill, 1 decode                  */
-    uint8_t draining[PADSIM_MAX_GPUS];  /* in neither pool (A26)                */
-    int32_t cmd_cap_w[PADSIM_MAX_GPUS]; /* commanded caps (targets)             */
+    uint8_t role[PADSIM_MAX_GPUS];         /* 0 prefill, 1 decode                      */
+    uint8_t draining[PADSIM_MAX_GPUS];     /* drain in progress: in neither pool (A26) */
+    int32_t cmd_cap_w[PADSIM_MAX_GPUS];    /* commanded caps                           */
+    int32_t eff_cap_w[PADSIM_MAX_GPUS];    /* effective caps (what the budget charges)  */
+    int32_t pending_raise_w[PADSIM_MAX_GPUS];  /* raise applied at the settle, 0 = none */
+    double settle_deadline_s[PADSIM_MAX_GPUS]; /* < 0: none                             */
+    double flip_deadline_s[PADSIM_MAX_GPUS];   /* < 0: none (set once the drain is done) */
     int32_t n_gpus;
-    int32_t drain_pending;              /* a role change is in progress         */
-    double last_move_s;                 /* Alg.1 last_move_time         */
+    double last_move_s;                    /* Alg. 1 last_move_time, 0 initially */
 } padsim_ctrl_state;
 typedef struct {
-    double ttft_stat_s, tpot_stat_s;    /* window p90 statistics (A22)          */
-    double ttft_slo_s, tpot_slo_s;      /* SLOs in effect               */
-    int32_t q_prefill;                  /* |Q_P| queued prompts         */
-    int32_t load[PADSIM_MAX_GPUS];      /* P: outstanding tokens, D: active+pending */
+    double ttft_stat_s, tpot_stat_s;       /* window p90 statistics (A22), 0 = empty   */
+    double ttft_slo_s, tpot_slo_s;         /* SLOs in effect                   */
+    double rate_p, rate_d;                 /* Alg. 1 inputs, unused by the guards (A21) */
+    int32_t q_prefill, q_decode;           /* |Q_P| queued prompts; |Q_D| (A21) */
+    int32_t load[PADSIM_MAX_GPUS];         /* P: outstanding tokens, D: active+pending  */
+    double drained_empty_s[PADSIM_MAX_GPUS];   /* draining GPU: when it became empty, else < 0 */
 } padsim_window_stats;
 typedef struct {
-    int32_t kind;                       /* 0 none, 1 move-power, 2 move-gpu, 3 saturated */
-    int32_t direction;                  /* 0 D->P, 1 P->D, -1 none              */
-    int32_t gpu;                        /* drained GPU (move-gpu) else -1       */
-    int32_t new_cap_w[PADSIM_MAX_GPUS]; /* caps once the move settles           */
+    int32_t kind;                          /* 0 none, 1 move-power, 2 move-gpu, 3 saturated */
+    int32_t direction;                     /* 0 D->P, 1 P->D, -1 none                 */
+    int32_t gpu;                           /* drained GPU (move-gpu) else -1           */
+    int32_t new_cap_w[PADSIM_MAX_GPUS];    /* targets once the move settles            */
 } padsim_action;
-int padsim_step_controller(padsim_ctx* ctx, const padsim_policy* policy,
-                           const padsim_budget* budget, const padsim_model* model,
-                           padsim_ctrl_state* inout, const padsim_window_stats* stats,
-                           double now_s, padsim_action* out);
+int padsim_step_controller(const padsim_policy* policy, const padsim_budget* budget,
+                           const padsim_model* model, padsim_ctrl_state* inout,
+                           const padsim_window_stats* stats, double now_s, padsim_action* out);
+
+/* The same Alg. 1 decision (step 2 only; no transitions, no state change) run
+ * on the device by the __device__ code the dynamic replay kernel uses
+ * (controller.cuh ctl_step): for parity tests of the kernel's controller
+ * against the host step.  Reads role, draining, cmd_cap_w, pending_raise_w,
+ * last_move_s of *state.  Synchronous on the context's stream.              */
+int padsim_controller_decide_device(padsim_ctx* ctx, const padsim_policy* policy,
+                                    const padsim_budget* budget, const padsim_model* model,
+                                    const padsim_ctrl_state* state, const padsim_window_stats* stats,
+                                    double now_s, padsim_action* out);
+
+/* ---- launch tuning (tests, ablations) ----------------------------------------
+ * padsim_set_tuning (before padsim_plan; kept until changed): overrides of the
+ * launch configuration the planner otherwise picks from the workload size.
+ * Results never depend on it (every variant is parity-tested); 0 / -1 = auto.
+ *   stage_a_threads      32, 128 or 256 threads per stage-A CTA
+ *   stage_c_classes      3 or 5 decode-pool classes
+ *   stage_c_batch_lists  bit k: class k uses sorted batch lists (-1 auto)
+ *   joint_threads        32 or 128 threads per joint-replay CTA
+ *   joint_reg_cap        1: the 168-register one-warp joint variant, 0: not (-1 auto)
+ *   joint_lanes_per_warp replays per warp item of the joint kernel (1..32)
+ *   joint_after_stage_a  1: joint replays wait for stage A (-1 auto)
+ *   serialize            1: padsim_run launches every kernel on its stream, one
+ *                        after another (per-kernel times in isolation, for the
+ *                        roofline), 0: concurrent streams (read at run time)      */
+typedef struct {
+    int32_t stage_a_threads, stage_c_classes, stage_c_batch_lists;
+    int32_t joint_threads, joint_reg_cap, joint_lanes_per_warp, joint_after_stage_a;
+    int32_t serialize;
+} padsim_tuning;
+int padsim_set_tuning(padsim_ctx* ctx, const padsim_tuning* tuning);
+
+/* Kernel launches issued by the last padsim_run (for the bench's launch count). */
+int padsim_launch_count(padsim_ctx* ctx, int32_t* n);
 
 /* ---- a1 candidate enumeration (host) ----------------------------------------
  * All pool-uniform (x, p, d): x ∈ [1, N−1] prefill GPUs at p W, N−x decode

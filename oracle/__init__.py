@@ -54,7 +54,7 @@ class Model(C.Structure):
 
 class Policy(C.Structure):
     _fields_ = [("kind", C.c_int32), ("threshold", C.c_int32), ("step_w", C.c_int32),
-                ("dec_ceiling_w", C.c_int32), ("cooldown_s", C.c_double), ("tick_s", C.c_double),
+                ("dec_ceiling_w", C.c_int32), ("window_stamp", C.c_int32), ("cooldown_s", C.c_double), ("tick_s", C.c_double),
                 ("window_s", C.c_double), ("settle_s", C.c_double), ("reassign_s", C.c_double)]
 
 
@@ -75,8 +75,19 @@ class LogRec(C.Structure):
                 ("b", C.c_int32)]
 
 
+class TickRec(C.Structure):
+    _fields_ = [("t", C.c_double), ("ttft_stat", C.c_double), ("tpot_stat", C.c_double),
+                ("ttft_slo", C.c_double), ("tpot_slo", C.c_double), ("q_prefill", C.c_int32),
+                ("kind", C.c_int32), ("direction", C.c_int32), ("gpu", C.c_int32),
+                ("load", C.c_int32 * MAX_GPUS), ("drained_empty", C.c_double * MAX_GPUS),
+                ("role", C.c_uint8 * MAX_GPUS), ("draining", C.c_uint8 * MAX_GPUS),
+                ("cmd", C.c_int32 * MAX_GPUS), ("eff", C.c_int32 * MAX_GPUS),
+                ("raise_to", C.c_int32 * MAX_GPUS), ("last_move", C.c_double)]
+
+
 class Log(C.Structure):
-    _fields_ = [("cap", C.c_int32), ("n", C.c_int32), ("recs", C.POINTER(LogRec))]
+    _fields_ = [("cap", C.c_int32), ("n", C.c_int32), ("recs", C.POINTER(LogRec)),
+                ("tcap", C.c_int32), ("tn", C.c_int32), ("ticks", C.POINTER(TickRec))]
 
 
 class CtlState(C.Structure):
@@ -129,7 +140,7 @@ def lib():
                                     _P(C.c_double), _P(Summary), _P(Log)]
             L.or_evaluate.restype = C.c_int
             L.or_evaluate.argtypes = [_P(Model), C.c_int32, C.c_int32, _P(C.c_uint8), _P(C.c_int32),
-                                      _P(Policy), C.c_int32, _P(Slo), C.c_int32, _P(C.c_int32),
+                                      _P(Policy), C.c_int32, _P(C.c_int32), _P(Slo), C.c_int32, _P(C.c_int32),
                                       _P(_P(C.c_double)), _P(_P(C.c_int32)), _P(_P(C.c_int32)),
                                       _P(_P(C.c_uint8)), C.c_int32, _P(C.c_double), C.c_int32,
                                       _P(C.c_int64), _P(C.c_double), _P(C.c_int64), _P(C.c_int32),
@@ -174,6 +185,7 @@ def make_policy(p: dict) -> Policy:
     P = Policy()
     for k in ("kind", "threshold", "step_w", "dec_ceiling_w"):
         setattr(P, k, int(p[k]))
+    P.window_stamp = int(p.get("window_stamp", 0))
     for k in ("cooldown_s", "tick_s", "window_s", "settle_s", "reassign_s"):
         setattr(P, k, float(p[k]))
     return P
@@ -244,7 +256,7 @@ def _trace_arrays(tr):
 
 
 def replay(model: dict, role, cap, policy: dict, budget_w: int, slo: dict, trace: dict,
-           qps_per_gpu: float, log_cap: int = 0):
+           qps_per_gpu: float, log_cap: int = 0, tick_cap: int = 0):
     """One replay; returns dict with per-request arrays, summary and log."""
     role = np.ascontiguousarray(role, dtype=np.uint8)
     cap = np.ascontiguousarray(cap, dtype=np.int32)
@@ -255,9 +267,12 @@ def replay(model: dict, role, cap, policy: dict, budget_w: int, slo: dict, trace
     sm = Summary()
     lg = None
     recs = None
-    if log_cap:
-        recs = (LogRec * log_cap)()
-        lg = Log(log_cap, 0, C.cast(recs, _P(LogRec)))
+    ticks = None
+    if log_cap or tick_cap:
+        recs = (LogRec * max(log_cap, 1))()
+        ticks = (TickRec * tick_cap)() if tick_cap else None
+        lg = Log(log_cap, 0, C.cast(recs, _P(LogRec)), tick_cap, 0,
+                 C.cast(ticks, _P(TickRec)) if ticks is not None else None)
     M, P, S = make_model(model), make_policy(policy), make_slo(slo)
     rc = lib().or_replay(C.byref(M), role.size, _ptr(role, C.c_uint8), _ptr(cap, C.c_int32),
                          C.byref(P), int(budget_w), C.byref(S), R, _ptr(s, C.c_double),
@@ -280,11 +295,21 @@ def replay(model: dict, role, cap, policy: dict, budget_w: int, slo: dict, trace
         n = min(lg.n, log_cap)
         res["log"] = [(recs[k].t, recs[k].type, recs[k].gpu, recs[k].a, recs[k].b) for k in range(n)]
         res["log_overflow"] = lg.n > log_cap
+        if ticks is not None:
+            n = len(role)
+            res["ticks"] = [dict(t=x.t, ttft_stat=x.ttft_stat, tpot_stat=x.tpot_stat, ttft_slo=x.ttft_slo,
+                                 tpot_slo=x.tpot_slo, q_prefill=x.q_prefill, kind=x.kind,
+                                 direction=x.direction, gpu=x.gpu, load=list(x.load[:n]),
+                                 drained_empty=list(x.drained_empty[:n]), role=list(x.role[:n]),
+                                 draining=list(x.draining[:n]), cmd=list(x.cmd[:n]), eff=list(x.eff[:n]),
+                                 raise_to=list(x.raise_to[:n]), last_move=x.last_move)
+                            for x in ticks[: min(lg.tn, tick_cap)]]
+            res["ticks_overflow"] = lg.tn > tick_cap
     return res
 
 
 def evaluate(model: dict, role, cap, policies, budget_w: int, slo: dict, traces, qps,
-             n_threads: int = 1, per_replay: bool = False):
+             n_threads: int = 1, per_replay: bool = False, cand_budget_w=None):
     """Full evaluation: candidates x QPS x traces. role/cap: [C][N]."""
     role = np.ascontiguousarray(role, dtype=np.uint8)
     cap = np.ascontiguousarray(cap, dtype=np.int32)
@@ -307,8 +332,9 @@ def evaluate(model: dict, role, cap, policies, budget_w: int, slo: dict, traces,
     rg = np.zeros((Cn, Q, S), np.float64) if per_replay else None
     rd = np.zeros((Cn, Q, S), np.float64) if per_replay else None
     M, SL = make_model(model), make_slo(slo)
+    cb = None if cand_budget_w is None else np.ascontiguousarray(cand_budget_w, dtype=np.int32)
     rc = lib().or_evaluate(C.byref(M), N, Cn, _ptr(role, C.c_uint8), _ptr(cap, C.c_int32), pols,
-                           int(budget_w), C.byref(SL), S, _ptr(nreq, C.c_int32), sp, ip, op, pp, Q,
+                           int(budget_w), _ptr(cb, C.c_int32) if cb is not None else None, C.byref(SL), S, _ptr(nreq, C.c_int32), sp, ip, op, pp, Q,
                            _ptr(qps, C.c_double), int(n_threads), _ptr(met, C.c_int64),
                            _ptr(good, C.c_double), _ptr(near, C.c_int64), _ptr(am, C.c_int32),
                            _ptr(rm, C.c_int32) if per_replay else None,

@@ -288,6 +288,7 @@ typedef struct {
     int* act_id; int* act_fin; int n_act; long ctx; long sum_join;
     ring_t pend; int step, step0; double t_seg, L, dL;
     int in_step, at_boundary, comp_changed, dirty;
+    double empty_at;      /* draining: the instant it became empty (flip at +reassign) */
 } wk_t;
 
 typedef struct { double* stamp; double* val; int n, lo; } samples_t;
@@ -569,6 +570,7 @@ int or_replay(const or_model* m, int32_t N, const uint8_t* role, const int32_t* 
         if (!(pol->tick_s > 0 && pol->settle_s > 0 && pol->reassign_s > 0 &&
               pol->cooldown_s >= pol->settle_s && pol->window_s >= 0 && pol->step_w > 0 &&
               pol->threshold >= 0 && pol->dec_ceiling_w >= m->min_w &&
+              (pol->window_stamp == 0 || pol->window_stamp == 1) &&
               pol->dec_ceiling_w <= m->max_w && (long)N * m->min_w <= B)) return -1;
     }
     for (int i = 0; i < R; i++) {
@@ -637,7 +639,9 @@ int or_replay(const or_model* m, int32_t N, const uint8_t* role, const int32_t* 
     }
 
 #define COMPLETE(ID, T, TP) do { int id_ = (ID); comp[id_] = (T); tpot[id_] = (TP); done[id_] = 1; \
-        completed++; s_tpot.stamp[s_tpot.n] = (T); s_tpot.val[s_tpot.n] = (TP); s_tpot.n++; } while (0)
+        completed++; s_tpot.stamp[s_tpot.n] = (T); s_tpot.val[s_tpot.n] = (TP); s_tpot.n++; \
+        if (pol->window_stamp) {   /* TTFT sampled at completion */ \
+            s_ttft.stamp[s_ttft.n] = (T); s_ttft.val[s_ttft.n] = pe[id_] - a[id_]; s_ttft.n++; } } while (0)
 
     while (completed < R) {
         if (h.n == 0) { rc = -9; goto out; }     /* cannot happen: progress guaranteed */
@@ -697,7 +701,9 @@ int or_replay(const or_model* m, int32_t N, const uint8_t* role, const int32_t* 
                     int i = w->batch[k];
                     pe[i] = t;
                     w->outstanding -= in_tok[i];
-                    s_ttft.stamp[s_ttft.n] = t; s_ttft.val[s_ttft.n] = t - a[i]; s_ttft.n++;
+                    if (!pol->window_stamp) {      /* A22: TTFT known at the first token */
+                        s_ttft.stamp[s_ttft.n] = t; s_ttft.val[s_ttft.n] = t - a[i]; s_ttft.n++;
+                    }
                     if (tbusy < m->slots) {
                         tbusy++;
                         te[i] = t + or_kv_lat(m, in_tok[i]);
@@ -809,6 +815,18 @@ int or_replay(const or_model* m, int32_t N, const uint8_t* role, const int32_t* 
                 ob.ttft_slo = slo->ttft;
                 ob.tpot_slo = phase2_seen ? slo->tpot[1] : slo->tpot[0];
                 or_step_controller(pol, m, B, &st, &ob, t, &act);
+                or_tick_rec* tr_ = (lg && lg->ticks && lg->tn < lg->tcap) ? &lg->ticks[lg->tn] : NULL;
+                if (lg && lg->ticks) lg->tn++;
+                if (tr_) {
+                    memset(tr_, 0, sizeof(*tr_));
+                    tr_->t = t; tr_->ttft_stat = ttft_stat; tr_->tpot_stat = tpot_stat;
+                    tr_->ttft_slo = ob.ttft_slo; tr_->tpot_slo = ob.tpot_slo; tr_->q_prefill = ob.q_prefill;
+                    tr_->kind = act.kind; tr_->direction = act.direction; tr_->gpu = act.gpu;
+                    for (int g = 0; g < N; g++) {
+                        tr_->load[g] = ob.load[g];
+                        tr_->drained_empty[g] = (W[g].draining && W[g].flip_sched) ? W[g].empty_at : -1.0;
+                    }
+                }
                 if (act.kind == 1 || act.kind == 2) {
                     last_move = st.last_move;
                     if (act.kind == 2) {
@@ -863,6 +881,13 @@ int or_replay(const or_model* m, int32_t N, const uint8_t* role, const int32_t* 
                 } else if (act.kind == 3) {
                     sum->n_saturated++;
                     log_put(lg, t, OR_LOG_SATURATED, -1, act.direction, 0);
+                }
+                if (tr_) {
+                    for (int g = 0; g < N; g++) {
+                        tr_->role[g] = (uint8_t)W[g].role; tr_->draining[g] = (uint8_t)W[g].draining;
+                        tr_->cmd[g] = W[g].cmd; tr_->eff[g] = W[g].eff; tr_->raise_to[g] = W[g].raise_to;
+                    }
+                    tr_->last_move = last_move;
                 }
                 tick_k++;
                 if (heap_push(&h, (double)tick_k * pol->tick_s, K_TICK, 0)) goto out;
@@ -934,6 +959,7 @@ int or_replay(const or_model* m, int32_t N, const uint8_t* role, const int32_t* 
                                      : (w->n_act == 0 && w->pend.len == 0 && !w->in_step);
             if (empty) {
                 w->flip_sched = 1;
+                w->empty_at = t;
                 if (heap_push(&h, t + pol->reassign_s, K_FLIP, g)) goto out;
             }
         }
@@ -1003,7 +1029,7 @@ int or_met_for_slos(int32_t R, const double* ttft, const double* tpot, const uin
 /* ------------------------------------------------------------------------ */
 typedef struct {
     const or_model* m; int32_t N, C, S, Q; const uint8_t* role; const int32_t* cap;
-    const or_policy* pol; int32_t B; const or_slo* slo; const int32_t* n_req;
+    const or_policy* pol; int32_t B; const int32_t* cand_B; const or_slo* slo; const int32_t* n_req;
     const double* const* s_unit; const int32_t* const* in_tok; const int32_t* const* out_tok;
     const uint8_t* const* phase; const double* qps;
     int32_t* r_met; int32_t* r_near; double* r_good; double* r_dur;
@@ -1023,7 +1049,7 @@ static void* worker_main(void* arg) {
         int c = (int)(r / ((long)J->S * J->Q));
         or_summary sm;
         int rc = or_replay(J->m, J->N, J->role + (size_t)c * J->N, J->cap + (size_t)c * J->N,
-                           &J->pol[c], J->B, J->slo, J->n_req[s], J->s_unit[s], J->in_tok[s],
+                           &J->pol[c], J->cand_B ? J->cand_B[c] : J->B, J->slo, J->n_req[s], J->s_unit[s], J->in_tok[s],
                            J->out_tok[s], J->phase[s], J->qps[q], NULL, NULL, NULL, NULL, NULL,
                            NULL, &sm, NULL);
         if (rc) { J->err = rc; continue; }
@@ -1036,8 +1062,8 @@ static void* worker_main(void* arg) {
 }
 
 int or_evaluate(const or_model* m, int32_t N, int32_t C, const uint8_t* role,
-                const int32_t* cap, const or_policy* pol, int32_t B, const or_slo* slo,
-                int32_t S, const int32_t* n_req, const double* const* s_unit,
+                const int32_t* cap, const or_policy* pol, int32_t B, const int32_t* cand_B,
+                const or_slo* slo, int32_t S, const int32_t* n_req, const double* const* s_unit,
                 const int32_t* const* in_tok, const int32_t* const* out_tok,
                 const uint8_t* const* phase, int32_t Q, const double* qps,
                 int32_t n_threads, int64_t* met, double* goodput, int64_t* near_boundary,
@@ -1047,7 +1073,7 @@ int or_evaluate(const or_model* m, int32_t N, int32_t C, const uint8_t* role,
     job_t J;
     memset(&J, 0, sizeof J);
     J.m = m; J.N = N; J.C = C; J.S = S; J.Q = Q; J.role = role; J.cap = cap; J.pol = pol;
-    J.B = B; J.slo = slo; J.n_req = n_req; J.s_unit = s_unit; J.in_tok = in_tok;
+    J.B = B; J.cand_B = cand_B; J.slo = slo; J.n_req = n_req; J.s_unit = s_unit; J.in_tok = in_tok;
     J.out_tok = out_tok; J.phase = phase; J.qps = qps;
     J.r_met = (int32_t*)malloc(sizeof(int32_t) * (size_t)total);
     J.r_near = (int32_t*)malloc(sizeof(int32_t) * (size_t)total);

@@ -52,6 +52,8 @@ typedef struct {
     int32_t threshold;    /* Alg.1 THRESHOLD on |Q_P|                        */
     int32_t step_w;       /* MovePower step (W)                              */
     int32_t dec_ceiling_w;/* decode dynamic ceiling (600 W)           */
+    int32_t window_stamp; /* TTFT window samples stamped at 0: first token
+                             (A22), 1: completion        */
     double cooldown_s, tick_s, window_s, settle_s, reassign_s;
 } or_policy;
 
@@ -73,7 +75,19 @@ enum { OR_LOG_MOVE_POWER = 1, OR_LOG_MOVE_GPU = 2, OR_LOG_SATURATED = 3,
        OR_LOG_SETTLE = 4, OR_LOG_FLIP = 5, OR_LOG_BUDGET = 6, OR_LOG_ROLES = 7,
        OR_LOG_CAPS = 8 };
 typedef struct { double t; int32_t type, gpu, a, b; } or_log_rec;
-typedef struct { int32_t cap; int32_t n; or_log_rec* recs; } or_log;
+/* one controller tick: what Alg. 1 saw (window statistics, |Q_P|, per-GPU
+ * load, drain-completion times), what it decided, and the node state after
+ * the tick (for the host step_controller parity test)                       */
+typedef struct {
+    double t, ttft_stat, tpot_stat, ttft_slo, tpot_slo;
+    int32_t q_prefill, kind, direction, gpu;
+    int32_t load[OR_MAX_GPUS];
+    double drained_empty[OR_MAX_GPUS];     /* draining GPU emptied at, else -1 */
+    uint8_t role[OR_MAX_GPUS], draining[OR_MAX_GPUS];
+    int32_t cmd[OR_MAX_GPUS], eff[OR_MAX_GPUS], raise_to[OR_MAX_GPUS];
+    double last_move;
+} or_tick_rec;
+typedef struct { int32_t cap; int32_t n; or_log_rec* recs; int32_t tcap; int32_t tn; or_tick_rec* ticks; } or_log;
 
 /* model functions (c.1) */
 double or_speedup(const or_curve* c, int32_t w);
@@ -98,8 +112,9 @@ int or_replay(const or_model* m, int32_t n_gpus, const uint8_t* role, const int3
  * (Σmet desc, Σcaps asc, index asc) (c.4).  Optional per-replay outputs
  * indexed [(c*n_qps + q)*n_traces + s].                                      */
 int or_evaluate(const or_model* m, int32_t n_gpus, int32_t n_cand, const uint8_t* role,
-                const int32_t* cap, const or_policy* pol, int32_t budget_w, const or_slo* slo,
-                int32_t n_traces, const int32_t* n_req, const double* const* s_unit,
+                const int32_t* cap, const or_policy* pol, int32_t budget_w,
+                const int32_t* cand_budget_w /* nullable: per-candidate budgets [n_cand] */,
+                const or_slo* slo, int32_t n_traces, const int32_t* n_req, const double* const* s_unit,
                 const int32_t* const* in_tok, const int32_t* const* out_tok,
                 const uint8_t* const* phase, int32_t n_qps, const double* qps,
                 int32_t n_threads, int64_t* met, double* goodput, int64_t* near_boundary,

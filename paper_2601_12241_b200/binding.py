@@ -54,7 +54,8 @@ class Model(C.Structure):
 
 class Policy(C.Structure):
     _fields_ = [("kind", C.c_int32), ("queue_threshold", C.c_int32), ("power_step_w", C.c_int32),
-                ("decode_ceiling_w", C.c_int32), ("cooldown_s", C.c_double), ("tick_s", C.c_double),
+                ("decode_ceiling_w", C.c_int32), ("window_stamp", C.c_int32), ("cooldown_s", C.c_double),
+                ("tick_s", C.c_double),
                 ("window_s", C.c_double), ("settle_s", C.c_double), ("reassign_s", C.c_double)]
 
 
@@ -68,7 +69,7 @@ class Slo(C.Structure):
 
 
 class Budget(C.Structure):
-    _fields_ = [("budget_w", C.c_int32)]
+    _fields_ = [("budget_w", C.c_int32), ("cand_budget_w", C.POINTER(C.c_int32))]
 
 
 class Result(C.Structure):
@@ -87,14 +88,28 @@ class DeviceResults(C.Structure):
 
 class CtrlState(C.Structure):
     _fields_ = [("role", C.c_uint8 * MAX_GPUS), ("draining", C.c_uint8 * MAX_GPUS),
-                ("cmd_cap_w", C.c_int32 * MAX_GPUS), ("n_gpus", C.c_int32),
-                ("drain_pending", C.c_int32), ("last_move_s", C.c_double)]
+                ("cmd_cap_w", C.c_int32 * MAX_GPUS), ("eff_cap_w", C.c_int32 * MAX_GPUS),
+                ("pending_raise_w", C.c_int32 * MAX_GPUS), ("settle_deadline_s", C.c_double * MAX_GPUS),
+                ("flip_deadline_s", C.c_double * MAX_GPUS), ("n_gpus", C.c_int32),
+                ("last_move_s", C.c_double)]
 
 
 class WindowStats(C.Structure):
     _fields_ = [("ttft_stat_s", C.c_double), ("tpot_stat_s", C.c_double),
-                ("ttft_slo_s", C.c_double), ("tpot_slo_s", C.c_double), ("q_prefill", C.c_int32),
-                ("load", C.c_int32 * MAX_GPUS)]
+                ("ttft_slo_s", C.c_double), ("tpot_slo_s", C.c_double), ("rate_p", C.c_double),
+                ("rate_d", C.c_double), ("q_prefill", C.c_int32), ("q_decode", C.c_int32),
+                ("load", C.c_int32 * MAX_GPUS), ("drained_empty_s", C.c_double * MAX_GPUS)]
+
+
+class Tuning(C.Structure):
+    _fields_ = [("stage_a_threads", C.c_int32), ("stage_c_classes", C.c_int32),
+                ("stage_c_batch_lists", C.c_int32), ("joint_threads", C.c_int32),
+                ("joint_reg_cap", C.c_int32), ("joint_lanes_per_warp", C.c_int32),
+                ("joint_after_stage_a", C.c_int32), ("serialize", C.c_int32)]
+
+
+TUNING_AUTO = dict(stage_a_threads=0, stage_c_classes=0, stage_c_batch_lists=-1, joint_threads=0,
+                   joint_reg_cap=-1, joint_lanes_per_warp=0, joint_after_stage_a=-1, serialize=0)
 
 
 class Action(C.Structure):
@@ -105,7 +120,8 @@ class Action(C.Structure):
 EXPORTS = ["padsim_create", "padsim_destroy", "padsim_last_error", "padsim_version",
            "padsim_evaluate_allocations", "padsim_plan", "padsim_run", "padsim_fetch",
            "padsim_get_device_results", "padsim_fetch_replays", "padsim_fetch_records",
-           "padsim_argmax_device", "padsim_step_controller", "padsim_enumerate_pool_uniform",
+           "padsim_argmax_device", "padsim_step_controller", "padsim_controller_decide_device",
+           "padsim_set_tuning", "padsim_launch_count", "padsim_enumerate_pool_uniform",
            "padsim_replay_kernel_ms", "padsim_kernel_times_ms", "padsim_set_slo_sweep",
            "padsim_fetch_extras", "padsim_fetch_decomposition", "padsim_fetch_percentiles"]
 
@@ -122,7 +138,7 @@ def load(path: str = LIB_PATH):
         raise PadsimError(-7, f"{path} not built: run paper_2601_12241_b200.build.build()")
     L = C.CDLL(path)
     vp = C.c_void_p
-    L.padsim_create.argtypes = [C.c_int32, _P(vp)]
+    L.padsim_create.argtypes = [C.c_int32, vp, _P(vp)]
     L.padsim_destroy.argtypes = [vp]
     L.padsim_destroy.restype = None
     L.padsim_last_error.argtypes = [vp]
@@ -146,9 +162,13 @@ def load(path: str = LIB_PATH):
     L.padsim_fetch_records.argtypes = [vp, vp] + [_P(C.c_double)] * 5 + [_P(C.c_int32)]
     L.padsim_fetch_decomposition.argtypes = [vp, vp] + [_P(C.c_double)] * 4
     L.padsim_fetch_percentiles.argtypes = [vp, vp, _P(C.c_int32), C.c_int32, _P(C.c_double)]
-    L.padsim_argmax_device.argtypes = [vp, vp, vp, C.c_int32, C.c_int32, vp]
-    L.padsim_step_controller.argtypes = [vp, _P(Policy), _P(Budget), _P(Model), _P(CtrlState),
+    L.padsim_argmax_device.argtypes = [vp, vp, vp, vp, C.c_int32, C.c_int32, vp]
+    L.padsim_step_controller.argtypes = [_P(Policy), _P(Budget), _P(Model), _P(CtrlState),
                                          _P(WindowStats), C.c_double, _P(Action)]
+    L.padsim_controller_decide_device.argtypes = [vp, _P(Policy), _P(Budget), _P(Model), _P(CtrlState),
+                                                  _P(WindowStats), C.c_double, _P(Action)]
+    L.padsim_set_tuning.argtypes = [vp, _P(Tuning)]
+    L.padsim_launch_count.argtypes = [vp, _P(C.c_int32)]
     L.padsim_enumerate_pool_uniform.argtypes = [C.c_int32] * 6 + [_P(C.c_int32), C.c_int32,
                                                                   _P(C.c_int32)]
     _lib = L
@@ -186,6 +206,7 @@ def make_policy(p: dict) -> Policy:
     P = Policy()
     P.kind, P.queue_threshold = int(p["kind"]), int(p["threshold"])
     P.power_step_w, P.decode_ceiling_w = int(p["step_w"]), int(p["dec_ceiling_w"])
+    P.window_stamp = int(p.get("window_stamp", 0))
     P.cooldown_s, P.tick_s, P.window_s = float(p["cooldown_s"]), float(p["tick_s"]), float(p["window_s"])
     P.settle_s, P.reassign_s = float(p["settle_s"]), float(p["reassign_s"])
     return P
@@ -200,6 +221,18 @@ def make_slo(s: dict) -> Slo:
 
 def _p(a, ct):
     return a.ctypes.data_as(_P(ct))
+
+
+def make_budget(budget_w, cand_budget_w=None, keep=None) -> Budget:
+    """padsim_budget: the node budget, or one budget per candidate."""
+    if cand_budget_w is None:
+        return Budget(int(budget_w), None)
+    cb = np.ascontiguousarray(cand_budget_w, dtype=np.int32)
+    if keep is not None:
+        keep.objs.append(cb)
+    b = Budget(int(budget_w), _p(cb, C.c_int32))
+    b._cb = cb                                  # keep the array alive with the struct
+    return b
 
 
 class _Keep:
@@ -241,14 +274,38 @@ def make_candidates(role, cap, policies, keep: _Keep):
 class Context:
     """One padsim_ctx bound to a CUDA device."""
 
-    def __init__(self, device: int = 0):
+    def __init__(self, device: int = 0, stream=None, tuning: dict | None = None):
         self.L = load()
         self.ptr = C.c_void_p()
-        rc = self.L.padsim_create(int(device), C.byref(self.ptr))
+        rc = self.L.padsim_create(int(device), C.c_void_p(stream or 0), C.byref(self.ptr))
         if rc != 0:
             raise PadsimError(rc, "padsim_create (no CUDA device?)")
         self.shape = None
         self._keep = None
+        self.n_sweep = 0
+        if tuning:
+            self.set_tuning(tuning)
+
+    def set_tuning(self, tuning: dict | None):
+        """Launch-configuration overrides (padsim_set_tuning); results never depend on them."""
+        t = dict(TUNING_AUTO, **(tuning or {}))
+        self._check(self.L.padsim_set_tuning(self.ptr, C.byref(Tuning(**t))), "set_tuning")
+
+    def launch_count(self) -> int:
+        n = C.c_int32(0)
+        self._check(self.L.padsim_launch_count(self.ptr, C.byref(n)), "launch_count")
+        return int(n.value)
+
+    def decide_device(self, policy: dict, model: dict, budget_w: int, state: dict, stats: dict, now: float):
+        """padsim_controller_decide_device: the kernel's Alg. 1 decision (no state change)."""
+        st, ws = _ctrl_structs(state, stats)
+        act = Action()
+        self._check(self.L.padsim_controller_decide_device(
+            self.ptr, C.byref(make_policy(policy)), C.byref(make_budget(budget_w)), C.byref(make_model(model)),
+            C.byref(st), C.byref(ws), float(now), C.byref(act)), "controller_decide_device")
+        n = st.n_gpus
+        return dict(kind=act.kind, direction=act.direction, gpu=act.gpu,
+                    new_cap=[act.new_cap_w[g] for g in range(n)])
 
     def close(self):
         if self.ptr:
@@ -267,15 +324,16 @@ class Context:
             raise PadsimError(rc, f"{what}: {msg.decode() if msg else ''}")
 
     def plan(self, traces, qps, model, role, cap, policies, slo, budget_w, records=False,
-             joint=False):
+             joint=False, cand_budget_w=None):
         keep = _Keep()
         tr = make_traces(traces, keep)
         q = keep.arr(qps, np.float64)
         cands = make_candidates(role, cap, policies, keep)
         bad = C.c_int32(-1)
+        self.n_sweep = 0                           # padsim_plan clears the SLO sweep
         rc = self.L.padsim_plan(self.ptr, tr, len(traces), _p(q, C.c_double), q.size,
                                 C.byref(make_model(model)), C.byref(cands), C.byref(make_slo(slo)),
-                                C.byref(Budget(int(budget_w))),
+                                C.byref(make_budget(budget_w, cand_budget_w, keep)),
                                 (RECORDS if records else 0) | (JOINT if joint else 0), C.byref(bad))
         if rc != 0:
             e = PadsimError(rc, self.L.padsim_last_error(self.ptr).decode())
@@ -381,43 +439,73 @@ class Context:
         self._check(self.L.padsim_get_device_results(self.ptr, C.byref(d)), "device_results")
         return d
 
-    def argmax_device(self, d_met_ptr: int, n_cand: int, n_qps: int, d_argmax_ptr: int, stream=None):
+    def argmax_device(self, d_met_ptr: int, n_cand: int, n_qps: int, d_argmax_ptr: int, stream=None,
+                      d_capsum_ptr: int | None = None):
+        """Argmax kernel on a device met array [n_cand, n_qps] (d_capsum_ptr: device
+        int32 Σcaps per candidate; None = the planned candidates')."""
         self._check(self.L.padsim_argmax_device(self.ptr, C.c_void_p(stream or 0), C.c_void_p(d_met_ptr),
-                                                n_cand, n_qps, C.c_void_p(d_argmax_ptr)), "argmax")
+                                                C.c_void_p(d_capsum_ptr or 0), n_cand, n_qps,
+                                                C.c_void_p(d_argmax_ptr)), "argmax")
 
-    def step_controller(self, policy: dict, model: dict, budget_w: int, state: dict, stats: dict,
-                        now: float):
-        n = len(state["role"])
-        st = CtrlState()
-        st.n_gpus = n
-        for g in range(n):
-            st.role[g] = int(state["role"][g])
-            st.draining[g] = int(state.get("draining", [0] * n)[g])
-            st.cmd_cap_w[g] = int(state["cmd"][g])
-        st.drain_pending = int(state.get("drain_pending", 0))
-        st.last_move_s = float(state.get("last_move", 0.0))
-        ws = WindowStats()
-        ws.ttft_stat_s, ws.tpot_stat_s = float(stats["ttft_stat"]), float(stats["tpot_stat"])
-        ws.ttft_slo_s, ws.tpot_slo_s = float(stats["ttft_slo"]), float(stats["tpot_slo"])
-        ws.q_prefill = int(stats.get("q_prefill", 0))
-        for g, l in enumerate(stats.get("load", [0] * n)):
-            ws.load[g] = int(l)
-        act = Action()
-        self._check(self.L.padsim_step_controller(
-            self.ptr, C.byref(make_policy(policy)), C.byref(Budget(int(budget_w))),
-            C.byref(make_model(model)), C.byref(st), C.byref(ws), float(now), C.byref(act)),
-            "step_controller")
-        a = dict(kind=act.kind, direction=act.direction, gpu=act.gpu,
-                 new_cap=[act.new_cap_w[g] for g in range(n)])
-        s = dict(role=[st.role[g] for g in range(n)], draining=[st.draining[g] for g in range(n)],
-                 cmd=[st.cmd_cap_w[g] for g in range(n)], drain_pending=st.drain_pending,
-                 last_move=st.last_move_s)
-        return a, s
+
+
+def _ctrl_structs(state: dict, stats: dict):
+    n = len(state["role"])
+    st = CtrlState()
+    st.n_gpus = n
+    for g in range(n):
+        st.role[g] = int(state["role"][g])
+        st.draining[g] = int(state.get("draining", [0] * n)[g])
+        st.cmd_cap_w[g] = int(state["cmd"][g])
+        st.eff_cap_w[g] = int(state.get("eff", state["cmd"])[g])
+        st.pending_raise_w[g] = int(state.get("raise", [0] * n)[g])
+        st.settle_deadline_s[g] = float(state.get("settle_deadline", [-1.0] * n)[g])
+        st.flip_deadline_s[g] = float(state.get("flip_deadline", [-1.0] * n)[g])
+    st.last_move_s = float(state.get("last_move", 0.0))
+    ws = WindowStats()
+    ws.ttft_stat_s, ws.tpot_stat_s = float(stats["ttft_stat"]), float(stats["tpot_stat"])
+    ws.ttft_slo_s, ws.tpot_slo_s = float(stats["ttft_slo"]), float(stats["tpot_slo"])
+    ws.q_prefill = int(stats.get("q_prefill", 0))
+    for g, l in enumerate(stats.get("load", [0] * n)):
+        ws.load[g] = int(l)
+    for g in range(MAX_GPUS):
+        ws.drained_empty_s[g] = -1.0
+    for g, e in enumerate(stats.get("drained_empty", [-1.0] * n)):
+        ws.drained_empty_s[g] = float(e)
+    return st, ws
+
+
+def step_controller(policy: dict, model: dict, budget_w: int, state: dict, stats: dict, now: float):
+    """padsim_step_controller — pure host Alg. 1 step on the full node state.
+
+    state: role, cmd, eff, raise, settle_deadline, flip_deadline, draining, last_move
+    (lists of n_gpus; missing optional keys default to no pending transition).
+    Returns (action dict, new state dict)."""
+    L = load()
+    st, ws = _ctrl_structs(state, stats)
+    act = Action()
+    rc = L.padsim_step_controller(C.byref(make_policy(policy)), C.byref(make_budget(budget_w)),
+                                  C.byref(make_model(model)), C.byref(st), C.byref(ws), float(now),
+                                  C.byref(act))
+    if rc != 0:
+        raise PadsimError(rc, "padsim_step_controller")
+    n = st.n_gpus
+    a = dict(kind=act.kind, direction=act.direction, gpu=act.gpu, new_cap=[act.new_cap_w[g] for g in range(n)])
+    s = dict(role=[st.role[g] for g in range(n)], draining=[st.draining[g] for g in range(n)],
+             cmd=[st.cmd_cap_w[g] for g in range(n)], eff=[st.eff_cap_w[g] for g in range(n)],
+             raise_=[st.pending_raise_w[g] for g in range(n)],
+             settle_deadline=[st.settle_deadline_s[g] for g in range(n)],
+             flip_deadline=[st.flip_deadline_s[g] for g in range(n)], last_move=st.last_move_s)
+    s["raise"] = s.pop("raise_")
+    return a, s
 
 
 def evaluate_allocations(traces, qps, model, role, cap, policies, slo, budget_w, device=0,
-                         ctx: Context | None = None):
-    """One-shot padsim_evaluate_allocations (host buffers in, host results out)."""
+                         ctx: Context | None = None, cand_budget_w=None):
+    """One-shot padsim_evaluate_allocations (host buffers in, host results out).
+
+    With ``ctx`` the call re-plans that context: its shape / kept arrays are
+    updated so later fetch* calls on it size their buffers from this plan."""
     own = ctx is None
     ctx = ctx or Context(device)
     keep = _Keep()
@@ -432,8 +520,13 @@ def evaluate_allocations(traces, qps, model, role, cap, policies, slo, budget_w,
     res = Result(_p(met, C.c_int64), _p(good, C.c_double), _p(near, C.c_int64), _p(am, C.c_int32), -1)
     rc = ctx.L.padsim_evaluate_allocations(ctx.ptr, tr, len(traces), _p(q, C.c_double), Q,
                                            C.byref(make_model(model)), C.byref(cands),
-                                           C.byref(make_slo(slo)), C.byref(Budget(int(budget_w))),
+                                           C.byref(make_slo(slo)),
+                                           C.byref(make_budget(budget_w, cand_budget_w, keep)),
                                            C.byref(res))
+    if not own:                        # the context now holds this plan
+        ctx.shape = (Cn, Q, len(traces), max([t["s_unit"].size for t in traces] + [0]))
+        ctx._keep = keep
+        ctx.n_sweep = 0
     try:
         if rc != 0:
             e = PadsimError(rc, ctx.L.padsim_last_error(ctx.ptr).decode())

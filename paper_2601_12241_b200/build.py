@@ -20,6 +20,7 @@ FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-li
 
 def _sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cuh")) +
+                  glob.glob(os.path.join(CSRC, "*.cpp")) +
                   [os.path.join(ROOT, "include", "padsim.h")])
 
 
@@ -33,7 +34,9 @@ def needs_build() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
-    cmd = [NVCC, *FLAGS, "-o", LIB + ".tmp", os.path.join(CSRC, "padsim.cu")]
+    # the host controller step (controller_host.cpp) is plain C++, compiled on its own
+    cmd = [NVCC, *FLAGS, "-o", LIB + ".tmp", os.path.join(CSRC, "padsim.cu"),
+           os.path.join(CSRC, "controller_host.cpp")]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd))

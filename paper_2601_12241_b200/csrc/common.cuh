@@ -84,7 +84,8 @@ __device__ __forceinline__ int seg_first_ge(double ts0, double L, double dL, int
 // Everything a replay kernel launch needs (passed by value as a kernel param).
 struct Plan {
     DevModel m;
-    int N, C, Q, S, Rmax, B;
+    int N, C, Q, S, Rmax;
+    const int* cbud;                   // [C] node budget per candidate (padsim_budget)
     // traces: SoA, trace s occupies [toff[s], toff[s]+nreq[s]); toff multiple of 16
     const long long* toff;
     const int* nreq;

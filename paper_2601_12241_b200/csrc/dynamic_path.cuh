@@ -257,6 +257,7 @@ struct JReplay {
     long long rec_base;
     // dynamic
     padsim_policy pol;
+    int Bc;              // this candidate's node budget (DistributeUniformPower)
     double tick_t, settle_t, flip_t, last_move;
     long long tick_k;
     int flip_g, drain_pending, phase2;
@@ -299,6 +300,14 @@ struct JReplay {
         for (int z = 0; z < nk; z++) {
             const double tz = T.phase[i] ? P.sw.tpot1[z] : P.sw.tpot0[z];
             if (ttft <= P.sw.ttft[z] && tpot <= tz) metk[z]++;
+        }
+        if (DYN && pol.window_stamp) {       // TTFT sampled at completion
+            const unsigned char f = (ttft <= P.ttft_slo ? 1 : 0) | (ttft < P.ttft_slo ? 2 : 0);
+            wts[w_th] = t;
+            wtf[w_th] = f;
+            w_th++;
+            w_tle += f & 1;
+            w_tlt += f >> 1;
         }
         if (DYN) {
             const unsigned char f = (tpot <= P.tpot_slo0 ? 1 : 0) | (tpot < P.tpot_slo0 ? 2 : 0) |
@@ -363,7 +372,7 @@ struct JReplay {
             dec += T.in_tok[i];
             bq = bq + (bstart - arr(i));
             be = be + (t - bstart);
-            if (DYN) {
+            if (DYN && !pol.window_stamp) {   // A22: TTFT known at the first token
                 const double ttft = t - arr(i);
                 const unsigned char f = (ttft <= P.ttft_slo ? 1 : 0) | (ttft < P.ttft_slo ? 2 : 0);
                 wts[w_th] = t;
@@ -679,7 +688,7 @@ struct JReplay {
             int newcap[NG];
             int gsel, dir;
             JCtlView<Mask> view{&W, pmask, ws};
-            const int act = ctl_step(pol, P.m.min_w, P.m.max_w, P.B, N, view, drain_pending != 0,
+            const int act = ctl_step(pol, P.m.min_w, P.m.max_w, Bc, N, view, drain_pending != 0,
                                      last_move, t, sg, newcap, &gsel, &dir);
             if (act == ACT_MOVE_POWER || act == ACT_MOVE_GPU) {
                 last_move = t;
@@ -804,6 +813,7 @@ struct JReplay {
         maxcomp = -PAD_INF;
         if (DYN) {
             pol = P.pol[c];
+            Bc = P.cbud[c];
             tick_k = 1;
             tick_t = (double)tick_k * pol.tick_s;
             settle_t = flip_t = PAD_INF;

@@ -30,11 +30,14 @@ using namespace padsim;
 struct padsim_ctx {
     int device = 0;
     int n_sm = 0;
+    cudaStream_t stream = nullptr;   // stream of the one-shot API (padsim_create)
+    padsim_tuning tune{0, 0, -1, 0, -1, 0, -1, 0};   // launch overrides (padsim_set_tuning)
+    int n_launches = 0;              // kernels launched by the last padsim_run
     std::string err;
     // plan
     bool planned = false;
     uint32_t flags = 0;
-    int N = 0, C = 0, Q = 0, S = 0, Rmax = 0, B = 0;
+    int N = 0, C = 0, Q = 0, S = 0, Rmax = 0;
     padsim_model model{};
     padsim_slo slo{};
     std::vector<int> static_list, dyn_list, coal_list;
@@ -56,6 +59,7 @@ struct padsim_ctx {
     unsigned char* d_role = nullptr;
     int* d_cap = nullptr;
     int* d_capsum = nullptr;
+    int* d_cbud = nullptr;           // [C] per-candidate node budget (padsim_budget)
     padsim_policy* d_pol = nullptr;
     double* d_qps = nullptr;
     int* d_clist_static = nullptr;
@@ -101,6 +105,7 @@ struct padsim_ctx {
     size_t smem_static = 0, smem_dyn = 0;
     // host staging for the one-shot API
     padsim_ctrl_state* d_ctl_state = nullptr;
+    padsim_window_stats* d_ctl_stats = nullptr;
     padsim_action* d_ctl_act = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, evA = nullptr, evC = nullptr;
     cudaEvent_t evJ0 = nullptr, evJ1 = nullptr;
@@ -367,49 +372,45 @@ __global__ void argmax_kernel(const long long* met, const int* capsum, int C, in
 }
 
 // ---------------------------------------------------------------------------
-// row a6 ABI: one controller step on the device (same ctl_step as the replay)
+// row a6: the Alg. 1 decision on the device (same ctl_step as the replay
+// kernel), for parity of the kernel's controller with padsim_step_controller
 // ---------------------------------------------------------------------------
 struct AbiView {
     const padsim_ctrl_state* st;
     const padsim_window_stats* ws;
     __device__ int role(int g) const { return st->role[g]; }
     __device__ bool draining(int g) const { return st->draining[g] != 0; }
-    __device__ int target(int g) const { return st->cmd_cap_w[g]; }
+    __device__ int target(int g) const {
+        return st->pending_raise_w[g] > 0 ? st->pending_raise_w[g] : st->cmd_cap_w[g];
+    }
     __device__ long long load(int g) const { return ws->load[g]; }
 };
 
 __global__ void controller_kernel(const padsim_policy pol, const int min_w, const int max_w,
-                                  const int budget, padsim_ctrl_state* st,
-                                  const padsim_window_stats ws, const double now,
+                                  const int budget, const padsim_ctrl_state* st,
+                                  const padsim_window_stats* ws, const double now,
                                   padsim_action* act) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     CtlSignals sg;
-    sg.ttft_gt = ws.ttft_stat_s > ws.ttft_slo_s;
-    sg.ttft_lt = ws.ttft_stat_s < ws.ttft_slo_s;
-    sg.tpot_gt = ws.tpot_stat_s > ws.tpot_slo_s;
-    sg.tpot_lt = ws.tpot_stat_s < ws.tpot_slo_s;
-    sg.q_prefill = ws.q_prefill;
-    AbiView v{st, &ws};
+    sg.ttft_gt = ws->ttft_stat_s > ws->ttft_slo_s;
+    sg.ttft_lt = ws->ttft_stat_s < ws->ttft_slo_s;
+    sg.tpot_gt = ws->tpot_stat_s > ws->tpot_slo_s;
+    sg.tpot_lt = ws->tpot_stat_s < ws->tpot_slo_s;
+    sg.q_prefill = ws->q_prefill;
+    AbiView v{st, ws};
     int newcap[PADSIM_MAX_GPUS];
     int gsel, dir;
     const int N = st->n_gpus;
-    const int kind = ctl_step(pol, min_w, max_w, budget, N, v, st->drain_pending != 0,
-                              st->last_move_s, now, sg, newcap, &gsel, &dir);
+    bool pending = false;
+    for (int g = 0; g < N; g++) pending = pending || st->draining[g];
+    const int kind = ctl_step(pol, min_w, max_w, budget, N, v, pending, st->last_move_s, now, sg, newcap,
+                              &gsel, &dir);
     act->kind = kind;
     act->direction = dir;
     act->gpu = gsel;
-    for (int g = 0; g < PADSIM_MAX_GPUS; g++) act->new_cap_w[g] = g < N ? st->cmd_cap_w[g] : 0;
-    if (kind == ACT_MOVE_POWER || kind == ACT_MOVE_GPU) {
-        for (int g = 0; g < N; g++) {
-            act->new_cap_w[g] = newcap[g];
-            st->cmd_cap_w[g] = newcap[g];
-        }
-        st->last_move_s = now;
-        if (kind == ACT_MOVE_GPU) {
-            st->draining[gsel] = 1;
-            st->drain_pending = 1;
-        }
-    }
+    for (int g = 0; g < PADSIM_MAX_GPUS; g++) act->new_cap_w[g] = g < N ? v.target(g) : 0;
+    if (kind == ACT_MOVE_POWER || kind == ACT_MOVE_GPU)
+        for (int g = 0; g < N; g++) act->new_cap_w[g] = newcap[g];
 }
 
 // ---------------------------------------------------------------------------
@@ -448,6 +449,7 @@ static int validate_model(padsim_ctx* ctx, const padsim_model* m) {
 static int validate_policy(padsim_ctx* ctx, const padsim_policy* p, const padsim_model* m, int N,
                            int B) {
     if (p->kind < 0 || p->kind > 4) return fail(ctx, PADSIM_EINVAL, "policy kind");
+    if (p->window_stamp < 0 || p->window_stamp > 1) return fail(ctx, PADSIM_EINVAL, "window_stamp must be 0/1");
     if (p->kind == 0 || p->kind == 4) return PADSIM_OK;
     if (!(p->tick_s > 0 && p->settle_s > 0 && p->reassign_s > 0 && p->cooldown_s >= p->settle_s &&
           p->window_s >= 0 && p->power_step_w > 0 && p->queue_threshold >= 0 &&
@@ -532,7 +534,8 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
     // launches leave their SMs latency-bound (measured: cfg 2 45.8 → 51.5 ms with
     // five, cfg 4 621 → 609 ms)
     const long long n_static_rep = (long long)ccs.size() * Q * S;
-    const bool fine = (n_static_rep >= 400000LL && !getenv("PADSIM_KC3")) || getenv("PADSIM_KC5");
+    const int kcs = ctx->tune.stage_c_classes;
+    const bool fine = kcs == 5 || (kcs != 3 && n_static_rep >= 400000LL);
     ctx->kc_fine = fine;
     auto kcls = [fine](int y) { return fine ? kc_class(y) : (y <= 2 ? 1 : y <= 4 ? 2 : kNumKC - 1); };
     std::stable_sort(ccs.begin(), ccs.end(), [&](const CC& a, const CC& b) {
@@ -623,8 +626,8 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
         // and shared memory then holds 16 resident warps per SM instead of 12
         int tb = GQS >= (long long)ctx->n_sm * 2 * kThreads ? kThreads : 32;
         if (tb == kThreads && GQS >= (long long)ctx->n_sm * 2 * 256) tb = kATbBig;
-        if (const char* e = getenv("PADSIM_A_TB")) {       // experiment knob: 32 / 128 / 256
-            const int v = atoi(e);
+        {
+            const int v = ctx->tune.stage_a_threads;             // padsim_set_tuning override
             if (v == 32 || v == kThreads || v == kATbBig) tb = v;
         }
         ctx->fA_tb = tb;
@@ -672,13 +675,11 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
         ctx->d_workC = d_wc;
         const bool ctxm = model->decode_per_ctx_tok_s != 0.0;
         F.bits_in_smem = wheel <= 256 ? 1 : 0;
-        if (getenv("PADSIM_BITS_GLOBAL")) F.bits_in_smem = 0;          // experiment knob
-        F.c_prefetch = getenv("PADSIM_NO_PREFETCH") ? 0 : 1;            // experiment knob
+        F.c_prefetch = 1;
         // measured (cfg 4): the lane clock window slows stage C (683 -> 721 ms at
         // 16-64 inter-arrivals, 780 at 4) — its stream reads already coalesce
         // well enough — so it is off here; the joint kernel gains from it
         F.sync_win = 0.f;
-        if (const char* e = getenv("PADSIM_SYNC_WIN_C")) F.sync_win = (float)atof(e);   // experiment knob
         F.smem_trace = 0;
         size_t fr = 0, tm = 0;
         CK(cudaMemGetInfo(&fr, &tm));
@@ -694,16 +695,13 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
             // memory — 16 instead of 12 resident warps per SM: cfg 4 610 → 584 ms; the
             // others lose — all classes 700 ms, cfg 2's KW = 7 class 46.6 → 47.3 ms)
             int blmask = ctx->kc_fine ? (1 << (kNumKC - 1)) : 0;
-            if (const char* e = getenv("PADSIM_BL_MASK")) blmask = atoi(e);
+            if (ctx->tune.stage_c_batch_lists >= 0) blmask = ctx->tune.stage_c_batch_lists;
             const bool blc = (blmask >> kc) & 1;
             ctx->kc_bl[kc] = blc;
             const size_t wbytes = (size_t)KWc * kThreads *
                                   (kCWorkSlotBytes + (blc ? sizeof(int) : 0) + (ctxm ? kCWorkCtxSlotBytes : 0));
             const size_t bbytes = (size_t)KWc * (wheel / 32) * kThreads * sizeof(unsigned);
-            int bsm = blc ? 0 : F.bits_in_smem;
-            // experiment knob: the largest class keeps its wheel bitmaps in global
-            // memory so more of its warps fit in shared memory
-            if (kc == kNumKC - 1 && getenv("PADSIM_BITS_GLOBAL_BIG")) bsm = 0;
+            const int bsm = blc ? 0 : F.bits_in_smem;
             ctx->kc_bits_smem[kc] = bsm;
             ctx->kc_off_sdec[kc] = wbytes + (bsm ? bbytes : 0);
             const size_t base = ctx->kc_off_sdec[kc] + (size_t)F.m.ncap * sizeof(double);
@@ -723,11 +721,10 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
             const size_t hbytes = (size_t)KWc * kThreads * sizeof(unsigned);
             const size_t lbytes = (size_t)F.c_lslots * F.m.max_db * sizeof(double);
             size_t sm = base;
-            ctx->kc_hca[kc] = !getenv("PADSIM_NO_HCA") && occ_of(sm + hbytes) >= occ0;
+            ctx->kc_hca[kc] = occ_of(sm + hbytes) >= occ0;
             ctx->kc_off_hca[kc] = sm;
             if (ctx->kc_hca[kc]) sm += hbytes;
-            ctx->kc_ltab[kc] = !ctxm && F.c_lslots <= kLtabRows && !getenv("PADSIM_NO_LTAB") &&
-                               occ_of(sm + lbytes) >= occ0;
+            ctx->kc_ltab[kc] = !ctxm && F.c_lslots <= kLtabRows && occ_of(sm + lbytes) >= occ0;
             ctx->kc_off_ltab[kc] = sm;
             if (ctx->kc_ltab[kc]) sm += lbytes;
             ctx->kc_smem[kc] = sm;
@@ -756,7 +753,7 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
         // stage A (cfg 3) is latency-bound, and next to a large one (cfg 4) the
         // 168-register joint CTAs take the SM slots stage A's waves leave free
         // (measured: cfg 4 524 -> 506 ms/step against starting after stage A)
-        ctx->j_with_a = !getenv("PADSIM_JOINT_AFTER_A");   // knob: joint replays after stage A
+        ctx->j_with_a = ctx->tune.joint_after_stage_a != 1;
     }
     F.rep_met = ctx->d_rep_met; F.rep_near = ctx->d_rep_near; F.rep_dur = ctx->d_rep_dur;
     F.rep_good = ctx->d_rep_good; F.rep_events = ctx->d_rep_events;
@@ -773,7 +770,7 @@ extern "C" {
 
 const char* padsim_version(void) { return kVersion; }
 
-int padsim_create(int32_t dev, padsim_ctx** out) {
+int padsim_create(int32_t dev, void* stream, padsim_ctx** out) {
     if (!out) return PADSIM_EINVAL;
     *out = nullptr;
     int n = 0;
@@ -784,6 +781,7 @@ int padsim_create(int32_t dev, padsim_ctx** out) {
     padsim_ctx* ctx = new (std::nothrow) padsim_ctx();
     if (!ctx) return PADSIM_ENOMEM;
     ctx->device = dev;
+    ctx->stream = (cudaStream_t)stream;
     if (cudaSetDevice(dev) != cudaSuccess ||
         cudaDeviceGetAttribute(&ctx->n_sm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
         cudaGetLastError();
@@ -801,6 +799,7 @@ void padsim_destroy(padsim_ctx* ctx) {
     release_buffers(ctx);
     if (ctx->d_ctl_state) cudaFree(ctx->d_ctl_state);
     if (ctx->d_ctl_act) cudaFree(ctx->d_ctl_act);
+    if (ctx->d_ctl_stats) cudaFree(ctx->d_ctl_stats);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     if (ctx->evA) cudaEventDestroy(ctx->evA);
@@ -864,14 +863,17 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
     int rc = validate_model(ctx, model);
     if (rc) return rc;
     const int N = cands->n_gpus, C = cands->n_cand, B = budget->budget_w;
+    const int32_t* cbud = budget->cand_budget_w;     // nullable: one budget per candidate
     if (N < 2 || N > PADSIM_MAX_GPUS || C < 1 || !cands->role || !cands->cap_w || !cands->policy)
         return fail(ctx, PADSIM_EINVAL, "candidates");
     if (!(slo->ttft_s > 0 && slo->tpot_s[0] > 0 && slo->tpot_s[1] > 0))
         return fail(ctx, PADSIM_EINVAL, "SLOs must be > 0");
     for (int q = 0; q < n_qps; q++)
         if (!(qps[q] > 0) || !std::isfinite(qps[q])) return fail(ctx, PADSIM_EINVAL, "qps must be > 0");
-    std::vector<int> capsum(C);
+    std::vector<int> capsum(C), cbudget(C);
     for (int c = 0; c < C; c++) {
+        const int Bc = cbud ? cbud[c] : B;
+        cbudget[c] = Bc;
         int np = 0;
         long long cs = 0;
         for (int g = 0; g < N; g++) {
@@ -890,11 +892,11 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
             if (bad_index) *bad_index = c;
             return fail(ctx, PADSIM_EROLE, "need >= 1 prefill and >= 1 decode GPU");
         }
-        if (cs > B) {
+        if (cs > Bc) {
             if (bad_index) *bad_index = c;
             return fail(ctx, PADSIM_EBUDGET, "sum of caps exceeds the node budget");
         }
-        rc = validate_policy(ctx, &cands->policy[c], model, N, B);
+        rc = validate_policy(ctx, &cands->policy[c], model, N, Bc);
         if (rc) { if (bad_index) *bad_index = c; return rc; }
         capsum[c] = (int)cs;
     }
@@ -918,7 +920,7 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
         Rmax = std::max(Rmax, t.n_req);
     }
     toff[n_traces] = tot;
-    ctx->N = N; ctx->C = C; ctx->Q = n_qps; ctx->S = n_traces; ctx->Rmax = Rmax; ctx->B = B;
+    ctx->N = N; ctx->C = C; ctx->Q = n_qps; ctx->S = n_traces; ctx->Rmax = Rmax;
     ctx->model = *model;
     ctx->slo = *slo;
     ctx->flags = flags;
@@ -960,6 +962,7 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
     AL(ctx->d_role, (size_t)C * N);
     AL(ctx->d_cap, (size_t)C * N);
     AL(ctx->d_capsum, C);
+    AL(ctx->d_cbud, C);
     AL(ctx->d_pol, C);
     AL(ctx->d_qps, n_qps);
     AL(ctx->d_clist_static, std::max<size_t>(1, ctx->static_list.size()));
@@ -1025,6 +1028,7 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
     CK(cudaMemcpy(ctx->d_role, cands->role, (size_t)C * N, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(ctx->d_cap, cands->cap_w, sizeof(int) * (size_t)C * N, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(ctx->d_capsum, capsum.data(), sizeof(int) * C, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->d_cbud, cbudget.data(), sizeof(int) * C, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(ctx->d_pol, cands->policy, sizeof(padsim_policy) * C, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(ctx->d_qps, qps, sizeof(double) * n_qps, cudaMemcpyHostToDevice));
     if (!ctx->static_list.empty())
@@ -1061,7 +1065,7 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
         P.m.max_pb = model->max_prefill_batch; P.m.pb_tokens = model->prefill_token_budget;
         P.m.max_db = model->max_decode_batch; P.m.ctx_growth = model->decode_ctx_growth; P.m.slots = model->transfer_slots;
         P.m.spre = ctx->d_spre; P.m.sdec = ctx->d_sdec; P.m.den = ctx->d_den; P.m.ltab = ctx->d_ltab;
-        P.N = N; P.C = C; P.Q = n_qps; P.S = n_traces; P.Rmax = Rmax; P.B = B;
+        P.N = N; P.C = C; P.Q = n_qps; P.S = n_traces; P.Rmax = Rmax; P.cbud = ctx->d_cbud;
         P.toff = ctx->d_toff; P.nreq = ctx->d_nreq; P.s_unit = ctx->d_s_unit; P.kv = ctx->d_kv;
         P.in_tok = ctx->d_in; P.out_tok = ctx->d_out; P.phase = ctx->d_phase;
         P.role = ctx->d_role; P.cap = ctx->d_cap; P.pol = ctx->d_pol; P.qps = ctx->d_qps;
@@ -1109,7 +1113,7 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
         // N > 8: the per-GPU next-event / routing keys in global scratch instead of
         // 32 KB of shared memory per warp, so registers (11 warps/SM) instead of shared
         // memory (7) bound the occupancy: cfg 5 subset (65 k replays) 27.7 -> 23.3 s
-        P.j_kglob = NG == 64 && getenv("PADSIM_J64_KSMEM") == nullptr;   // knob: keep them in smem
+        P.j_kglob = NG == 64;
         if (P.j_kglob) P.off_keys = take((size_t)NG * 32 * (sizeof(double) + 2 * sizeof(int)));
         P.warp_bytes = off;
         ctx->j8[dyn] = true;
@@ -1124,9 +1128,10 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
         // (round end, with batch lists and the merged window walk: 8 inter-arrivals
         // cfg 3 315 -> 308 ms, 32: 328 ms; cfg 4 unchanged)
         P.sync_win = 8.f;
-        if (const char* e = getenv("PADSIM_SYNC_WIN")) P.sync_win = (float)atof(e);   // experiment knob
         const long long UJ = (long long)n_traces * n_qps * P.n_clist;
-        const int tbj = (NG == 8 && UJ >= (long long)ctx->n_sm * 3 * kThreads) ? kThreads : 32;
+        int tbj = (NG == 8 && UJ >= (long long)ctx->n_sm * 3 * kThreads) ? kThreads : 32;
+        if (NG == 8 && (ctx->tune.joint_threads == 32 || ctx->tune.joint_threads == kThreads))
+            tbj = ctx->tune.joint_threads;
         ctx->j_tb[dyn] = tbj;
         const void* fnj;
         size_t jb;
@@ -1139,14 +1144,13 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
         // 522 ms); when they are the bulk of the step (cfg 3) the 232-register
         // variant is faster (327 vs 357 ms).  PADSIM_J_R168=0/1 overrides.
         ctx->j_r168 = ctx->fact && ctx->kc_fine && NG == 8 && tbj == 32;
-        if (const char* e = getenv("PADSIM_J_R168")) ctx->j_r168 = atoi(e) != 0;
+        if (ctx->tune.joint_reg_cap >= 0) ctx->j_r168 = ctx->tune.joint_reg_cap != 0 && NG == 8 && tbj == 32;
         fnj = joint_fn(dyn, tbj, NG, cx, ctx->j_r168);
         P.smem_trace_bytes = jb;
         CK(cudaFuncSetAttribute(fnj, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jb));
         int occj = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occj, fnj, tbj, jb));
         occj = std::max(occj, 1);
-        if (const char* e = getenv("PADSIM_J_OCC")) occj = std::max(1, std::min(occj, atoi(e)));   // knob
         // replays per warp item: 32, or fewer when the joint workload would leave
         // the SMs with fewer than ~4 latency-bound warps each (measured on cfg 3,
         // 13.4k replays: 32 lanes 464 ms, 16 lanes 387 ms, 8 lanes 452 ms)
@@ -1154,7 +1158,7 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
             const long long UJ2 = (long long)n_traces * n_qps * P.n_clist;
             int lpw = 32;
             while (lpw > 4 && UJ2 / lpw < (long long)ctx->n_sm * 4) lpw >>= 1;
-            if (const char* e = getenv("PADSIM_J_LPW")) lpw = std::max(1, std::min(32, atoi(e)));   // knob
+            if (ctx->tune.joint_lanes_per_warp > 0) lpw = std::min(32, ctx->tune.joint_lanes_per_warp);
             P.lpw = lpw;
         }
         const long long items = ((long long)n_qps * P.n_clist + P.lpw - 1) / P.lpw;
@@ -1165,9 +1169,8 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
         P.scratch_per_cta = per_cta;
         size_t frj = 0, tmj = 0;
         CK(cudaMemGetInfo(&frj, &tmj));
-        // scratch cap: a fraction of device memory (knob PADSIM_J_MEMFRAC, default 0.3)
-        double mfr = 0.3;
-        if (const char* e = getenv("PADSIM_J_MEMFRAC")) mfr = std::min(0.8, std::max(0.05, atof(e)));
+        // scratch cap: 30 % of device memory
+        const double mfr = 0.3;
         const long long cap_ctas = std::max<long long>(n_traces, (long long)((double)tmj * mfr / (double)per_cta));
         long long gridj = std::min<long long>(per_trace * n_traces, (cap_ctas / n_traces) * n_traces);
         gridj = std::max<long long>(gridj, n_traces);
@@ -1187,7 +1190,7 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
         P.m.dec_per_ctx = model->decode_per_ctx_tok_s;
         P.m.max_db = model->max_decode_batch; P.m.ctx_growth = model->decode_ctx_growth; P.m.chunk = model->prefill_chunk_tokens;
         P.m.spre = ctx->d_spre; P.m.sdec = ctx->d_sdec; P.m.den = ctx->d_den; P.m.ltab = ctx->d_ltab;
-        P.N = N; P.C = C; P.Q = n_qps; P.S = n_traces; P.Rmax = Rmax; P.B = B;
+        P.N = N; P.C = C; P.Q = n_qps; P.S = n_traces; P.Rmax = Rmax; P.cbud = ctx->d_cbud;
         P.toff = ctx->d_toff; P.nreq = ctx->d_nreq; P.s_unit = ctx->d_s_unit; P.kv = ctx->d_kv;
         P.in_tok = ctx->d_in; P.out_tok = ctx->d_out; P.phase = ctx->d_phase;
         P.role = ctx->d_role; P.cap = ctx->d_cap; P.pol = ctx->d_pol; P.qps = ctx->d_qps;
@@ -1255,6 +1258,7 @@ int padsim_run(padsim_ctx* ctx, void* stream) {
         CK(cudaEventCreateWithFlags(&ctx->evCf, cudaEventDisableTiming));
     }
     CK(cudaEventRecord(ctx->ev0, st));
+    int launches = 0;
     // Schedule (measured on cfg 4): stage A runs first on the whole GPU; the joint
     // replays (dynamic candidates, static ones when N > 8, coalesced baselines) then
     // run on a side stream concurrently with stage C.  Stage C's resident grid is
@@ -1270,11 +1274,13 @@ int padsim_run(padsim_ctx* ctx, void* stream) {
         else if (ctx->fA_tb == kThreads) stageA_kernel<kThreads><<<ga, kThreads, ctx->fA_smem, st>>>(F);
         else stageA_kernel<32><<<ga, 32, ctx->fA_smem, st>>>(F);
         CK(cudaGetLastError());
+        launches++;
     }
     CK(cudaEventRecord(ctx->evA, st));
     const bool any_joint = ctx->plan_dyn.n_clist > 0 || ctx->plan_static.n_clist > 0 ||
                            ctx->plan_coal.n_clist > 0;
-    cudaStream_t js = ctx->fact && any_joint ? ctx->side : st;
+    const bool ser = ctx->tune.serialize != 0;     // every kernel on `st`, one after another
+    cudaStream_t js = ctx->fact && any_joint && !ser ? ctx->side : st;
     if (js != st) CK(cudaStreamWaitEvent(js, ctx->j_with_a ? ctx->ev0 : ctx->evA, 0));
     CK(cudaEventRecord(ctx->evJ0, js));
     for (int dyn = 0; dyn < 2; dyn++) {
@@ -1288,6 +1294,7 @@ int padsim_run(padsim_ctx* ctx, void* stream) {
             void* args[] = {(void*)&P};
             CK(cudaLaunchKernel(joint_fn(dyn != 0, tbl, ctx->j_ng, ctx->j_cx, ctx->j_r168), dim3(grid), dim3(tbl), args,
                                 smem, js));
+            launches++;
         }
         CK(cudaGetLastError());
     }
@@ -1297,6 +1304,7 @@ int padsim_run(padsim_ctx* ctx, void* stream) {
         else
             coalesced_kernel<false><<<ctx->grid_coal, 32, 0, js>>>(ctx->plan_coal);
         CK(cudaGetLastError());
+        launches++;
     }
     CK(cudaEventRecord(ctx->evJ1, js));
     CK(cudaEventRecord(ctx->evC0, st));
@@ -1308,12 +1316,10 @@ int padsim_run(padsim_ctx* ctx, void* stream) {
         // class's tail overlaps the others (they share nothing but the stream
         // records written by stage A and the scratch — each class gets its own
         // scratch slice)
-        const bool rev = getenv("PADSIM_KC_REV") != nullptr;      // experiment knob: launch order
-        for (int kq = 0; kq < kNumKC; kq++) {
-            const int kc = rev ? kNumKC - 1 - kq : kq;
+        for (int kc = 0; kc < kNumKC; kc++) {
             if (ctx->kc_n[kc] == 0) continue;
-            cudaStream_t cs = ctx->sideC[kc];
-            CK(cudaStreamWaitEvent(cs, ctx->evCf, 0));
+            cudaStream_t cs = ser ? st : ctx->sideC[kc];
+            if (!ser) CK(cudaStreamWaitEvent(cs, ctx->evCf, 0));
             FPlan F = ctx->fplan;
             F.s_begin = 0;
             F.s_count = ctx->S;
@@ -1329,8 +1335,9 @@ int padsim_run(padsim_ctx* ctx, void* stream) {
             F.scrC = ctx->kc_scr[kc];
             stagec_launch(cm, ctx->fC_idx16, kc, ctx->kc_bl[kc], ctx->kc_grid[kc], ctx->kc_smem[kc], cs, F);
             CK(cudaGetLastError());
+            launches++;
         }
-        for (int kc = 0; kc < kNumKC; kc++) {
+        for (int kc = 0; kc < kNumKC && !ser; kc++) {
             if (ctx->kc_n[kc] == 0) continue;
             CK(cudaEventRecord(ctx->evCk[kc], ctx->sideC[kc]));
             CK(cudaStreamWaitEvent(st, ctx->evCk[kc], 0));
@@ -1352,6 +1359,29 @@ int padsim_run(padsim_ctx* ctx, void* stream) {
     CK(cudaGetLastError());
     argmax_kernel<<<ctx->Q, 256, 0, st>>>(ctx->d_met, ctx->d_capsum, ctx->C, ctx->Q, ctx->d_argmax);
     CK(cudaGetLastError());
+    ctx->n_launches = launches + 3;     // + reduce, max80, argmax
+    return PADSIM_OK;
+}
+
+int padsim_launch_count(padsim_ctx* ctx, int32_t* n) {
+    if (!ctx || !n) return PADSIM_EINVAL;
+    *n = ctx->n_launches;
+    return PADSIM_OK;
+}
+
+int padsim_set_tuning(padsim_ctx* ctx, const padsim_tuning* t) {
+    if (!ctx) return PADSIM_EINVAL;
+    if (!t) { ctx->tune = padsim_tuning{0, 0, -1, 0, -1, 0, -1, 0}; return PADSIM_OK; }
+    if ((t->stage_a_threads != 0 && t->stage_a_threads != 32 && t->stage_a_threads != kThreads &&
+         t->stage_a_threads != kATbBig) ||
+        (t->stage_c_classes != 0 && t->stage_c_classes != 3 && t->stage_c_classes != 5) ||
+        t->stage_c_batch_lists < -1 || t->stage_c_batch_lists >= (1 << kNumKC) ||
+        (t->joint_threads != 0 && t->joint_threads != 32 && t->joint_threads != kThreads) ||
+        t->joint_reg_cap < -1 || t->joint_reg_cap > 1 || t->joint_lanes_per_warp < 0 ||
+        t->joint_lanes_per_warp > 32 || t->joint_after_stage_a < -1 || t->joint_after_stage_a > 1 ||
+        t->serialize < 0 || t->serialize > 1)
+        return fail(ctx, PADSIM_EINVAL, "tuning value out of range");
+    ctx->tune = *t;
     return PADSIM_OK;
 }
 
@@ -1517,13 +1547,14 @@ int padsim_fetch_records(padsim_ctx* ctx, void* stream, double* ttft, double* tp
     return PADSIM_OK;
 }
 
-int padsim_argmax_device(padsim_ctx* ctx, void* stream, const int64_t* d_met, int32_t n_cand,
-                         int32_t n_qps, int32_t* d_argmax) {
-    if (!ctx || !d_met || !d_argmax) return PADSIM_EINVAL;
-    if (!ctx->planned || n_cand != ctx->C || n_qps < 1)
-        return fail(ctx, PADSIM_EINVAL, "argmax shape does not match the plan");
+int padsim_argmax_device(padsim_ctx* ctx, void* stream, const int64_t* d_met, const int32_t* d_capsum,
+                         int32_t n_cand, int32_t n_qps, int32_t* d_argmax) {
+    if (!ctx || !d_met || !d_argmax || n_cand < 1 || n_qps < 1) return PADSIM_EINVAL;
+    if (!d_capsum && (!ctx->planned || n_cand != ctx->C))
+        return fail(ctx, PADSIM_EINVAL, "argmax without d_capsum needs the plan's candidate count");
     CK(cudaSetDevice(ctx->device));
-    argmax_kernel<<<n_qps, 256, 0, (cudaStream_t)stream>>>((const long long*)d_met, ctx->d_capsum,
+    argmax_kernel<<<n_qps, 256, 0, (cudaStream_t)stream>>>((const long long*)d_met,
+                                                           d_capsum ? d_capsum : ctx->d_capsum,
                                                            n_cand, n_qps, d_argmax);
     CK(cudaGetLastError());
     return PADSIM_OK;
@@ -1538,33 +1569,38 @@ int padsim_evaluate_allocations(padsim_ctx* ctx, const padsim_trace* traces, int
     int rc = padsim_plan(ctx, traces, n_traces, qps, n_qps, model, cands, slo, budget, 0, &bad);
     out->bad_index = bad;
     if (rc) return rc;
-    rc = padsim_run(ctx, nullptr);
+    rc = padsim_run(ctx, ctx->stream);
     if (rc) return rc;
-    rc = padsim_fetch(ctx, nullptr, out);
+    rc = padsim_fetch(ctx, ctx->stream, out);
     out->bad_index = -1;
     return rc;
 }
 
-int padsim_step_controller(padsim_ctx* ctx, const padsim_policy* policy, const padsim_budget* budget,
-                           const padsim_model* model, padsim_ctrl_state* st,
-                           const padsim_window_stats* ws, double now, padsim_action* act) {
+int padsim_controller_decide_device(padsim_ctx* ctx, const padsim_policy* policy,
+                                    const padsim_budget* budget, const padsim_model* model,
+                                    const padsim_ctrl_state* st, const padsim_window_stats* ws,
+                                    double now, padsim_action* act) {
     if (!ctx || !policy || !budget || !model || !st || !ws || !act) return PADSIM_EINVAL;
     if (st->n_gpus < 2 || st->n_gpus > PADSIM_MAX_GPUS) return fail(ctx, PADSIM_EINVAL, "n_gpus");
     int rc = validate_model(ctx, model);
     if (rc) return rc;
     rc = validate_policy(ctx, policy, model, st->n_gpus, budget->budget_w);
     if (rc) return rc;
+    if (policy->kind == 4) return fail(ctx, PADSIM_EINVAL, "coalesced policy has no controller");
     CK(cudaSetDevice(ctx->device));
     if (!ctx->d_ctl_state) {
         CK(cudaMalloc(&ctx->d_ctl_state, sizeof(padsim_ctrl_state)));
+        CK(cudaMalloc(&ctx->d_ctl_stats, sizeof(padsim_window_stats)));
         CK(cudaMalloc(&ctx->d_ctl_act, sizeof(padsim_action)));
     }
-    CK(cudaMemcpy(ctx->d_ctl_state, st, sizeof(*st), cudaMemcpyHostToDevice));
-    controller_kernel<<<1, 32>>>(*policy, model->min_w, model->max_w, budget->budget_w,
-                                 ctx->d_ctl_state, *ws, now, ctx->d_ctl_act);
+    cudaStream_t sm = ctx->stream;
+    CK(cudaMemcpyAsync(ctx->d_ctl_state, st, sizeof(*st), cudaMemcpyHostToDevice, sm));
+    CK(cudaMemcpyAsync(ctx->d_ctl_stats, ws, sizeof(*ws), cudaMemcpyHostToDevice, sm));
+    controller_kernel<<<1, 32, 0, sm>>>(*policy, model->min_w, model->max_w, budget->budget_w,
+                                        ctx->d_ctl_state, ctx->d_ctl_stats, now, ctx->d_ctl_act);
     CK(cudaGetLastError());
-    CK(cudaMemcpy(st, ctx->d_ctl_state, sizeof(*st), cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(act, ctx->d_ctl_act, sizeof(*act), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpyAsync(act, ctx->d_ctl_act, sizeof(*act), cudaMemcpyDeviceToHost, sm));
+    CK(cudaStreamSynchronize(sm));
     return PADSIM_OK;
 }
 

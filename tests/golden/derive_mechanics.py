@@ -162,6 +162,38 @@ def window():
                 exclusive=dict(base, policy=dict(pol, window_s=w_out), expect_no_move_before=2.5))
 
 
+def window_completion():
+    """Scenario B' — the same window under SPEC's completion stamping (policy
+    window_stamp = 1; "completion-time-stamped", "over completions in
+    [now - W, now]").  Eight requests at t=0 (8192 prompt): r0, r1 have 200
+    output tokens, r2..r7 one (they complete at their transfer end, TPOT 0).
+    Window W = W_in = 1.0 - pe0 as in scenario B.  First-token stamping: the
+    samples of r0/r1 (stamped pe0) are in the window at tick 1.0 and |Q_P| = 4
+    -> move at 1.0.  Completion stamping: no request completes before 1.0
+    (r2/r3 transfer-complete at e2 + kv = 1.504), so the window is empty at
+    1.0; at tick 2.0 it is [2.0 - W, 2.0] = [1.7405, 2.0]: r2/r3's stamps
+    (1.504) are outside, r0/r1 complete together at c = te0 + 199*L2 (alone on
+    the decode GPU, n = 2: out = 1 requests never join a decode batch) = 1.97,
+    inside, with TTFT 0.7405 > 0.5; [r6, r7] are still queued (|Q_P| = 2) ->
+    first move at 2.0.
+    """
+    pe0 = D600_2
+    w_in = 1.0 - pe0
+    te0 = pe0 + KV8192
+    c01 = te0 + 199.0 * decode_lat(2, 600)
+    assert 2.0 - w_in <= c01 <= 2.0
+    e2 = pe0 + D600_2
+    assert e2 + KV8192 < 2.0 - w_in
+    base = dict(n_gpus=2, role=[0, 1], cap=[600, 600], budget=1200,
+                slo=dict(ttft=0.5, tpot=[10.0, 10.0]), qps=1.0,
+                trace=dict(s_unit=[0.0] * 8, in_tok=[8192] * 8, out_tok=[200, 200] + [1] * 6))
+    pol = dict(kind=1, threshold=0, step_w=50, dec_ceiling_w=600, cooldown_s=0.5, tick_s=1.0,
+               settle_s=0.3, reassign_s=3.0, window_s=w_in)
+    return dict(_doc=window_completion.__doc__, c01=c01,
+                first_token=dict(base, policy=dict(pol, window_stamp=0), expect_first_move_t=1.0),
+                completion=dict(base, policy=dict(pol, window_stamp=1), expect_first_move_t=2.0))
+
+
 def move_gpu():
     """Scenario C — MoveGPU: re-routing in queue order, flip at empty + reassign
     (P:294 "drained of all in-flight requests ... reassignment latency"; S:256;
@@ -273,7 +305,8 @@ def boundary():
 
 
 def main():
-    out = dict(_source=__doc__, settle=settle(), window=window(), move_gpu=move_gpu(),
+    out = dict(_source=__doc__, settle=settle(), window=window(), window_completion=window_completion(),
+               move_gpu=move_gpu(),
                phase_switch=phase_switch(), boundary=boundary())
     with open(os.path.join(HERE, "mechanics.json"), "w") as f:
         json.dump(out, f, indent=1)

@@ -9,10 +9,10 @@ REC = ("ttft", "tpot", "prefill_end", "completion", "transfer_end")
 RTOL = 1e-9   # north_star: FP64 per-request latencies within 1e-9 relative
 
 
-def gpu_records(traces, qps, model, role, cap, pols, slo, budget):
-    ctx = pkg.Context(0)
+def gpu_records(traces, qps, model, role, cap, pols, slo, budget, tuning=None, cand_budget=None):
+    ctx = pkg.Context(0, tuning=tuning)
     try:
-        ctx.plan(traces, qps, model, role, cap, pols, slo, budget, records=True)
+        ctx.plan(traces, qps, model, role, cap, pols, slo, budget, records=True, cand_budget_w=cand_budget)
         ctx.run()
         res = ctx.fetch()
         rep = ctx.fetch_replays()
@@ -22,14 +22,17 @@ def gpu_records(traces, qps, model, role, cap, pols, slo, budget):
     return res, rep, rec
 
 
-def compare_records(traces, qps, model, role, cap, pols, slo, budget, exact=True):
-    """Per-request, per-replay comparison; returns number of requests compared."""
-    res, rep, rec = gpu_records(traces, qps, model, role, cap, pols, slo, budget)
+def compare_records(traces, qps, model, role, cap, pols, slo, budget, exact=True, tuning=None,
+                    cand_budget=None):
+    """Per-request, per-replay comparison; returns number of requests compared.
+    ``tuning``: launch-configuration overrides (padsim_set_tuning) to exercise."""
+    res, rep, rec = gpu_records(traces, qps, model, role, cap, pols, slo, budget, tuning, cand_budget)
     n = 0
     for c in range(role.shape[0]):
         for q, qv in enumerate(qps):
             for s, tr in enumerate(traces):
-                o = oracle.replay(model, role[c], cap[c], pols[c], budget, slo, tr, qv)
+                bc = budget if cand_budget is None else int(cand_budget[c])
+                o = oracle.replay(model, role[c], cap[c], pols[c], bc, slo, tr, qv)
                 R = tr["s_unit"].size
                 for k in REC:
                     g = rec[k][c, q, s, :R]
@@ -43,7 +46,8 @@ def compare_records(traces, qps, model, role, cap, pols, slo, budget, exact=True
                 assert rep["duration"][c, q, s] == o["duration"]
                 assert rep["goodput"][c, q, s] == o["goodput"]
                 n += R
-    ev = oracle.evaluate(model, role, cap, pols, budget, slo, traces, qps, n_threads=8)
+    ev = oracle.evaluate(model, role, cap, pols, budget, slo, traces, qps, n_threads=8,
+                         cand_budget_w=cand_budget)
     assert np.array_equal(res["met"], ev["met"])
     assert np.array_equal(res["argmax"], ev["argmax"])
     assert np.array_equal(res["near_boundary"], ev["near_boundary"])

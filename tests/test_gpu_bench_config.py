@@ -1,0 +1,65 @@
+"""Parity at the benchmarked configurations (SURVEY.md §8(d)
+"parity on the declared subset"): the GPU evaluates the FULL BASELINE grid in
+the launch configuration bench.py times (automatic tuning: for cfg 4 that is
+256-thread stage-A CTAs with KV slots in global scratch, five decode-pool
+classes, 168-register joint CTAs started next to stage A), and the oracle
+recomputes the declared subset replay by replay:
+  cfg 4 — all 976 candidates x 64 QPS x seeds {0, 1} (124 928 replays);
+  cfg 3 — all 425 candidates (420 dynamic policies + 5 static references, the
+          4P4D-750 W one at its own 6000 W budget) x 4 QPS x seeds {0, 1}.
+Per-replay met, goodput and duration must be identical."""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from workloads import DEFAULT_MODEL, get_config
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    from paper_2601_12241_b200.build import build
+    build()
+    import paper_2601_12241_b200 as p
+    return p
+
+
+def _subset_parity(pkg, name, seeds):
+    from bench import build_workload
+    cfg = get_config(name)
+    role, cap, pols, traces, qps, cb = build_workload(cfg, 0, pkg.enumerate_pool_uniform)
+    ctx = pkg.Context(0)
+    try:
+        ctx.plan(traces, qps, DEFAULT_MODEL, role, cap, pols, cfg["slo"], cfg["budget_w"], cand_budget_w=cb)
+        ctx.run()
+        res = ctx.fetch()
+        rep = ctx.fetch_replays()
+        ms = ctx.kernel_times_ms()
+    finally:
+        ctx.close()
+    ev = oracle.evaluate(DEFAULT_MODEL, role, cap, pols, cfg["budget_w"], cfg["slo"], traces[:seeds], qps,
+                         n_threads=os.cpu_count() or 1, per_replay=True, cand_budget_w=cb)
+    for k_gpu, k_or in (("met", "rep_met"), ("goodput", "rep_goodput"), ("duration", "rep_duration")):
+        g = rep[k_gpu][:, :, :seeds]
+        bad = np.argwhere(g != ev[k_or])
+        assert bad.size == 0, (name, k_gpu, bad[:5])
+    # the argmax kernel on the GPU's full Σmet (all seeds) = the A25 key
+    capsum = cap.sum(axis=1)
+    for q in range(len(qps)):
+        key = np.lexsort((np.arange(role.shape[0]), capsum, -res["met"][:, q]))
+        assert res["argmax"][q] == key[0]
+    assert np.array_equal(res["met"], rep["met"].sum(axis=2))
+    return ms
+
+
+def test_cfg4_full_grid_declared_subset(pkg):
+    ms = _subset_parity(pkg, "cfg4", 2)
+    assert ms[0] > 0 and ms[1] > 0 and ms[2] > 0      # stage A, stage C and joint replays all ran
+
+
+def test_cfg3_full_grid_subset(pkg):
+    ms = _subset_parity(pkg, "cfg3", 2)
+    assert ms[2] > 0

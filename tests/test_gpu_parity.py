@@ -37,13 +37,11 @@ def test_static_records_exact(pkg, family):
 
 
 @pytest.mark.parametrize("bl_mask", ["16", "31", "0"])
-def test_fine_decode_pool_classes(pkg, monkeypatch, bl_mask):
+def test_fine_decode_pool_classes(pkg, bl_mask):
     # large workloads split stage C into five decode-pool classes (KW = 1, 2, 4, 5, 7)
     # and use sorted batch lists for the KW = 7 class; force both on a small case
     # (every y = 1..7 appears; batch lists on no / the largest / every class):
     # records bit-exact
-    monkeypatch.setenv("PADSIM_KC5", "1")
-    monkeypatch.setenv("PADSIM_BL_MASK", bl_mask)
     # (with five classes the dynamic replays next to them use the 168-register
     # joint variant: two dynamic candidates exercise it)
     xpd = [(7, 500, 700), (6, 550, 650), (5, 600, 600), (4, 600, 600), (3, 650, 560),
@@ -51,7 +49,43 @@ def test_fine_decode_pool_classes(pkg, monkeypatch, bl_mask):
     role, cap = static_candidates(8, xpd)
     pols = [policy("static")] * 7 + [policy("dyn-both", cooldown_s=2.0), policy("dyn-power")]
     traces = [make_trace("lb", s, 250) for s in range(2)]
-    compare_records(traces, [0.5, 1.5, 3.0], DEFAULT_MODEL, role, cap, pols, DEFAULT_SLO, 4800)
+    compare_records(traces, [0.5, 1.5, 3.0], DEFAULT_MODEL, role, cap, pols, DEFAULT_SLO, 4800,
+                    tuning=dict(stage_c_classes=5, stage_c_batch_lists=int(bl_mask)))
+
+
+# Every launch variant the planner can pick for a large workload, forced on small
+# cases: stage A CTAs of 256 (the cfg 4 headline path: KV slots in global scratch),
+# 128 and 32 threads; joint replays in 128-thread CTAs, in 168-register one-warp
+# CTAs, after stage A; few lanes per warp item.  Records bit-exact against the oracle.
+TUNINGS = [dict(stage_a_threads=256), dict(stage_a_threads=128), dict(stage_a_threads=32),
+           dict(joint_threads=128), dict(joint_threads=32, joint_reg_cap=1),
+           dict(joint_after_stage_a=1, joint_lanes_per_warp=4),
+           dict(stage_a_threads=256, stage_c_classes=5, joint_reg_cap=1)]
+
+
+@pytest.mark.parametrize("tuning", TUNINGS, ids=lambda t: ",".join(f"{k}={v}" for k, v in t.items()))
+def test_launch_variants_records_exact(pkg, tuning):
+    xpd = XPD[:6]
+    role, cap = static_candidates(8, xpd + [(4, 600, 600), (3, 600, 600)])
+    pols = [policy("static")] * len(xpd) + [policy("dyn-both", cooldown_s=2.0), policy("dyn-power")]
+    traces = [make_trace("lb", 7 + s, 260) for s in range(2)] + [make_trace("phase", 3, 300)]
+    compare_records(traces, [0.5, 1.5, 3.0], DEFAULT_MODEL, role, cap, pols, PHASE_SLO, 4800, tuning=tuning)
+
+
+def test_window_stamp_completion_and_candidate_budgets(pkg):
+    # policy window_stamp = 1 (SPEC S:309/S:357 completion-stamped TTFT samples) and
+    # per-candidate budgets (Fig. 5a's 4P4D-750 W reference at 6000 W; a
+    # 4000 W dyn-gpu candidate whose DistributeUniformPower target is 500 W)
+    xpd = [(4, 600, 600), (5, 600, 600), (4, 750, 750), (3, 500, 500), (4, 600, 600)]
+    role, cap = static_candidates(8, xpd)
+    pols = [policy("dyn-both", window_stamp=1, cooldown_s=2.0), policy("dyn-power", window_stamp=1),
+            policy("static"), policy("dyn-gpu", window_stamp=1, cooldown_s=2.0), policy("dyn-both")]
+    cb = np.array([4800, 4800, 6000, 4000, 4800], np.int32)
+    traces = [make_trace("phase", s, 600) for s in range(2)]
+    compare_records(traces, [1.5, 2.5], DEFAULT_MODEL, role, cap, pols, PHASE_SLO, 4800, cand_budget=cb)
+    with pytest.raises(pkg.PadsimError) as e:          # 6000 W candidate under the 4800 W node budget
+        pkg.evaluate_allocations(traces, [1.5], DEFAULT_MODEL, role[2:3], cap[2:3], pols[2:3], PHASE_SLO, 4800)
+    assert e.value.rc == -3
 
 
 @pytest.mark.parametrize("kind", ["dyn-power", "dyn-gpu", "dyn-both"])
@@ -204,7 +238,10 @@ def test_validation_errors(pkg):
     assert e.value.rc == -6
 
 
-def test_step_controller_parity(pkg):
+def test_controller_device_matches_host_and_oracle(pkg):
+    # the kernel's __device__ ctl_step (padsim_controller_decide_device) against the
+    # host padsim_step_controller and the oracle's Alg. 1 step on random states
+    from paper_2601_12241_b200.binding import step_controller as host_step
     rng = np.random.default_rng(5)
     ctx = pkg.Context(0)
     try:
@@ -216,8 +253,7 @@ def test_step_controller_parity(pkg):
             drain = [0] * n
             if rng.random() < 0.2:
                 drain[int(rng.integers(n))] = 1
-            st = dict(role=role, cmd=cmd, draining=drain, drain_pending=int(sum(drain) > 0),
-                      last_move=float(rng.choice([0.0, 3.0, 9.5])))
+            st = dict(role=role, cmd=cmd, draining=drain, last_move=float(rng.choice([0.0, 3.0, 9.5])))
             stats = dict(ttft_stat=float(rng.choice([0.0, 0.5, 1.0, 1.4])),
                          tpot_stat=float(rng.choice([0.0, 0.02, 0.04, 0.05])),
                          ttft_slo=1.0, tpot_slo=0.04, q_prefill=int(rng.integers(0, 20)),
@@ -227,11 +263,11 @@ def test_step_controller_parity(pkg):
                          dec_ceiling_w=int(rng.choice([600, 750])))
             budget = max(4800, 400 * n)
             now = float(rng.choice([5.0, 10.0, 13.5]))
-            a1, s1 = ctx.step_controller(pol, DEFAULT_MODEL, budget, st, stats, now)
-            a2, s2 = oracle.step_controller(pol, DEFAULT_MODEL, budget,
-                                            dict(st), dict(stats), now)
-            assert a1 == a2, (trial, a1, a2)
-            assert s1 == s2, (trial, s1, s2)
+            a_dev = ctx.decide_device(pol, DEFAULT_MODEL, budget, st, stats, now)
+            a_host, _ = host_step(pol, DEFAULT_MODEL, budget, st, stats, now)
+            a_or, _ = oracle.step_controller(pol, DEFAULT_MODEL, budget, dict(st, drain_pending=int(sum(drain) > 0)),
+                                             dict(stats), now)
+            assert a_dev == a_host == a_or, (trial, a_dev, a_host, a_or)
     finally:
         ctx.close()
 

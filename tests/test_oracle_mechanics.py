@@ -97,6 +97,18 @@ def test_b_window_excludes_older_sample(model):
     assert all(t >= sc["expect_no_move_before"] for t, _, _ in _moves(r))
 
 
+@pytest.mark.parametrize("mode", ["first_token", "completion"])
+def test_b_window_stamping_modes(model, mode):
+    # policy window_stamp: 0 = TTFT sample at the first token (A22), 1 = at
+    # completion: the first move lands at 1.0 / 2.0
+    sc = G["window_completion"][mode]
+    r = _run(model, sc)
+    mv = _moves(r)
+    assert mv and mv[0][0] == sc["expect_first_move_t"]
+    if mode == "completion":          # no move before r0/r1 complete: their decode is undisturbed
+        assert r["completion"][0] == r["completion"][1] == G["window_completion"]["c01"]
+
+
 def test_c_move_gpu_reroute_and_flip(model):
     # reversed re-routing would give r8 the last batch; a flip without the
     # reassignment delay would split r9/r11 over two decode GPUs

@@ -8,7 +8,6 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-sys.path.insert(0, os.path.join(ROOT, "bench_support"))
 
 from bench import build_workload  # noqa: E402
 from workloads import DEFAULT_MODEL, get_config  # noqa: E402
@@ -24,11 +23,11 @@ from paper_2601_12241_b200.build import build  # noqa: E402
 
 build()
 cfg = get_config(a.config)
-role, cap, pols, traces, qps = build_workload(cfg, 0, pkg.enumerate_pool_uniform)
+role, cap, pols, traces, qps, cb = build_workload(cfg, 0, pkg.enumerate_pool_uniform)
 if a.traces:
     traces = traces[: a.traces]
 ctx = pkg.Context(0)
-ctx.plan(traces, qps, DEFAULT_MODEL, role, cap, pols, cfg["slo"], cfg["budget_w"])
+ctx.plan(traces, qps, DEFAULT_MODEL, role, cap, pols, cfg["slo"], cfg["budget_w"], cand_budget_w=cb)
 for _ in range(a.runs):
     ctx.run()
     print("replay ms", ctx.replay_kernel_ms())

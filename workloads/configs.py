@@ -26,7 +26,7 @@ DEFAULT_MODEL = {
 # Alg. 1 constants (S:372 defaults; P:294 sub-second tick, P:300 cooldown 2–6 s,
 # P:161 settle "hundreds of ms", P:294 reassignment 2–5 s, P:449 decode peak 600 W)
 DEFAULT_POLICY = {
-    "kind": 0, "threshold": 8, "step_w": 50, "dec_ceiling_w": 600,
+    "kind": 0, "threshold": 8, "step_w": 50, "dec_ceiling_w": 600, "window_stamp": 0,
     "cooldown_s": 4.0, "tick_s": 0.25, "window_s": 5.0, "settle_s": 0.3, "reassign_s": 3.0,
 }
 KIND = {"static": 0, "dyn-power": 1, "dyn-gpu": 2, "dyn-both": 3,
@@ -66,7 +66,10 @@ CONFIGS = {
                  slo=DEFAULT_SLO),
     # 3: dynamic policies swept on the two-phase trace (Fig. 9 / Fig. 10)
     "cfg3": dict(n_gpus=8, budget_w=4800, space=None, dynamic="sweep",
-                 statics=[(4, 600, 600), (5, 600, 600), (4, 750, 450), (4, 675, 525)],
+                 # static references of Fig. 5a / §5.1: 4P4D-600, 5P3D-600,
+                 # 4P-750/4D-450, 4P-675/4D-525 at the node's 4800 W, and 4P4D-750 at 6000 W
+                 # (x, p, d[, budget_w])
+                 statics=[(4, 600, 600), (5, 600, 600), (4, 750, 450), (4, 675, 525), (4, 750, 750, 6000)],
                  qps=[1.5, 2.0, 2.5, 3.0], family="phase", seeds=8, n_req=10000, slo=PHASE_SLO),
     # 4: exhaustive static + dynamic, 64 QPS x 32 seeds (north-star target)
     "cfg4": dict(n_gpus=8, budget_w=4800, space=dict(step_w=25), dynamic="splits",
