@@ -358,11 +358,16 @@ int padsim_controller_decide_device(padsim_ctx* ctx, const padsim_policy* policy
  *   joint_after_stage_a  1: joint replays wait for stage A (-1 auto)
  *   serialize            1: padsim_run launches every kernel on its stream, one
  *                        after another (per-kernel times in isolation, for the
- *                        roofline), 0: concurrent streams (read at run time)      */
+ *                        roofline), 0: concurrent streams (read at run time)
+ *   joint_groups         N ≤ 8 joint replays: 1 lane groups (one lane per simulated
+ *                        GPU, 4 replays per warp; group_path.cuh), 0 one thread per
+ *                        replay (dynamic_path.cuh), -1 auto (one thread per replay:
+ *                        measured faster)                             */
 typedef struct {
     int32_t stage_a_threads, stage_c_classes, stage_c_batch_lists;
     int32_t joint_threads, joint_reg_cap, joint_lanes_per_warp, joint_after_stage_a;
     int32_t serialize;
+    int32_t joint_groups;
 } padsim_tuning;
 int padsim_set_tuning(padsim_ctx* ctx, const padsim_tuning* tuning);
 

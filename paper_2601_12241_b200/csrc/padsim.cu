@@ -22,6 +22,7 @@
 #include "replay.cuh"
 #include "static_path.cuh"
 #include "dynamic_path.cuh"
+#include "group_path.cuh"
 
 #include <map>
 
@@ -31,7 +32,7 @@ struct padsim_ctx {
     int device = 0;
     int n_sm = 0;
     cudaStream_t stream = nullptr;   // stream of the one-shot API (padsim_create)
-    padsim_tuning tune{0, 0, -1, 0, -1, 0, -1, 0};   // launch overrides (padsim_set_tuning)
+    padsim_tuning tune{0, 0, -1, 0, -1, 0, -1, 0, -1};   // launch overrides (padsim_set_tuning)
     int n_launches = 0;              // kernels launched by the last padsim_run
     std::string err;
     // plan
@@ -143,6 +144,7 @@ struct padsim_ctx {
     std::vector<int> max_out;   // per trace
     bool j8[2] = {false, false};   // [static, dynamic] list planned on the joint kernel
     int j_ng = 8;                  // its GPU-slot width (8 or 64)
+    bool j_grp = false;            // N ≤ 8 joint replays on lane groups (jointg_kernel)
     unsigned* d_workJ[2] = {nullptr, nullptr};
 };
 
@@ -486,6 +488,13 @@ template <bool D, int TB, int NG>
 static const void* joint_fn_t(bool cx) {
     return cx ? (const void*)joint_kernel<D, TB, NG, true> : (const void*)joint_kernel<D, TB, NG, false>;
 }
+// lane-group joint replay (group_path.cuh) for (dynamic, context term, CTA size)
+template <bool D>
+static const void* jointg_fn_t(bool cx, int tb) {
+    if (tb == kThreads) return cx ? (const void*)jointg_kernel<D, true, kThreads> : (const void*)jointg_kernel<D, false, kThreads>;
+    return cx ? (const void*)jointg_kernel<D, true, 32> : (const void*)jointg_kernel<D, false, 32>;
+}
+static const void* jointg_fn(bool dyn, bool cx, int tb) { return dyn ? jointg_fn_t<true>(cx, tb) : jointg_fn_t<false>(cx, tb); }
 static const void* joint_fn(bool dyn, int tb, int ng, bool cx, bool r168 = false) {
     if (ng == 64) return dyn ? joint_fn_t<true, 32, 64>(cx) : joint_fn_t<false, 32, 64>(cx);
     if (tb == kThreads) return dyn ? joint_fn_t<true, kThreads, 8>(cx) : joint_fn_t<false, kThreads, 8>(cx);
@@ -1118,6 +1127,14 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
         P.warp_bytes = off;
         ctx->j8[dyn] = true;
         ctx->j_ng = NG;
+        // N ≤ 8, padsim_set_tuning joint_groups = 1: lane groups (one lane per
+        // simulated GPU, 4 replays per warp, group_path.cuh).  Parity-green but
+        // measured slower than one thread per replay (cfg 3 386 vs 300 ms, cfg 4
+        // 687 vs 487 ms: group collectives under intra-warp divergence take the
+        // WARPSYNC.COLLECTIVE slow path, and a DES instant rarely has per-GPU
+        // parallel work), so auto keeps the one-thread-per-replay kernel
+        ctx->j_grp = NG == 8 && ctx->tune.joint_groups == 1;
+        if (ctx->j_grp) P.warp_bytes = gscratch_layout(R, rslots, dyn != 0).bytes;
         unsigned* d_wj;
         AL(d_wj, n_traces);
         ctx->d_workJ[dyn] = d_wj;
@@ -1129,7 +1146,7 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
         // cfg 3 315 -> 308 ms, 32: 328 ms; cfg 4 unchanged)
         P.sync_win = 8.f;
         const long long UJ = (long long)n_traces * n_qps * P.n_clist;
-        int tbj = (NG == 8 && UJ >= (long long)ctx->n_sm * 3 * kThreads) ? kThreads : 32;
+        int tbj = (NG == 8 && !ctx->j_grp && UJ >= (long long)ctx->n_sm * 3 * kThreads) ? kThreads : 32;
         if (NG == 8 && (ctx->tune.joint_threads == 32 || ctx->tune.joint_threads == kThreads))
             tbj = ctx->tune.joint_threads;
         ctx->j_tb[dyn] = tbj;
@@ -1146,6 +1163,11 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
         ctx->j_r168 = ctx->fact && ctx->kc_fine && NG == 8 && tbj == 32;
         if (ctx->tune.joint_reg_cap >= 0) ctx->j_r168 = ctx->tune.joint_reg_cap != 0 && NG == 8 && tbj == 32;
         fnj = joint_fn(dyn, tbj, NG, cx, ctx->j_r168);
+        if (ctx->j_grp) {            // no shared memory; registers bound the occupancy
+            ctx->j_r168 = false;
+            jb = 0;
+            fnj = jointg_fn(dyn != 0, cx, tbj);
+        }
         P.smem_trace_bytes = jb;
         CK(cudaFuncSetAttribute(fnj, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jb));
         int occj = 0;
@@ -1159,7 +1181,7 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
             int lpw = 32;
             while (lpw > 4 && UJ2 / lpw < (long long)ctx->n_sm * 4) lpw >>= 1;
             if (ctx->tune.joint_lanes_per_warp > 0) lpw = std::min(32, ctx->tune.joint_lanes_per_warp);
-            P.lpw = lpw;
+            P.lpw = ctx->j_grp ? kGPW : lpw;
         }
         const long long items = ((long long)n_qps * P.n_clist + P.lpw - 1) / P.lpw;
         const int wpc = tbj / 32;
@@ -1292,8 +1314,9 @@ int padsim_run(padsim_ctx* ctx, void* stream) {
         {
             const int tbl = ctx->j_ng == 64 ? 32 : ctx->j_tb[dyn];
             void* args[] = {(void*)&P};
-            CK(cudaLaunchKernel(joint_fn(dyn != 0, tbl, ctx->j_ng, ctx->j_cx, ctx->j_r168), dim3(grid), dim3(tbl), args,
-                                smem, js));
+            const void* fn = ctx->j_grp ? jointg_fn(dyn != 0, ctx->j_cx, tbl)
+                                        : joint_fn(dyn != 0, tbl, ctx->j_ng, ctx->j_cx, ctx->j_r168);
+            CK(cudaLaunchKernel(fn, dim3(grid), dim3(tbl), args, smem, js));
             launches++;
         }
         CK(cudaGetLastError());
@@ -1371,7 +1394,7 @@ int padsim_launch_count(padsim_ctx* ctx, int32_t* n) {
 
 int padsim_set_tuning(padsim_ctx* ctx, const padsim_tuning* t) {
     if (!ctx) return PADSIM_EINVAL;
-    if (!t) { ctx->tune = padsim_tuning{0, 0, -1, 0, -1, 0, -1, 0}; return PADSIM_OK; }
+    if (!t) { ctx->tune = padsim_tuning{0, 0, -1, 0, -1, 0, -1, 0, -1}; return PADSIM_OK; }
     if ((t->stage_a_threads != 0 && t->stage_a_threads != 32 && t->stage_a_threads != kThreads &&
          t->stage_a_threads != kATbBig) ||
         (t->stage_c_classes != 0 && t->stage_c_classes != 3 && t->stage_c_classes != 5) ||
@@ -1379,7 +1402,7 @@ int padsim_set_tuning(padsim_ctx* ctx, const padsim_tuning* t) {
         (t->joint_threads != 0 && t->joint_threads != 32 && t->joint_threads != kThreads) ||
         t->joint_reg_cap < -1 || t->joint_reg_cap > 1 || t->joint_lanes_per_warp < 0 ||
         t->joint_lanes_per_warp > 32 || t->joint_after_stage_a < -1 || t->joint_after_stage_a > 1 ||
-        t->serialize < 0 || t->serialize > 1)
+        t->serialize < 0 || t->serialize > 1 || t->joint_groups < -1 || t->joint_groups > 1)
         return fail(ctx, PADSIM_EINVAL, "tuning value out of range");
     ctx->tune = *t;
     return PADSIM_OK;

@@ -60,7 +60,9 @@ def test_fine_decode_pool_classes(pkg, bl_mask):
 TUNINGS = [dict(stage_a_threads=256), dict(stage_a_threads=128), dict(stage_a_threads=32),
            dict(joint_threads=128), dict(joint_threads=32, joint_reg_cap=1),
            dict(joint_after_stage_a=1, joint_lanes_per_warp=4),
-           dict(stage_a_threads=256, stage_c_classes=5, joint_reg_cap=1)]
+           dict(stage_a_threads=256, stage_c_classes=5, joint_reg_cap=1),
+           dict(joint_groups=1), dict(joint_groups=1, joint_threads=128),
+           dict(joint_groups=1, stage_c_classes=5)]
 
 
 @pytest.mark.parametrize("tuning", TUNINGS, ids=lambda t: ",".join(f"{k}={v}" for k, v in t.items()))
@@ -88,15 +90,18 @@ def test_window_stamp_completion_and_candidate_budgets(pkg):
     assert e.value.rc == -3
 
 
+@pytest.mark.parametrize("groups", [0, 1], ids=["thread", "lane-groups"])
 @pytest.mark.parametrize("kind", ["dyn-power", "dyn-gpu", "dyn-both"])
-def test_dynamic_records_exact(pkg, kind):
+def test_dynamic_records_exact(pkg, kind, groups):
+    # groups = 1: the lane-group joint kernel (group_path.cuh), one lane per GPU
     xpd = [(4, 600, 600), (5, 600, 600), (3, 600, 600), (4, 750, 450)]
     role, cap = static_candidates(8, xpd)
     pols = [policy(kind, cooldown_s=2.0), policy(kind, threshold=2, window_s=2.5, cooldown_s=3.0),
             policy(kind, step_w=25), policy(kind, step_w=100, window_s=10.0)]
     traces = [make_trace("phase", s, 800) for s in range(2)]
     qps = [1.5, 2.0, 3.0]
-    compare_records(traces, qps, DEFAULT_MODEL, role, cap, pols, PHASE_SLO, 4800)
+    compare_records(traces, qps, DEFAULT_MODEL, role, cap, pols, PHASE_SLO, 4800,
+                    tuning=dict(joint_groups=groups))
 
 
 def test_mixed_static_dynamic_and_argmax(pkg):
@@ -286,8 +291,8 @@ def test_joint_kernel_matches_factorized_path(pkg):
     traces = [make_trace("lb", 40 + s, 400) for s in range(2)] + [make_trace("lb_bursty", 3, 300)]
     qps = [0.5, 1.75, 3.5]
     outs = []
-    for joint in (False, True):
-        ctx = pkg.Context(0)
+    for joint, groups in ((False, 0), (True, 0), (True, 1)):
+        ctx = pkg.Context(0, tuning=dict(joint_groups=groups))
         try:
             ctx.plan(traces, qps, DEFAULT_MODEL, role, cap, pols, DEFAULT_SLO, 4800, records=True,
                      joint=joint)
@@ -295,13 +300,14 @@ def test_joint_kernel_matches_factorized_path(pkg):
             outs.append((ctx.fetch(), ctx.fetch_replays(), ctx.fetch_records()))
         finally:
             ctx.close()
-    (ra, pa, ca), (rb, pb, cb) = outs
-    for k in ra:
-        assert np.array_equal(ra[k], rb[k]), k
-    for k in ("met", "near_boundary", "duration", "goodput"):
-        assert np.array_equal(pa[k], pb[k]), k
-    for k in ca:
-        assert np.array_equal(ca[k], cb[k]), k
+    (ra, pa, ca) = outs[0]
+    for rb, pb, cb in outs[1:]:        # joint kernel, one thread / one lane group per replay
+        for k in ra:
+            assert np.array_equal(ra[k], rb[k]), k
+        for k in ("met", "near_boundary", "duration", "goodput"):
+            assert np.array_equal(pa[k], pb[k]), k
+        for k in ca:
+            assert np.array_equal(ca[k], cb[k]), k
     ref = oracle.evaluate(DEFAULT_MODEL, role, cap, pols, 4800, DEFAULT_SLO, traces, qps, n_threads=8)
     assert np.array_equal(ra["met"], ref["met"]) and np.array_equal(ra["argmax"], ref["argmax"])
 
