@@ -1,0 +1,49 @@
+"""A/B of launch tunings on one box: padsim_run time (CUDA events around the
+whole run) of a BASELINE config under several padsim_set_tuning overrides,
+interleaved runs, median per tuning.  Results are identical by construction
+(every variant is parity-tested); this only measures speed.
+
+    python tools/tune_sweep.py --config cfg3 --runs 3 '{}' '{"joint_lanes_per_warp": 8}'
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from bench import build_workload  # noqa: E402
+from workloads import DEFAULT_MODEL, get_config  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="cfg3")
+ap.add_argument("--runs", type=int, default=3)
+ap.add_argument("tunings", nargs="+")
+a = ap.parse_args()
+
+import paper_2601_12241_b200 as pkg  # noqa: E402
+from paper_2601_12241_b200.build import build  # noqa: E402
+
+build()
+cfg = get_config(a.config)
+role, cap, pols, traces, qps, cb = build_workload(cfg, 0, pkg.enumerate_pool_uniform)
+ctxs = []
+for t in a.tunings:
+    ctx = pkg.Context(0, tuning=json.loads(t))
+    ctx.plan(traces, qps, DEFAULT_MODEL, role, cap, pols, cfg["slo"], cfg["budget_w"], cand_budget_w=cb)
+    ctx.run()                                  # warm-up
+    ctxs.append(ctx)
+ms = [[] for _ in ctxs]
+for _ in range(a.runs):
+    for j, ctx in enumerate(ctxs):
+        ctx.run()
+        ms[j].append(ctx.replay_kernel_ms())
+ref = ctxs[0].fetch()["met"]
+for t, ctx, m in zip(a.tunings, ctxs, ms):
+    same = bool((ctx.fetch()["met"] == ref).all())
+    print(json.dumps({"config": a.config, "tuning": json.loads(t), "ms": statistics.median(m),
+                      "all_ms": m, "met_equal": same}))
+for ctx in ctxs:
+    ctx.close()
