@@ -46,7 +46,8 @@ TRAFFIC_PATH = os.path.join(ROOT, "profiles", "ncu_traffic.json")   # dram bytes
 # arrival scale (1 mul), its share of the prefill batch latency (1 div), TTFT
 # (1 sub), transfer end (1 add) = 4; stage C — two segment boundaries (2 x (mul +
 # add)), TPOT (sub + div), two SLO compares = 8; the joint replay does both = 12.
-FP64_OPS_PER_REQ = {"stageA_kernel": 4, "stageC_kernel": 8, "joint_kernel": 12}
+FP64_OPS_PER_REQ = {"stageA_kernel": 4, "stageC_kernel": 8, "joint_kernel": 12,
+                    "stageA_wide_kernel": 4, "stageC_wide_kernel": 8}
 WARP_INSTR_BUDGET = 15      # warp-instructions per simulated request (8-lane groups)
 
 
@@ -350,10 +351,11 @@ def main():
     ev_static = int(ev_rep[~is_dyn].sum().item()) if Cl else 0
     ev_dyn = int(ev_rep[is_dyn].sum().item()) if Cl else 0
     ev_a = int(as_tensor(d.d_aux_events, d.n_aux_events, torch.int64, "<i8").sum().item()) \
-        if d.n_aux_events > 0 else 0
-    if ev_a == 0:            # N > 8: static replays run in the joint kernel
+        if d.n_aux_events > 0 else 0     # stage A instants (factorized static paths)
+    if ev_a == 0:            # static replays ran in the joint kernel
         ev_dyn += ev_static
         ev_static = 0
+    wide = role.shape[1] > 8 and ev_a > 0     # N > 8: the wide-node factorized path
     # per-rank replay results of the timed configuration (for the parity sample)
     rep = ctx.fetch_replays()
 
@@ -374,10 +376,12 @@ def main():
     r_sum = sum(int(t["s_unit"].size) for t in traces)
     static_idx = [c for c in sh.cand if pols[c]["kind"] == 0]
     groups = {tuple(int(v) for v in cap[c][role[c] == 0]) for c in static_idx}
-    fact = ev_a > 0                       # the factorized static path ran (N <= 8)
+    fact = ev_a > 0                       # a factorized static path ran (N <= 8, or wide N <= 64)
     req_k = {"stageA_kernel": len(groups) * Ql * r_sum if fact else 0,
              "stageC_kernel": len(static_idx) * Ql * r_sum if fact else 0,
              "joint_kernel": (Cl - len(static_idx) + (0 if fact else len(static_idx))) * Ql * r_sum}
+    req_k["stageA_wide_kernel"] = req_k["stageA_kernel"]
+    req_k["stageC_wide_kernel"] = req_k["stageC_kernel"]
 
     # e2e: the public API with host buffers (evaluate_sharded = padsim_evaluate_allocations on
     # this rank's shard + allgather + argmax; one process: exactly padsim_evaluate_allocations)
@@ -401,7 +405,8 @@ def main():
         mp_ = micro_peaks()
         clocks = clk.summary()
         km = np.mean(np.array(kern_ms), axis=0) if kern_ms else np.zeros(3)
-        names = ["stageA_kernel", "stageC_kernel", "joint_kernel"]
+        names = (["stageA_wide_kernel", "stageC_wide_kernel", "joint_kernel"] if wide
+                 else ["stageA_kernel", "stageC_kernel", "joint_kernel"])
         evs = [ev_a, ev_static, ev_dyn]
         # dominant kernel = the one with the most isolated device time
         dom = int(np.argmax(iso))

@@ -362,12 +362,16 @@ int padsim_controller_decide_device(padsim_ctx* ctx, const padsim_policy* policy
  *   joint_groups         N ≤ 8 joint replays: 1 lane groups (one lane per simulated
  *                        GPU, 4 replays per warp; group_path.cuh), 0 one thread per
  *                        replay (dynamic_path.cuh), -1 auto (one thread per replay:
- *                        measured faster)                             */
+ *                        measured faster)
+ *   wide_path            8 < N ≤ 64 static candidates: 1/-1 the factorized
+ *                        warp-per-replay stages (wide_path.cuh), 0 the joint kernel
+ *   wide_chunk           traces per stage A → C chunk of the wide path (0 auto:
+ *                        as many as half the free device memory holds)        */
 typedef struct {
     int32_t stage_a_threads, stage_c_classes, stage_c_batch_lists;
     int32_t joint_threads, joint_reg_cap, joint_lanes_per_warp, joint_after_stage_a;
     int32_t serialize;
-    int32_t joint_groups;
+    int32_t joint_groups, wide_path, wide_chunk;
 } padsim_tuning;
 int padsim_set_tuning(padsim_ctx* ctx, const padsim_tuning* tuning);
 

@@ -106,12 +106,12 @@ class Tuning(C.Structure):
                 ("stage_c_batch_lists", C.c_int32), ("joint_threads", C.c_int32),
                 ("joint_reg_cap", C.c_int32), ("joint_lanes_per_warp", C.c_int32),
                 ("joint_after_stage_a", C.c_int32), ("serialize", C.c_int32),
-                ("joint_groups", C.c_int32)]
+                ("joint_groups", C.c_int32), ("wide_path", C.c_int32), ("wide_chunk", C.c_int32)]
 
 
 TUNING_AUTO = dict(stage_a_threads=0, stage_c_classes=0, stage_c_batch_lists=-1, joint_threads=0,
                    joint_reg_cap=-1, joint_lanes_per_warp=0, joint_after_stage_a=-1, serialize=0,
-                   joint_groups=-1)
+                   joint_groups=-1, wide_path=-1, wide_chunk=0)
 
 
 class Action(C.Structure):

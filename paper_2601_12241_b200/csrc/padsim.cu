@@ -23,6 +23,7 @@
 #include "static_path.cuh"
 #include "dynamic_path.cuh"
 #include "group_path.cuh"
+#include "wide_path.cuh"
 
 #include <map>
 
@@ -32,7 +33,7 @@ struct padsim_ctx {
     int device = 0;
     int n_sm = 0;
     cudaStream_t stream = nullptr;   // stream of the one-shot API (padsim_create)
-    padsim_tuning tune{0, 0, -1, 0, -1, 0, -1, 0, -1};   // launch overrides (padsim_set_tuning)
+    padsim_tuning tune{0, 0, -1, 0, -1, 0, -1, 0, -1, -1, 0};   // launch overrides (padsim_set_tuning)
     int n_launches = 0;              // kernels launched by the last padsim_run
     std::string err;
     // plan
@@ -145,6 +146,13 @@ struct padsim_ctx {
     bool j8[2] = {false, false};   // [static, dynamic] list planned on the joint kernel
     int j_ng = 8;                  // its GPU-slot width (8 or 64)
     bool j_grp = false;            // N ≤ 8 joint replays on lane groups (jointg_kernel)
+    // factorized static path for wide nodes (8 < N ≤ 64, wide_path.cuh)
+    bool wide = false;
+    int w_chunk = 1;               // traces per stage A → C chunk (stream buffers sized for it)
+    int wA_grid = 0, wC_grid = 0;  // CTAs per chunk
+    unsigned* d_workW = nullptr;   // work counters [2][S] (stage A, stage C)
+    std::vector<cudaEvent_t> evW;  // per chunk: stage A start/stop, stage C start/stop
+    int n_wchunks = 0;             // chunks of the last run
     unsigned* d_workJ[2] = {nullptr, nullptr};
 };
 
@@ -201,6 +209,7 @@ static void free_plan(padsim_ctx* ctx) {
     ctx->buf_cursor = 0;       // buffers are kept for reuse by the next plan
     ctx->planned = false;
     ctx->fact = false;
+    ctx->wide = false;
     ctx->j8[0] = ctx->j8[1] = false;
     ctx->static_list.clear();
     ctx->dyn_list.clear();
@@ -775,6 +784,132 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
     return PADSIM_OK;
 }
 
+// Wide nodes (8 < N ≤ 64): groups static candidates by prefill pool as
+// plan_factorized does and lays out the warp-per-replay stages (wide_path.cuh).
+// The stage A → C stream (40 B per request per (group, QPS, trace)) is sized
+// for a chunk of traces; padsim_run replays the traces chunk by chunk.
+static int plan_wide(padsim_ctx* ctx, const padsim_model* model, const padsim_slo* slo, int Q, int S,
+                     int Rmax, const padsim_candidates* cands) {
+    const int N = ctx->N;
+    std::map<std::vector<int>, int> gid;
+    std::vector<int> gx, gcap;
+    struct CC { int group, cand, y; std::vector<int> dc; };
+    std::vector<CC> ccs;
+    for (int c : ctx->static_list) {
+        std::vector<int> pc, dc;
+        for (int g = 0; g < N; g++) {
+            const int w = cands->cap_w[(size_t)c * N + g];
+            (cands->role[(size_t)c * N + g] == 0 ? pc : dc).push_back(w);
+        }
+        auto it = gid.find(pc);
+        int gi;
+        if (it == gid.end()) {
+            gi = (int)gid.size();
+            gid.emplace(pc, gi);
+            gx.push_back((int)pc.size());
+            for (int w = 0; w < kWMax; w++) gcap.push_back(w < (int)pc.size() ? pc[w] : model->min_w);
+        } else {
+            gi = it->second;
+        }
+        ccs.push_back(CC{gi, c, (int)dc.size(), dc});
+    }
+    // warps of a CTA take consecutive candidates of one prefill group (same stream)
+    std::stable_sort(ccs.begin(), ccs.end(), [](const CC& a, const CC& b) { return a.group < b.group; });
+    const int G = (int)gx.size(), NC = (int)ccs.size();
+    std::vector<int> cc_cand(NC), cc_group(NC), cc_y(NC), cc_dcap((size_t)NC * kWMax);
+    for (int k = 0; k < NC; k++) {
+        cc_cand[k] = ccs[k].cand; cc_group[k] = ccs[k].group; cc_y[k] = ccs[k].y;
+        for (int w = 0; w < kWMax; w++)
+            cc_dcap[(size_t)k * kWMax + w] = w < ccs[k].y ? ccs[k].dc[w] : model->min_w;
+    }
+    FPlan& F = ctx->fplan;
+    std::memset(&F, 0, sizeof(F));
+    F.m.min_w = model->min_w; F.m.max_w = model->max_w; F.m.ncap = model->max_w - model->min_w + 1;
+    F.m.rate = model->prefill_base_rate; F.m.eff = model->prefill_batch_eff;
+    F.m.dec_fixed = model->decode_fixed_s; F.m.dec_per_seq = model->decode_per_seq_s;
+    F.m.dec_per_ctx = model->decode_per_ctx_tok_s; F.m.kvb = model->kv_bytes_per_token;
+    F.m.bw = model->fabric_bw_Bps; F.m.ovh = model->transfer_overhead_s;
+    F.m.max_pb = model->max_prefill_batch; F.m.pb_tokens = model->prefill_token_budget;
+    F.m.max_db = model->max_decode_batch; F.m.slots = model->transfer_slots;
+    F.m.ctx_growth = model->decode_ctx_growth;
+    F.m.spre = ctx->d_spre; F.m.sdec = ctx->d_sdec; F.m.den = ctx->d_den; F.m.ltab = ctx->d_ltab;
+    F.N = N; F.Q = Q; F.S = S; F.Rmax = std::max(Rmax, 1);
+    F.toff = ctx->d_toff; F.nreq = ctx->d_nreq; F.s_unit = ctx->d_s_unit; F.kv = ctx->d_kv;
+    F.in_tok = ctx->d_in; F.out_tok = ctx->d_out; F.phase = ctx->d_phase; F.qps = ctx->d_qps;
+    F.ttft_slo = slo->ttft_s; F.tpot_slo0 = slo->tpot_s[0]; F.tpot_slo1 = slo->tpot_s[1];
+    F.n_groups = G;
+    F.n_cc = NC;
+    const size_t Rm = (size_t)F.Rmax;
+    const long long GQS = (long long)G * Q * S;
+    // traces per chunk: the stream of one trace is G·Q·Rmax·40 B (cfg 5: 26.8 GB)
+    size_t fr = 0, tm = 0;
+    CK(cudaMemGetInfo(&fr, &tm));
+    const size_t per_trace = (size_t)G * Q * Rm * (sizeof(SRec) + sizeof(SHot) + sizeof(double));
+    const size_t budget = fr / 2;
+    int chunk = (int)std::min<size_t>((size_t)S, std::max<size_t>(1, budget / std::max<size_t>(per_trace, 1)));
+    if (ctx->tune.wide_chunk > 0) chunk = std::min(S, (int)ctx->tune.wide_chunk);
+    chunk = std::max(chunk, 1);
+    ctx->w_chunk = chunk;
+    const long long GQC = (long long)G * Q * chunk;
+#define AL(p, n) do { int r_ = dalloc(ctx, &(p), (size_t)(n)); if (r_) return r_; } while (0)
+    int *d_gx, *d_gcap, *d_ccc, *d_ccg, *d_ccy, *d_ccd;
+    AL(d_gx, G); AL(d_gcap, (size_t)G * kWMax); AL(d_ccc, NC); AL(d_ccg, NC); AL(d_ccy, NC);
+    AL(d_ccd, (size_t)NC * kWMax);
+    CK(cudaMemcpy(d_gx, gx.data(), sizeof(int) * G, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_gcap, gcap.data(), sizeof(int) * G * kWMax, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_ccc, cc_cand.data(), sizeof(int) * NC, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_ccg, cc_group.data(), sizeof(int) * NC, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_ccy, cc_y.data(), sizeof(int) * NC, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_ccd, cc_dcap.data(), sizeof(int) * NC * kWMax, cudaMemcpyHostToDevice));
+    F.gx = d_gx; F.w_gcap = d_gcap; F.cc_cand = d_ccc; F.cc_group = d_ccg; F.cc_y = d_ccy; F.w_dcap = d_ccd;
+    SRec* d_rec;
+    SHot* d_hot;
+    double* d_pe;
+    long long* d_evA;
+    double *d_asq, *d_ase;
+    AL(d_rec, GQC * Rm); AL(d_hot, GQC * Rm); AL(d_pe, GQC * Rm);
+    AL(d_evA, GQS); AL(d_asq, GQS); AL(d_ase, GQS);
+    F.st_rec = d_rec; F.st_hot = d_hot; F.st_pe = d_pe; F.evA = d_evA; F.a_sq = d_asq; F.a_se = d_ase;
+    ctx->d_evA = d_evA;
+    ctx->n_evA = (int)GQS;
+    int rb = 1;
+    while (rb < model->max_decode_batch) rb <<= 1;
+    F.c_rb = rb;
+    F.a_warp_bytes = wide_a_layout(Rm).bytes;
+    F.c_warp_bytes = wide_c_layout(Rm, rb).bytes;
+    AL(ctx->d_workW, (size_t)2 * S);
+    // one warp per replay; CTAs (4 warps) bound to one trace of the chunk, warps pull
+    // replays from that trace's counter; scratch per resident warp
+    auto grid_of = [&](const void* fn, long long items, size_t warp_bytes, long long& grid) -> int {
+        int occ = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, 0));
+        occ = std::max(occ, 1);
+        long long per_tr = std::max<long long>(1, ((long long)ctx->n_sm * occ) / chunk);
+        per_tr = std::min<long long>(per_tr, (items + kWarps - 1) / kWarps);
+        const long long cap = std::max<long long>(1, (long long)((double)fr * 0.2 / ((double)warp_bytes * kWarps * chunk)));
+        grid = std::max<long long>(1, std::min(per_tr, cap)) * chunk;
+        return PADSIM_OK;
+    };
+    long long ga = 0, gc = 0;
+    if (int r_ = grid_of((const void*)stageA_wide_kernel, (long long)Q * G, F.a_warp_bytes, ga)) return r_;
+    if (int r_ = grid_of((const void*)stageC_wide_kernel, (long long)Q * NC, F.c_warp_bytes, gc)) return r_;
+    ctx->wA_grid = (int)ga;
+    ctx->wC_grid = (int)gc;
+    char *sa, *sc;
+    AL(sa, (size_t)ga * kWarps * F.a_warp_bytes);
+    AL(sc, (size_t)gc * kWarps * F.c_warp_bytes);
+    F.scrA = sa;
+    F.scrC = sc;
+    F.rep_met = ctx->d_rep_met; F.rep_near = ctx->d_rep_near; F.rep_dur = ctx->d_rep_dur;
+    F.rep_good = ctx->d_rep_good; F.rep_events = ctx->d_rep_events;
+    if (ctx->flags & PADSIM_RECORDS) {
+        F.rec_ttft = ctx->d_rec[0]; F.rec_tpot = ctx->d_rec[1]; F.rec_pe = ctx->d_rec[2];
+        F.rec_comp = ctx->d_rec[3]; F.rec_te = ctx->d_rec[4];
+    }
+#undef AL
+    return PADSIM_OK;
+}
+
 extern "C" {
 
 const char* padsim_version(void) { return kVersion; }
@@ -809,6 +944,7 @@ void padsim_destroy(padsim_ctx* ctx) {
     if (ctx->d_ctl_state) cudaFree(ctx->d_ctl_state);
     if (ctx->d_ctl_act) cudaFree(ctx->d_ctl_act);
     if (ctx->d_ctl_stats) cudaFree(ctx->d_ctl_stats);
+    for (auto e : ctx->evW) cudaEventDestroy(e);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     if (ctx->evA) cudaEventDestroy(ctx->evA);
@@ -1059,9 +1195,17 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
         int r_ = plan_factorized(ctx, model, slo, n_qps, n_traces, Rmax, tot, cands);
         if (r_) return r_;
     }
+    // wide nodes: the warp-per-replay factorized path (no context term: with one the
+    // static candidates stay on the joint kernel)
+    ctx->wide = N > 8 && N <= kWMax && !ctx->static_list.empty() && !(flags & PADSIM_JOINT) &&
+                Rmax < kRecMaxReq && model->decode_per_ctx_tok_s == 0.0 && ctx->tune.wide_path != 0;
+    if (ctx->wide) {
+        int r_ = plan_wide(ctx, model, slo, n_qps, n_traces, Rmax, cands);
+        if (r_) return r_;
+    }
     // replay launch plans for the joint kernel (dynamic candidates; static ones when N > 8)
     for (int dyn = 0; dyn < 2; dyn++) {
-        if (!dyn && ctx->fact) { std::memset(&ctx->plan_static, 0, sizeof(Plan)); continue; }
+        if (!dyn && (ctx->fact || ctx->wide)) { std::memset(&ctx->plan_static, 0, sizeof(Plan)); continue; }
         const std::vector<int>& lst = dyn ? ctx->dyn_list : ctx->static_list;
         Plan& P = dyn ? ctx->plan_dyn : ctx->plan_static;
         std::memset(&P, 0, sizeof(P));
@@ -1302,7 +1446,7 @@ int padsim_run(padsim_ctx* ctx, void* stream) {
     const bool any_joint = ctx->plan_dyn.n_clist > 0 || ctx->plan_static.n_clist > 0 ||
                            ctx->plan_coal.n_clist > 0;
     const bool ser = ctx->tune.serialize != 0;     // every kernel on `st`, one after another
-    cudaStream_t js = ctx->fact && any_joint && !ser ? ctx->side : st;
+    cudaStream_t js = (ctx->fact || ctx->wide) && any_joint && !ser ? ctx->side : st;
     if (js != st) CK(cudaStreamWaitEvent(js, ctx->j_with_a ? ctx->ev0 : ctx->evA, 0));
     CK(cudaEventRecord(ctx->evJ0, js));
     for (int dyn = 0; dyn < 2; dyn++) {
@@ -1366,6 +1510,34 @@ int padsim_run(padsim_ctx* ctx, void* stream) {
             CK(cudaStreamWaitEvent(st, ctx->evCk[kc], 0));
         }
     }
+    if (ctx->wide) {          // wide nodes: stage A → stage C per chunk of traces
+        CK(cudaMemsetAsync(ctx->d_workW, 0, (size_t)2 * ctx->S * sizeof(unsigned), st));
+        const int nch = (ctx->S + ctx->w_chunk - 1) / ctx->w_chunk;
+        while ((int)ctx->evW.size() < 4 * nch) {
+            cudaEvent_t e;
+            CK(cudaEventCreate(&e));
+            ctx->evW.push_back(e);
+        }
+        ctx->n_wchunks = nch;
+        for (int kch = 0; kch < nch; kch++) {
+            const int s0 = kch * ctx->w_chunk;
+            FPlan F = ctx->fplan;
+            F.s_begin = s0;
+            F.s_count = std::min(ctx->w_chunk, ctx->S - s0);
+            const int gA = ctx->wA_grid / ctx->w_chunk * F.s_count;
+            const int gC = ctx->wC_grid / ctx->w_chunk * F.s_count;
+            F.work = ctx->d_workW;
+            CK(cudaEventRecord(ctx->evW[4 * kch], st));
+            stageA_wide_kernel<<<gA, kThreads, 0, st>>>(F);
+            CK(cudaGetLastError());
+            CK(cudaEventRecord(ctx->evW[4 * kch + 1], st));
+            F.work = ctx->d_workW + ctx->S;
+            stageC_wide_kernel<<<gC, kThreads, 0, st>>>(F);
+            CK(cudaGetLastError());
+            CK(cudaEventRecord(ctx->evW[4 * kch + 2], st));
+            launches += 2;
+        }
+    }
     CK(cudaEventRecord(ctx->evC, st));
     if (js != st) CK(cudaStreamWaitEvent(st, ctx->evJ1, 0));   // join
     CK(cudaEventRecord(ctx->ev1, st));
@@ -1394,7 +1566,7 @@ int padsim_launch_count(padsim_ctx* ctx, int32_t* n) {
 
 int padsim_set_tuning(padsim_ctx* ctx, const padsim_tuning* t) {
     if (!ctx) return PADSIM_EINVAL;
-    if (!t) { ctx->tune = padsim_tuning{0, 0, -1, 0, -1, 0, -1, 0, -1}; return PADSIM_OK; }
+    if (!t) { ctx->tune = padsim_tuning{0, 0, -1, 0, -1, 0, -1, 0, -1, -1, 0}; return PADSIM_OK; }
     if ((t->stage_a_threads != 0 && t->stage_a_threads != 32 && t->stage_a_threads != kThreads &&
          t->stage_a_threads != kATbBig) ||
         (t->stage_c_classes != 0 && t->stage_c_classes != 3 && t->stage_c_classes != 5) ||
@@ -1402,7 +1574,8 @@ int padsim_set_tuning(padsim_ctx* ctx, const padsim_tuning* t) {
         (t->joint_threads != 0 && t->joint_threads != 32 && t->joint_threads != kThreads) ||
         t->joint_reg_cap < -1 || t->joint_reg_cap > 1 || t->joint_lanes_per_warp < 0 ||
         t->joint_lanes_per_warp > 32 || t->joint_after_stage_a < -1 || t->joint_after_stage_a > 1 ||
-        t->serialize < 0 || t->serialize > 1 || t->joint_groups < -1 || t->joint_groups > 1)
+        t->serialize < 0 || t->serialize > 1 || t->joint_groups < -1 || t->joint_groups > 1 ||
+        t->wide_path < -1 || t->wide_path > 1 || t->wide_chunk < 0)
         return fail(ctx, PADSIM_EINVAL, "tuning value out of range");
     ctx->tune = *t;
     return PADSIM_OK;
@@ -1434,7 +1607,7 @@ int padsim_get_device_results(padsim_ctx* ctx, padsim_device_results* o) {
     o->d_rep_events = (int64_t*)ctx->d_rep_events;
     o->n_cand = ctx->C; o->n_qps = ctx->Q; o->n_traces = ctx->S;
     o->d_aux_events = (int64_t*)ctx->d_evA;
-    o->n_aux_events = ctx->fact ? ctx->n_evA : 0;
+    o->n_aux_events = (ctx->fact || ctx->wide) ? ctx->n_evA : 0;
     return PADSIM_OK;
 }
 
@@ -1535,6 +1708,16 @@ int padsim_kernel_times_ms(padsim_ctx* ctx, float* ms3) {
     CK(cudaEventElapsedTime(&ms3[0], ctx->ev0, ctx->evA));
     CK(cudaEventElapsedTime(&ms3[1], ctx->evC0, ctx->evC));
     CK(cudaEventElapsedTime(&ms3[2], ctx->evJ0, ctx->evJ1));
+    if (ctx->wide) {        // wide nodes: Σ over the chunks' stage A / stage C launches
+        ms3[0] = ms3[1] = 0.f;
+        for (int k = 0; k < ctx->n_wchunks; k++) {
+            float a = 0.f, c = 0.f;
+            CK(cudaEventElapsedTime(&a, ctx->evW[4 * k], ctx->evW[4 * k + 1]));
+            CK(cudaEventElapsedTime(&c, ctx->evW[4 * k + 1], ctx->evW[4 * k + 2]));
+            ms3[0] += a;
+            ms3[1] += c;
+        }
+    }
     return PADSIM_OK;
 }
 

@@ -138,6 +138,9 @@ struct FPlan {
     int c_prefetch;         // prefetch the completion record into L2 at decode join
     float sync_win;         // lane clock window in mean inter-arrival times (0 = off)
     int smem_trace;
+    // wide nodes (8 < N ≤ 64, wide_path.cuh): caps of up to 64 workers per role
+    const int* w_gcap;      // [G][64] prefill caps of each group, P-id order
+    const int* w_dcap;      // [n_cc][64] decode caps of each candidate, D-id order
     // outputs (r = (c*Q + q)*S + s)
     int* rep_met;
     int* rep_near;
