@@ -17,9 +17,11 @@
 // ≤ 32 KV transfer slots of stage A are one per lane.  Per-worker passes run
 // lane-parallel: the dispatch pass (each touched worker forms its batch /
 // segment on its own lane).  Queues (prompt FIFOs, KV-wait FIFO, pending
-// joins) are linked through a per-replay `link` array; decode batches are
-// per-worker lists sorted by (finish step, stream index) with each member's
-// completion record copied next to its entry (a leave loads both together).
+// joins) are linked through a per-replay `link` array; a decode batch is an
+// unsorted per-worker array of (finish step, stream index) entries: a join
+// appends (one store), a leave scans the array lane-parallel (one coalesced
+// load per 32 members), scores the leavers and compacts the rest, and the next
+// finish step is a warp min — no sorted insertion, no dependent load chain.
 // Same semantics and operation order as the oracle (DESIGN.md §3 c.2).
 #pragma once
 #include <cuda_runtime.h>
@@ -60,7 +62,7 @@ template <class V> __device__ __forceinline__ void w_put(V (&a)[2], int j, V v) 
 
 // per-warp scratch of the wide stages
 struct WScratchA { size_t link, bytes; };
-struct WScratchC { size_t link, ring, rrec, bytes; };
+struct WScratchC { size_t link, bat, bytes; };
 __host__ __device__ inline WScratchA wide_a_layout(size_t R) {
     WScratchA L{};
     L.link = 0;
@@ -72,8 +74,7 @@ __host__ __device__ inline WScratchC wide_c_layout(size_t R, int RB) {
     size_t off = 0;
     auto take = [&](size_t b) { const size_t o = off; off += (b + 255) & ~(size_t)255; return o; };
     L.link = take(R * sizeof(int));
-    L.ring = take((size_t)kWMax * RB * sizeof(unsigned long long));
-    L.rrec = take((size_t)kWMax * RB * sizeof(SRec));
+    L.bat = take((size_t)kWMax * RB * sizeof(unsigned long long));
     L.bytes = off;
     return L;
 }
@@ -269,12 +270,12 @@ __global__ void __launch_bounds__(kThreads) stageA_wide_kernel(const __grid_cons
 // One decode worker of stage C (wide), held in the registers of its lane.
 struct WDec {
     double tn, tseg, L;
-    int nact, ql, qh, qt, stm, nxs, st0, mfin, bf, ci;
+    int nact, ql, qh, qt, stm, nxs, st0, mfin, ci;
     bool on;
     __device__ __forceinline__ void init(bool o, int cap_idx) {
         on = o; ci = cap_idx;
         tn = PAD_INF; tseg = 0.0; L = 1.0;
-        nact = 0; ql = 0; qh = qt = kNoIdx; stm = 0; nxs = 0; st0 = 0; mfin = 0x7fffffff; bf = 0;
+        nact = 0; ql = 0; qh = qt = kNoIdx; stm = 0; nxs = 0; st0 = 0; mfin = 0x7fffffff;
     }
     // A13 routing key: active + pending (~0 = no such worker)
     __device__ __forceinline__ unsigned long long key() const {
@@ -293,11 +294,10 @@ struct WDec {
         }
     }
     // dispatch at t (idle, at a boundary, or a join boundary exactly at t): admit
-    // pending joins into the sorted batch list, start a new segment if the batch
-    // changed
+    // pending joins (appended to the worker's unsorted batch array: one store, no
+    // load), start a new segment if the batch changed
     __device__ __forceinline__ void dispatch(double t, bool ab, bool changed, int max_db, const int* link,
-                                             const SRec* recs, unsigned long long* rg, SRec* rr, int RBm,
-                                             const double* ltab) {
+                                             const SRec* recs, unsigned long long* bw, const double* ltab) {
         int n = nact;
         if (n > 0 && !ab) {
             if (tn != t) return;               // mid-step
@@ -311,26 +311,12 @@ struct WDec {
         const int step = stm;
         int mf = mfin;
         int h = qh;
-        const int f = bf;
         while (n < max_db && qn > 0) {
             const int kk = h;
             qn--;
             if (qn > 0) h = link[kk];
-            const SRec rc = recs[kk];
-            const int fin = step + ((rc.meta & 0x7fffffff) - 1);
-            // insert (fin, kk) and its record into the sorted list from the back
-            const unsigned long long e = ((unsigned long long)(unsigned)fin << 32) | (unsigned)kk;
-            int z = n;
-            while (z > 0) {
-                const int zp = (f + z - 1) & RBm;
-                const unsigned long long pv = rg[zp];
-                if (pv < e) break;
-                rg[(f + z) & RBm] = pv;
-                rr[(f + z) & RBm] = rr[zp];
-                z--;
-            }
-            rg[(f + z) & RBm] = e;
-            rr[(f + z) & RBm] = rc;
+            const int fin = step + ((recs[kk].meta & 0x7fffffff) - 1);
+            bw[n] = ((unsigned long long)(unsigned)fin << 32) | (unsigned)kk;
             n++;
             mf = fin < mf ? fin : mf;
             joined = true;
@@ -364,13 +350,12 @@ __global__ void __launch_bounds__(kThreads) stageC_wide_kernel(const __grid_cons
     const int s = P.s_begin + sl;
     const long long off = P.toff[s];
     const int R = P.nreq[s];
-    const int RB = P.c_rb, RBm = P.c_rb - 1;
+    const int RB = P.c_rb;
     const int max_db = P.m.max_db;
     char* wb = P.scrC + ((size_t)blockIdx.x * kWarps + warp) * P.c_warp_bytes;
     const WScratchC L = wide_c_layout((size_t)P.Rmax, RB);
     int* link = (int*)(wb + L.link);
-    unsigned long long* ring = (unsigned long long*)(wb + L.ring);
-    SRec* rrec = (SRec*)(wb + L.rrec);
+    unsigned long long* bat = (unsigned long long*)(wb + L.bat);   // [worker][RB] (fin << 32 | k), unsorted
     const int QC = P.Q * P.n_cc;
     for (;;) {
         int item = 0;
@@ -441,26 +426,35 @@ __global__ void __launch_bounds__(kThreads) stageC_wide_kernel(const __grid_cons
                     if (wj) { W1.stm = sN; W1.tn = PAD_INF; } else { W0.stm = sN; W0.tn = PAD_INF; }
                 }
                 if (sN != mf0) continue;
+                // the members finishing at step sN leave: the worker's batch array is
+                // scanned lane-parallel (32 entries per load), the leavers scored in
+                // array order (completion order at one instant changes nothing), the
+                // rest compacted to the front, the next finish step a warp min
                 const int n0 = __shfl_sync(kFull, wj ? W1.nact : W0.nact, wl);
-                int f = __shfl_sync(kFull, wj ? W1.bf : W0.bf, wl);
-                const unsigned long long* rg = ring + (size_t)w * RB;
-                const SRec* rr = rrec + (size_t)w * RB;
+                unsigned long long* bw = bat + (size_t)w * RB;
                 int left = 0;
-                unsigned long long e = rg[f];
-                SRec rc = rr[f];
-                for (;;) {
-                    complete(rc, t, (t - rc.pe) / (double)((rc.meta & 0x7fffffff) - 1));
-                    left++;
-                    f = (f + 1) & RBm;
-                    if (left == n0) break;
-                    e = rg[f];
-                    rc = rr[f];
-                    if ((int)(e >> 32) != sN) break;
+                unsigned mfm = 0x7fffffffu;
+                for (int b0 = 0; b0 < n0; b0 += 32) {
+                    const int idx = b0 + lane;
+                    const bool ok = idx < n0;
+                    const unsigned long long e = ok ? bw[idx] : 0ull;
+                    const bool lv = ok && (int)(e >> 32) == sN;
+                    const unsigned ml = __ballot_sync(kFull, lv);
+                    const unsigned mr = __ballot_sync(kFull, ok && !lv);
+                    mfm = min(mfm, __reduce_min_sync(kFull, ok && !lv ? (unsigned)(e >> 32) : 0x7fffffffu));
+                    __syncwarp();
+                    if (ok && !lv) bw[b0 - left + __popc(mr & ((1u << lane) - 1u))] = e;
+                    for (unsigned mm = ml; mm; mm &= mm - 1) {
+                        const int kk = __shfl_sync(kFull, (int)(unsigned)e, __ffs(mm) - 1);
+                        const SRec rc = recs[kk];
+                        complete(rc, t, (t - rc.pe) / (double)((rc.meta & 0x7fffffff) - 1));
+                    }
+                    left += __popc(ml);
                 }
-                const int mf = left < n0 ? (int)(e >> 32) : 0x7fffffff;
                 if (lane == wl) {
                     WDec& X = wj ? W1 : W0;
-                    X.bf = f; X.nact = n0 - left; X.mfin = mf;
+                    X.nact = n0 - left;
+                    X.mfin = n0 - left > 0 ? (int)mfm : 0x7fffffff;
                 }
                 chg |= 1ull << w;
             }
@@ -491,10 +485,10 @@ __global__ void __launch_bounds__(kThreads) stageC_wide_kernel(const __grid_cons
             const unsigned long long dm = bd | touched;
             if ((dm >> lane) & 1ull)
                 W0.dispatch(t, (bd >> lane) & 1ull, (chg >> lane) & 1ull, max_db, link, recs,
-                            ring + (size_t)lane * RB, rrec + (size_t)lane * RB, RBm, P.m.ltab);
+                            bat + (size_t)lane * RB, P.m.ltab);
             if ((dm >> (lane + 32)) & 1ull)
                 W1.dispatch(t, (bd >> (lane + 32)) & 1ull, (chg >> (lane + 32)) & 1ull, max_db, link, recs,
-                            ring + (size_t)(lane + 32) * RB, rrec + (size_t)(lane + 32) * RB, RBm, P.m.ltab);
+                            bat + (size_t)(lane + 32) * RB, P.m.ltab);
             __syncwarp();
         }
         if (lane == 0) {

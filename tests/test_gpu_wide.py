@@ -87,6 +87,11 @@ def test_wide_matches_joint_kernel_and_extras(pkg):
         for k in a:
             if k == "events":        # DES instants: the factorized path counts stage C's only
                 continue
+            if k in ("rep_queue", "rep_exec", "sum_queue", "sum_exec"):
+                # Fig. 6 sums: stage A adds member by member, the joint kernel batch by
+                # batch (A38; test_gpu_decomposition.py holds both to the oracle at 1e-9)
+                assert np.allclose(np.asarray(a[k]), np.asarray(b[k]), rtol=1e-9, atol=0), k
+                continue
             assert np.array_equal(np.asarray(a[k]), np.asarray(b[k])), k
     ref = oracle.evaluate(DEFAULT_MODEL, role, cap, pols, 38400, DEFAULT_SLO, traces, qps, n_threads=8)
     assert np.array_equal(outs[0][0]["met"], ref["met"])

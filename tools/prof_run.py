@@ -16,6 +16,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="cfg2")
 ap.add_argument("--traces", type=int, default=0, help="limit traces (0 = all)")
 ap.add_argument("--runs", type=int, default=2)
+ap.add_argument("--cand-stride", type=int, default=1, help="every k-th candidate only")
 a = ap.parse_args()
 
 import paper_2601_12241_b200 as pkg  # noqa: E402
@@ -26,6 +27,10 @@ cfg = get_config(a.config)
 role, cap, pols, traces, qps, cb = build_workload(cfg, 0, pkg.enumerate_pool_uniform)
 if a.traces:
     traces = traces[: a.traces]
+if a.cand_stride > 1:
+    role, cap = role[:: a.cand_stride], cap[:: a.cand_stride]
+    pols = pols[:: a.cand_stride]
+    cb = None if cb is None else cb[:: a.cand_stride]
 ctx = pkg.Context(0)
 ctx.plan(traces, qps, DEFAULT_MODEL, role, cap, pols, cfg["slo"], cfg["budget_w"], cand_budget_w=cb)
 for _ in range(a.runs):

@@ -20,6 +20,8 @@ from workloads import DEFAULT_MODEL, get_config  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="cfg3")
 ap.add_argument("--runs", type=int, default=3)
+ap.add_argument("--traces", type=int, default=0, help="limit traces (0 = all)")
+ap.add_argument("--cand-stride", type=int, default=1, help="every k-th candidate only")
 ap.add_argument("tunings", nargs="+")
 a = ap.parse_args()
 
@@ -29,6 +31,11 @@ from paper_2601_12241_b200.build import build  # noqa: E402
 build()
 cfg = get_config(a.config)
 role, cap, pols, traces, qps, cb = build_workload(cfg, 0, pkg.enumerate_pool_uniform)
+if a.traces:
+    traces = traces[: a.traces]
+if a.cand_stride > 1:
+    role, cap, pols = role[:: a.cand_stride], cap[:: a.cand_stride], pols[:: a.cand_stride]
+    cb = None if cb is None else cb[:: a.cand_stride]
 ctxs = []
 for t in a.tunings:
     ctx = pkg.Context(0, tuning=json.loads(t))
