@@ -17,6 +17,7 @@ ap.add_argument("--config", default="cfg2")
 ap.add_argument("--traces", type=int, default=0, help="limit traces (0 = all)")
 ap.add_argument("--runs", type=int, default=2)
 ap.add_argument("--cand-stride", type=int, default=1, help="every k-th candidate only")
+ap.add_argument("--tuning", default="{}", help="padsim_set_tuning overrides (JSON)")
 a = ap.parse_args()
 
 import paper_2601_12241_b200 as pkg  # noqa: E402
@@ -31,7 +32,8 @@ if a.cand_stride > 1:
     role, cap = role[:: a.cand_stride], cap[:: a.cand_stride]
     pols = pols[:: a.cand_stride]
     cb = None if cb is None else cb[:: a.cand_stride]
-ctx = pkg.Context(0)
+import json  # noqa: E402
+ctx = pkg.Context(0, tuning=json.loads(a.tuning))
 ctx.plan(traces, qps, DEFAULT_MODEL, role, cap, pols, cfg["slo"], cfg["budget_w"], cand_budget_w=cb)
 for _ in range(a.runs):
     ctx.run()
