@@ -66,7 +66,9 @@ def requests_per_kernel(wl):
     if cfg["n_gpus"] <= 8:
         return {"stageA_kernel": len(groups) * Q * r_sum, "stageC_kernel": len(st) * Q * r_sum,
                 "joint_kernel": (C - len(st)) * Q * r_sum}
-    return {"joint_kernel": C * Q * r_sum}
+    # N > 8: static candidates on the wide-node factorized path, dynamic ones on the joint kernel
+    return {"stageA_wide_kernel": len(groups) * Q * r_sum, "stageC_wide_kernel": len(st) * Q * r_sum,
+            "joint_kernel": (C - len(st)) * Q * r_sum}
 
 
 def main():
