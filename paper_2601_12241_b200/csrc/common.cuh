@@ -45,7 +45,7 @@ struct DevModel {
 
 // Prefetch (to L2) of the timing-wheel head of a decode worker's next finish
 // bucket, issued when that bucket becomes known and read at the next leave.
-// A/B on one box (tools/run_ab.sh): cfg 4 785 -> 770 ms/step; an L1 prefetch
+// A/B on one box (tools/call_ab.sh): cfg 4 785 -> 770 ms/step; an L1 prefetch
 // (773 ms), keeping the head in registers (807 ms) and deciding the TPOT tests
 // without the FP64 division (814 ms) were no better.
 __device__ __forceinline__ void pf_head(const void* p) {

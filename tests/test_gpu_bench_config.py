@@ -63,3 +63,43 @@ def test_cfg4_full_grid_declared_subset(pkg):
 def test_cfg3_full_grid_subset(pkg):
     ms = _subset_parity(pkg, "cfg3", 2)
     assert ms[2] > 0
+
+
+def test_cfg5_full_grid_sampled(pkg):
+    # cfg 5 (64 GPUs, 38.4 kW, 8443 static candidates x 8 QPS x 4 traces of 100 000
+    # requests) in the launch configuration bench.py times — the wide-node factorized
+    # path, stream chunked by traces — and the oracle recomputing a sample of replays
+    # (every prefill-pool size band, both trace mixes, low and high load) one by one
+    from bench import build_workload
+    cfg = get_config("cfg5")
+    role, cap, pols, traces, qps, cb = build_workload(cfg, 0, pkg.enumerate_pool_uniform)
+    ctx = pkg.Context(0)
+    try:
+        ctx.plan(traces, qps, DEFAULT_MODEL, role, cap, pols, cfg["slo"], cfg["budget_w"])
+        ctx.run()
+        res = ctx.fetch()
+        rep = ctx.fetch_replays()
+        ms = ctx.kernel_times_ms()
+    finally:
+        ctx.close()
+    assert ms[0] > 0 and ms[1] > 0            # stage A / stage C (wide) ran
+    C, Q, S = role.shape[0], len(qps), len(traces)
+    rng = np.random.default_rng(5)
+    picks = [(int(c), int(rng.integers(Q)), s) for s in range(S)
+             for c in np.linspace(0, C - 1, 4).astype(int)]
+    import concurrent.futures as cf
+
+    def one(k):
+        c, q, s = k
+        return k, oracle.replay(DEFAULT_MODEL, role[c], cap[c], pols[c], cfg["budget_w"], cfg["slo"],
+                                traces[s], qps[q])
+    with cf.ThreadPoolExecutor(max_workers=os.cpu_count() or 1) as ex:
+        for (c, q, s), o in ex.map(one, picks):
+            assert rep["met"][c, q, s] == o["met"], (c, q, s)
+            assert rep["duration"][c, q, s] == o["duration"], (c, q, s)
+            assert rep["goodput"][c, q, s] == o["goodput"], (c, q, s)
+    assert np.array_equal(res["met"], rep["met"].sum(axis=2))
+    capsum = cap.sum(axis=1)
+    for q in range(Q):
+        key = np.lexsort((np.arange(C), capsum, -res["met"][:, q]))
+        assert res["argmax"][q] == key[0]
