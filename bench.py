@@ -245,7 +245,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="cfg4")
     ap.add_argument("--impl", default="padsim", choices=["padsim", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
@@ -397,7 +397,8 @@ def main():
                                ctx=ctx, device=local, cand_budget_w=cand_budget)
         if k > 0:
             e2e_times.append(time.perf_counter() - t0)
-    e2e_t = max_over_ranks(float(np.mean(e2e_times)) if e2e_times else float("nan"), device=dev)
+    # median over the e2e steps (host wall clock includes OS / driver jitter), max over ranks
+    e2e_t = max_over_ranks(float(np.median(e2e_times)) if e2e_times else float("nan"), device=dev)
     del out
 
     if rank == 0:
@@ -426,7 +427,8 @@ def main():
                        "replays_rank0": Cl * Ql * S, "l2": "flushed between steps (512 MiB write)"},
             "sim_req_per_s": value * r_sum / S,
             "e2e": {"value": units / e2e_t, "unit": "evals/s", "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": int(d2h), "api": "evaluate_sharded -> padsim_evaluate_allocations"},
+                    "d2h_bytes_per_step": int(d2h), "api": "evaluate_sharded -> padsim_evaluate_allocations",
+                    "steps": len(e2e_times), "stat": "median"},
             "gpu_launches": launches,
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak_fp64, "unit": "TFLOP/s",
                          "frac": achieved / peak_fp64,

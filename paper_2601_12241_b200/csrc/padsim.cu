@@ -149,7 +149,8 @@ struct padsim_ctx {
     // factorized static path for wide nodes (8 < N ≤ 64, wide_path.cuh)
     bool wide = false;
     int w_chunk = 1;               // traces per stage A → C chunk (stream buffers sized for it)
-    int wA_grid = 0, wC_grid = 0;  // CTAs per chunk
+    int wA_grid = 0, wC_grid = 0;  // resident CTAs available to a launch (scratch slots)
+    long long wA_items = 0, wC_items = 0;   // warp items per trace (stage A, stage C)
     unsigned* d_workW = nullptr;   // work counters [2][S] (stage A, stage C)
     std::vector<cudaEvent_t> evW;  // per chunk: stage A start/stop, stage C start/stop
     int n_wchunks = 0;             // chunks of the last run
@@ -849,6 +850,10 @@ static int plan_wide(padsim_ctx* ctx, const padsim_model* model, const padsim_sl
     int chunk = (int)std::min<size_t>((size_t)S, std::max<size_t>(1, budget / std::max<size_t>(per_trace, 1)));
     if (ctx->tune.wide_chunk > 0) chunk = std::min(S, (int)ctx->tune.wide_chunk);
     chunk = std::max(chunk, 1);
+    if (S > 0) {        // balanced chunks (cfg 5: 2 + 2 traces rather than 3 + 1)
+        const int nch = (S + chunk - 1) / chunk;
+        chunk = (S + nch - 1) / nch;
+    }
     ctx->w_chunk = chunk;
     const long long GQC = (long long)G * Q * chunk;
 #define AL(p, n) do { int r_ = dalloc(ctx, &(p), (size_t)(n)); if (r_) return r_; } while (0)
@@ -880,21 +885,24 @@ static int plan_wide(padsim_ctx* ctx, const padsim_model* model, const padsim_sl
     AL(ctx->d_workW, (size_t)2 * S);
     // one warp per replay; CTAs (4 warps) bound to one trace of the chunk, warps pull
     // replays from that trace's counter; scratch per resident warp
-    auto grid_of = [&](const void* fn, long long items, size_t warp_bytes, long long& grid) -> int {
+    // resident CTAs of a launch (the whole GPU, capped by a scratch budget of 20 % of the
+    // free memory, at least one per trace of a chunk); padsim_run splits them over the
+    // traces of each chunk, so a short last chunk still fills the GPU
+    auto grid_of = [&](const void* fn, size_t warp_bytes, long long& grid) -> int {
         int occ = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, 0));
         occ = std::max(occ, 1);
-        long long per_tr = std::max<long long>(1, ((long long)ctx->n_sm * occ) / chunk);
-        per_tr = std::min<long long>(per_tr, (items + kWarps - 1) / kWarps);
-        const long long cap = std::max<long long>(1, (long long)((double)fr * 0.2 / ((double)warp_bytes * kWarps * chunk)));
-        grid = std::max<long long>(1, std::min(per_tr, cap)) * chunk;
+        const long long cap = std::max<long long>(1, (long long)((double)fr * 0.2 / ((double)warp_bytes * kWarps)));
+        grid = std::max<long long>(chunk, std::min<long long>((long long)ctx->n_sm * occ, cap));
         return PADSIM_OK;
     };
     long long ga = 0, gc = 0;
-    if (int r_ = grid_of((const void*)stageA_wide_kernel, (long long)Q * G, F.a_warp_bytes, ga)) return r_;
-    if (int r_ = grid_of((const void*)stageC_wide_kernel, (long long)Q * NC, F.c_warp_bytes, gc)) return r_;
+    if (int r_ = grid_of((const void*)stageA_wide_kernel, F.a_warp_bytes, ga)) return r_;
+    if (int r_ = grid_of((const void*)stageC_wide_kernel, F.c_warp_bytes, gc)) return r_;
     ctx->wA_grid = (int)ga;
     ctx->wC_grid = (int)gc;
+    ctx->wA_items = (long long)Q * G;
+    ctx->wC_items = (long long)Q * NC;
     char *sa, *sc;
     AL(sa, (size_t)ga * kWarps * F.a_warp_bytes);
     AL(sc, (size_t)gc * kWarps * F.c_warp_bytes);
@@ -1524,8 +1532,15 @@ int padsim_run(padsim_ctx* ctx, void* stream) {
             FPlan F = ctx->fplan;
             F.s_begin = s0;
             F.s_count = std::min(ctx->w_chunk, ctx->S - s0);
-            const int gA = ctx->wA_grid / ctx->w_chunk * F.s_count;
-            const int gC = ctx->wC_grid / ctx->w_chunk * F.s_count;
+            // CTAs bound to one trace each: the launch's resident CTAs split over the
+            // chunk's traces, no more per trace than its items need
+            auto grid_for = [&](int tot, long long items) {
+                long long per = std::max<long long>(1, tot / F.s_count);
+                per = std::min<long long>(per, std::max<long long>(1, (items + kWarps - 1) / kWarps));
+                return (int)(per * F.s_count);
+            };
+            const int gA = grid_for(ctx->wA_grid, ctx->wA_items);
+            const int gC = grid_for(ctx->wC_grid, ctx->wC_items);
             F.work = ctx->d_workW;
             CK(cudaEventRecord(ctx->evW[4 * kch], st));
             stageA_wide_kernel<<<gA, kThreads, 0, st>>>(F);

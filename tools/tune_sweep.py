@@ -36,21 +36,19 @@ if a.traces:
 if a.cand_stride > 1:
     role, cap, pols = role[:: a.cand_stride], cap[:: a.cand_stride], pols[:: a.cand_stride]
     cb = None if cb is None else cb[:: a.cand_stride]
-ctxs = []
-for t in a.tunings:
-    ctx = pkg.Context(0, tuning=json.loads(t))
-    ctx.plan(traces, qps, DEFAULT_MODEL, role, cap, pols, cfg["slo"], cfg["budget_w"], cand_budget_w=cb)
-    ctx.run()                                  # warm-up
-    ctxs.append(ctx)
-ms = [[] for _ in ctxs]
+# one context at a time (each plans its scratch against the free device memory),
+# tunings interleaved round by round
+ms = [[] for _ in a.tunings]
+met = [None for _ in a.tunings]
 for _ in range(a.runs):
-    for j, ctx in enumerate(ctxs):
+    for j, t in enumerate(a.tunings):
+        ctx = pkg.Context(0, tuning=json.loads(t))
+        ctx.plan(traces, qps, DEFAULT_MODEL, role, cap, pols, cfg["slo"], cfg["budget_w"], cand_budget_w=cb)
+        ctx.run()                                  # warm-up
         ctx.run()
         ms[j].append(ctx.replay_kernel_ms())
-ref = ctxs[0].fetch()["met"]
-for t, ctx, m in zip(a.tunings, ctxs, ms):
-    same = bool((ctx.fetch()["met"] == ref).all())
+        met[j] = ctx.fetch()["met"]
+        ctx.close()
+for t, m, mt in zip(a.tunings, ms, met):
     print(json.dumps({"config": a.config, "tuning": json.loads(t), "ms": statistics.median(m),
-                      "all_ms": m, "met_equal": same}))
-for ctx in ctxs:
-    ctx.close()
+                      "all_ms": m, "met_equal": bool((mt == met[0]).all())}))
