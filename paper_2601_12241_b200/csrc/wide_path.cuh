@@ -33,6 +33,17 @@
 namespace padsim {
 
 constexpr int kWMax = 64;                  // worker slots (2 per lane)
+// resident CTAs per SM the compiler targets (register budget): stage C 8 → 64
+// registers, 32 warps per SM (cfg 5: 23.5 → 22.0 s/step against the default 96
+// registers / 20 warps; a replay per warp is latency-bound, more warps hide more;
+// 10 → 48 registers spills 200 B: 24.3 s); stage A 6 → 80 registers (21.96 s vs
+// 22.0-22.5 s at 64 / 130 registers)
+#ifndef PADSIM_WIDE_MINB
+#define PADSIM_WIDE_MINB 8
+#endif
+#ifndef PADSIM_WIDEA_MINB
+#define PADSIM_WIDEA_MINB 6
+#endif
 constexpr unsigned kFull = 0xffffffffu;
 
 __device__ __forceinline__ unsigned long long w_min_u64(unsigned long long v) {
@@ -83,7 +94,7 @@ __host__ __device__ inline WScratchC wide_c_layout(size_t R, int RB) {
 // stage A (wide): prefill workers + KV buffer → transfer-end stream, one warp
 // per (prefill group, QPS) of the CTA's trace.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads) stageA_wide_kernel(const __grid_constant__ FPlan P) {
+__global__ void __launch_bounds__(kThreads, PADSIM_WIDEA_MINB) stageA_wide_kernel(const __grid_constant__ FPlan P) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int sl = blockIdx.x % P.s_count;
     const int s = P.s_begin + sl;
@@ -344,7 +355,7 @@ struct WDec {
 // stage C (wide): decode workers consume the transfer-end stream (A13, A14),
 // one warp per (candidate, QPS) of the CTA's trace.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads) stageC_wide_kernel(const __grid_constant__ FPlan P) {
+__global__ void __launch_bounds__(kThreads, PADSIM_WIDE_MINB) stageC_wide_kernel(const __grid_constant__ FPlan P) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int sl = blockIdx.x % P.s_count;
     const int s = P.s_begin + sl;
