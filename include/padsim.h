@@ -251,6 +251,18 @@ int padsim_fetch_records(padsim_ctx* ctx, void* stream, double* ttft, double* tp
                          double* prefill_end, double* completion, double* transfer_end,
                          int32_t* r_max);
 
+/* One candidate x one trace x one QPS point, per-request records (SURVEY §8(b)
+ * parity/debug helper; the same kernels as padsim_evaluate_allocations): plans
+ * `ctx` with PADSIM_RECORDS for cands->n_cand == 1, runs it on the ctx's stream
+ * and copies the records of the replay to the caller's buffers, each
+ * [trace->n_req] doubles (any may be NULL):  ttft = prefill_end − arrival,
+ * tpot = (completion − prefill_end)/(out−1), 0 for out = 1 (A7), prefill_end,
+ * completion.  Errors as padsim_plan (EINVAL if n_cand != 1).  Re-plans ctx. */
+int padsim_replay_records(padsim_ctx* ctx, const padsim_trace* trace, double qps_per_gpu,
+                          const padsim_model* model, const padsim_candidates* one,
+                          const padsim_slo* slo, const padsim_budget* budget, double* ttft,
+                          double* tpot, double* prefill_end, double* completion);
+
 /* ---- Fig. 6 TTFT decomposition, percentiles ----------
  * padsim_fetch_decomposition (synchronises; any pointer may be NULL):
  *   rep_queue[r], rep_exec[r]   r = (c*Q + q)*S + s: Σ over the replay's

@@ -5,6 +5,7 @@ The product is the CUDA library ``libpadsim.so`` (C ABI: include/padsim.h);
 ``binding`` is its thin ctypes binding.  Nothing here imports ``oracle``.
 """
 from .binding import (Context, PadsimError, enumerate_pool_uniform,  # noqa: F401
-                      evaluate_allocations, load)
+                      evaluate_allocations, load, replay_records)
 
-__all__ = ["Context", "PadsimError", "enumerate_pool_uniform", "evaluate_allocations", "load"]
+__all__ = ["Context", "PadsimError", "enumerate_pool_uniform", "evaluate_allocations", "load",
+           "replay_records"]

@@ -125,7 +125,8 @@ EXPORTS = ["padsim_create", "padsim_destroy", "padsim_last_error", "padsim_versi
            "padsim_argmax_device", "padsim_step_controller", "padsim_controller_decide_device",
            "padsim_set_tuning", "padsim_launch_count", "padsim_enumerate_pool_uniform",
            "padsim_replay_kernel_ms", "padsim_kernel_times_ms", "padsim_set_slo_sweep",
-           "padsim_fetch_extras", "padsim_fetch_decomposition", "padsim_fetch_percentiles"]
+           "padsim_fetch_extras", "padsim_fetch_decomposition", "padsim_fetch_percentiles",
+           "padsim_replay_records"]
 
 _lib = None
 _P = C.POINTER
@@ -152,6 +153,8 @@ def load(path: str = LIB_PATH):
     L.padsim_plan.argtypes = [vp, _P(Trace), C.c_int32, _P(C.c_double), C.c_int32, _P(Model),
                               _P(Candidates), _P(Slo), _P(Budget), C.c_uint32, _P(C.c_int32)]
     L.padsim_run.argtypes = [vp, vp]
+    L.padsim_replay_records.argtypes = [vp, _P(Trace), C.c_double, _P(Model), _P(Candidates), _P(Slo),
+                                        _P(Budget)] + [_P(C.c_double)] * 4
     L.padsim_fetch.argtypes = [vp, vp, _P(Result)]
     L.padsim_get_device_results.argtypes = [vp, _P(DeviceResults)]
     L.padsim_replay_kernel_ms.argtypes = [vp, _P(C.c_float)]
@@ -500,6 +503,30 @@ def step_controller(policy: dict, model: dict, budget_w: int, state: dict, stats
              flip_deadline=[st.flip_deadline_s[g] for g in range(n)], last_move=st.last_move_s)
     s["raise"] = s.pop("raise_")
     return a, s
+
+
+def replay_records(trace, qps_per_gpu, model, role, cap, policy, slo, budget_w, device=0,
+                   ctx: Context | None = None):
+    """padsim_replay_records: one candidate (role[N], cap[N], policy) on one trace at
+    one QPS point → per-request ttft, tpot, prefill_end, completion (marshalling only)."""
+    own = ctx is None
+    ctx = ctx or Context(device)
+    try:
+        keep = _Keep()
+        tr = make_traces([trace], keep)
+        cands = make_candidates(np.asarray(role).reshape(1, -1), np.asarray(cap).reshape(1, -1),
+                                [policy], keep)
+        R = int(np.asarray(trace["s_unit"]).size)
+        out = {k: np.zeros(max(R, 1), np.float64) for k in ("ttft", "tpot", "prefill_end", "completion")}
+        ctx._check(ctx.L.padsim_replay_records(ctx.ptr, tr, float(qps_per_gpu), C.byref(make_model(model)),
+                                               C.byref(cands), C.byref(make_slo(slo)),
+                                               C.byref(make_budget(budget_w, None, keep)),
+                                               *[_p(out[k], C.c_double) for k in out]), "replay_records")
+        ctx.shape = None                 # the ctx was re-planned for this one replay
+        return {k: v[:R] for k, v in out.items()}
+    finally:
+        if own:
+            ctx.close()
 
 
 def evaluate_allocations(traces, qps, model, role, cap, policies, slo, budget_w, device=0,

@@ -1573,6 +1573,20 @@ int padsim_run(padsim_ctx* ctx, void* stream) {
     return PADSIM_OK;
 }
 
+int padsim_replay_records(padsim_ctx* ctx, const padsim_trace* trace, double qps_per_gpu,
+                          const padsim_model* model, const padsim_candidates* one,
+                          const padsim_slo* slo, const padsim_budget* budget, double* ttft,
+                          double* tpot, double* prefill_end, double* completion) {
+    if (!ctx || !trace || !one) return PADSIM_EINVAL;
+    if (one->n_cand != 1) return fail(ctx, PADSIM_EINVAL, "padsim_replay_records: n_cand must be 1");
+    int32_t bad = -1;
+    int rc = padsim_plan(ctx, trace, 1, &qps_per_gpu, 1, model, one, slo, budget, PADSIM_RECORDS, &bad);
+    if (rc) return rc;
+    rc = padsim_run(ctx, ctx->stream);
+    if (rc) return rc;
+    return padsim_fetch_records(ctx, ctx->stream, ttft, tpot, prefill_end, completion, nullptr, nullptr);
+}
+
 int padsim_launch_count(padsim_ctx* ctx, int32_t* n) {
     if (!ctx || !n) return PADSIM_EINVAL;
     *n = ctx->n_launches;

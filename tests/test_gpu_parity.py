@@ -418,3 +418,21 @@ def test_non_uniform_caps_within_pools(pkg):
     compare_records(traces, [0.75, 2.0], DEFAULT_MODEL, role, cap, pols, DEFAULT_SLO, 4800)
     compare_records(traces[:1], [1.5], DEFAULT_MODEL, role, cap,
                     [policy("dyn-both", cooldown_s=2.0)] * 3, DEFAULT_SLO, 4800)
+
+
+@pytest.mark.parametrize("N,xpd,kind", [(8, (4, 600, 600), "static"), (8, (3, 700, 500), "dyn-both"),
+                                         (16, (9, 650, 500), "static")])
+def test_replay_records_abi(pkg, N, xpd, kind):
+    # padsim_replay_records (SURVEY §8(b) parity helper): one candidate, one trace, one
+    # QPS point through the C ABI — the per-request records are the oracle's, bit for bit
+    role, cap = static_candidates(N, [xpd])
+    pol = policy(kind, cooldown_s=2.0)
+    tr = make_trace("phase" if kind != "static" else "lb", 17, 700)
+    slo = PHASE_SLO if kind != "static" else DEFAULT_SLO
+    got = pkg.replay_records(tr, 2.0, DEFAULT_MODEL, role[0], cap[0], pol, slo, 600 * N)
+    ref = oracle.replay(DEFAULT_MODEL, role[0], cap[0], pol, 600 * N, slo, tr, 2.0)
+    for k in ("ttft", "tpot", "prefill_end", "completion"):
+        assert np.array_equal(got[k], ref[k]), k
+    with pytest.raises(pkg.PadsimError) as e:          # Σ caps over the budget
+        pkg.replay_records(tr, 2.0, DEFAULT_MODEL, role[0], cap[0], pol, slo, 100)
+    assert e.value.rc == -3
