@@ -709,7 +709,7 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
             ctx->kc_grid[kc] = 0;
             if (ctx->kc_n[kc] == 0) continue;
             const int KWc = kc_kw(kc);
-            // batch-list variant per class: PADSIM_BL_MASK (bit kc) overrides the default
+            // batch-list variant per class: padsim_tuning.stage_c_batch_lists (bit kc) overrides the default
             // (measured: the KW = 7 class of large workloads gains from the freed shared
             // memory — 16 instead of 12 resident warps per SM: cfg 4 610 → 584 ms; the
             // others lose — all classes 700 ms, cfg 2's KW = 7 class 46.6 → 47.3 ms)
@@ -1311,7 +1311,7 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
         // next to a large stage C workload the joint replays run as one-warp CTAs
         // capped at 168 registers so they leave registers to stage C (cfg 4 536 →
         // 522 ms); when they are the bulk of the step (cfg 3) the 232-register
-        // variant is faster (327 vs 357 ms).  PADSIM_J_R168=0/1 overrides.
+        // variant is faster (327 vs 357 ms).  padsim_tuning.joint_reg_cap overrides.
         ctx->j_r168 = ctx->fact && ctx->kc_fine && NG == 8 && tbj == 32;
         if (ctx->tune.joint_reg_cap >= 0) ctx->j_r168 = ctx->tune.joint_reg_cap != 0 && NG == 8 && tbj == 32;
         fnj = joint_fn(dyn, tbj, NG, cx, ctx->j_r168);
