@@ -22,6 +22,9 @@ ap.add_argument("--config", default="cfg3")
 ap.add_argument("--runs", type=int, default=3)
 ap.add_argument("--traces", type=int, default=0, help="limit traces (0 = all)")
 ap.add_argument("--cand-stride", type=int, default=1, help="every k-th candidate only")
+ap.add_argument("--qps-stride", type=int, default=1,
+                help="QPS points q with q mod k == offset (one rank's shard of the strong split)")
+ap.add_argument("--qps-offset", type=int, default=0)
 ap.add_argument("tunings", nargs="+")
 a = ap.parse_args()
 
@@ -33,12 +36,15 @@ cfg = get_config(a.config)
 role, cap, pols, traces, qps, cb = build_workload(cfg, 0, pkg.enumerate_pool_uniform)
 if a.traces:
     traces = traces[: a.traces]
+if a.qps_stride > 1:
+    qps = qps[a.qps_offset:: a.qps_stride]
 if a.cand_stride > 1:
     role, cap, pols = role[:: a.cand_stride], cap[:: a.cand_stride], pols[:: a.cand_stride]
     cb = None if cb is None else cb[:: a.cand_stride]
 # one context at a time (each plans its scratch against the free device memory),
 # tunings interleaved round by round
 ms = [[] for _ in a.tunings]
+kms = [None for _ in a.tunings]
 met = [None for _ in a.tunings]
 for _ in range(a.runs):
     for j, t in enumerate(a.tunings):
@@ -47,8 +53,9 @@ for _ in range(a.runs):
         ctx.run()                                  # warm-up
         ctx.run()
         ms[j].append(ctx.replay_kernel_ms())
+        kms[j] = [round(x, 2) for x in ctx.kernel_times_ms()]
         met[j] = ctx.fetch()["met"]
         ctx.close()
-for t, m, mt in zip(a.tunings, ms, met):
+for t, m, km, mt in zip(a.tunings, ms, kms, met):
     print(json.dumps({"config": a.config, "tuning": json.loads(t), "ms": statistics.median(m),
-                      "all_ms": m, "met_equal": bool((mt == met[0]).all())}))
+                      "kernels_ms": km, "all_ms": m, "met_equal": bool((mt == met[0]).all())}))
