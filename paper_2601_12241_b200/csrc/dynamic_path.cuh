@@ -188,22 +188,27 @@ struct JWork {
     int* bf;    // D: ring index of the batch list's front (PADSIM_JBL)
     unsigned char* fl;
 };
-template <int TB>
-__host__ __device__ constexpr size_t j_work_bytes() { return (size_t)kJG * TB * (4 * sizeof(double) + 14 * sizeof(int) + 1); }
+// per-GPU SoA bytes: with the context term (CX) 4 doubles (tseg, L, sj, dL) + 13 ints +
+// flags; without it 2 doubles + 12 ints + flags (no sj, dL, ctx: 65 instead of 89 B per
+// GPU, so a one-warp CTA needs 16.6 instead of 22.8 KB and 13 instead of 9 fit an SM)
+template <int TB, bool CX>
+__host__ __device__ constexpr size_t j_work_bytes() {
+    return (size_t)kJG * TB * (CX ? 4 * sizeof(double) + 13 * sizeof(int) + 1 : 2 * sizeof(double) + 12 * sizeof(int) + 1);
+}
 
 enum : unsigned char { JF_DRAIN = 1, JF_DIRTY = 2 };
 
 // dynamic shared memory of the joint kernel (same base as the kernel's smem[])
 extern __shared__ __align__(128) unsigned char joint_dyn_smem[];
 
-template <int NG, int TB>
+template <int NG, int TB, bool CX>
 __host__ __device__ constexpr size_t joint_smem_base() {
-    return NG == 8 ? j_work_bytes<TB>() : (size_t)NG * TB * (sizeof(double) + 2 * sizeof(int));
+    return NG == 8 ? j_work_bytes<TB, CX>() : (size_t)NG * TB * (sizeof(double) + 2 * sizeof(int));
 }
 // + the per-thread Fig. 6 decomposition accumulators (2 doubles)
-template <int NG, int TB>
+template <int NG, int TB, bool CX>
 __host__ __device__ constexpr size_t joint_smem_bytes() {
-    return ((joint_smem_base<NG, TB>() + 15) & ~(size_t)15) + 2 * TB * sizeof(double);
+    return ((joint_smem_base<NG, TB, CX>() + 15) & ~(size_t)15) + 2 * TB * sizeof(double);
 }
 
 
@@ -282,10 +287,10 @@ struct JReplay {
     __device__ __forceinline__ void add_kp(int g, int d) { tab.add_p(g, d); }
     __device__ __forceinline__ void add_kd(int g, int d) { tab.add_d(g, d); }
     __device__ __forceinline__ double bnd(int o, int s) const {
-        return seg_bnd(W.tseg[o], W.L[o], gr ? W.dL[o] : 0.0, s - W.st0[o], gr);
+        return seg_bnd(W.tseg[o], W.L[o], (CX && gr) ? W.dL[o] : 0.0, s - W.st0[o], gr);
     }
     __device__ int first_bnd_ge(int o, double tau) const {
-        return seg_first_ge(W.tseg[o], W.L[o], gr ? W.dL[o] : 0.0, W.st0[o], W.b0[o], tau, gr);
+        return seg_first_ge(W.tseg[o], W.L[o], (CX && gr) ? W.dL[o] : 0.0, W.st0[o], W.b0[o], tau, gr);
     }
 
     __device__ void complete(int i, double t, double tpot) {
@@ -420,7 +425,7 @@ struct JReplay {
         auto leave = [&](int id) {
             complete(id, t, (t - PE(id)) / (double)(T.out_tok[id] - 1));
             if (CX) W.ctx[o] -= T.in_tok[id];
-            if (gr) W.sj[o] -= s - (T.out_tok[id] - 1);      // its join step (A40)
+            if (CX && gr) W.sj[o] -= s - (T.out_tok[id] - 1);      // its join step (A40)
             left++;
         };
         int mf = kIntMax;
@@ -569,7 +574,7 @@ struct JReplay {
             }
             n++;
             if (CX) W.ctx[o] += T.in_tok[i];
-            if (gr) W.sj[o] += step;
+            if (CX && gr) W.sj[o] += step;
             mf = fin < mf ? fin : mf;
             joined = true;
         }
@@ -587,10 +592,10 @@ struct JReplay {
                 } else {            // A15 / A40 context of the segment's first step
                     double xv = P.m.dec_fixed + P.m.dec_per_seq * (double)n;
                     long long cc = W.ctx[o];
-                    if (gr) cc += (long long)n * (step + 1) - W.sj[o];
+                    if (CX && gr) cc += (long long)n * (step + 1) - W.sj[o];
                     xv = xv + P.m.dec_per_ctx * (double)cc;
                     W.L[o] = xv / P.m.sdec[ci];
-                    if (gr) W.dL[o] = (P.m.dec_per_ctx * (double)n) / P.m.sdec[ci];
+                    if (CX && gr) W.dL[o] = (P.m.dec_per_ctx * (double)n) / P.m.sdec[ci];
                 }
                 W.fl[o] = f & (unsigned char)~JF_DIRTY;
             }
@@ -642,7 +647,8 @@ struct JReplay {
         dmask ^= ((Mask)1) << g;
         W.fl[o] = 0;
         W.a0[o] = 0; W.ql[o] = 0; W.b0[o] = 0; W.b1[o] = 0; W.st0[o] = 0;
-        W.mfin[o] = kIntMax; W.ctx[o] = 0; W.sj[o] = 0; W.bf[o] = 0;
+        W.mfin[o] = kIntMax; W.bf[o] = 0;
+        if (CX) { W.ctx[o] = 0; W.sj[o] = 0; }
         set_tnext(g, PAD_INF);
         tab.set_p(g, to_p ? 0 : kIntMax);
         tab.set_d(g, to_p ? kIntMax : 0);
@@ -798,11 +804,12 @@ struct JReplay {
             if (r == 0) pmask |= ((Mask)1) << g;
             if (r == 1) dmask |= ((Mask)1) << g;
             tab.init(g, r);
-            W.tseg[o] = 0.0; W.L[o] = 1.0; W.sj[o] = 0; W.dL[o] = 0.0;
+            W.tseg[o] = 0.0; W.L[o] = 1.0;
+            if (CX) { W.sj[o] = 0; W.dL[o] = 0.0; W.ctx[o] = 0; }
             W.a0[o] = 0; W.qh[o] = kNoIdx; W.qt[o] = kNoIdx; W.ql[o] = 0;
             W.b0[o] = 0; W.b1[o] = 0; W.st0[o] = 0; W.mfin[o] = kIntMax;
             W.eff[o] = W.cmd[o] = on ? ccap[g] : P.m.min_w;
-            W.rse[o] = 0; W.ctx[o] = 0; W.fl[o] = 0; W.bf[o] = 0;
+            W.rse[o] = 0; W.fl[o] = 0; W.bf[o] = 0;
         }
         Wh = P.wheel; Wm = Wh - 1; nwords = Wh >> 5;
         if (!PADSIM_JBL)
@@ -919,7 +926,7 @@ __global__ void __launch_bounds__(TB) __maxnreg__(MR) joint_kernel(const __grid_
     extern __shared__ __align__(128) unsigned char smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     char* wbase = P.scratch + ((size_t)blockIdx.x * (TB / 32) + warp) * P.warp_bytes;
-    const size_t accoff = (NG == 64 && P.j_kglob) ? 0 : ((joint_smem_base<NG, TB>() + 15) & ~(size_t)15);
+    const size_t accoff = (NG == 64 && P.j_kglob) ? 0 : ((joint_smem_base<NG, TB, CX>() + 15) & ~(size_t)15);
     JWork W;
     int ws;
     if (NG == 8) {           // per-GPU SoA in shared memory
@@ -927,15 +934,18 @@ __global__ void __launch_bounds__(TB) __maxnreg__(MR) joint_kernel(const __grid_
         unsigned char* p = smem;
         W.tseg = (double*)p + tid; p += n * sizeof(double);
         W.L = (double*)p + tid; p += n * sizeof(double);
-        W.sj = (long long*)p + tid; p += n * sizeof(long long);
-        W.dL = (double*)p + tid; p += n * sizeof(double);
+        W.sj = nullptr; W.dL = nullptr; W.ctx = nullptr;
+        if (CX) {
+            W.sj = (long long*)p + tid; p += n * sizeof(long long);
+            W.dL = (double*)p + tid; p += n * sizeof(double);
+        }
         int* ib = (int*)p;
         W.a0 = ib + 0 * n + tid; W.qh = ib + 1 * n + tid; W.qt = ib + 2 * n + tid;
         W.ql = ib + 3 * n + tid; W.b0 = ib + 4 * n + tid; W.b1 = ib + 5 * n + tid;
         W.st0 = ib + 6 * n + tid; W.mfin = ib + 7 * n + tid; W.eff = ib + 8 * n + tid;
-        W.cmd = ib + 9 * n + tid; W.rse = ib + 10 * n + tid; W.ctx = ib + 11 * n + tid;
-        W.bf = ib + 13 * n + tid;
-        p += 14 * n * sizeof(int);
+        W.cmd = ib + 9 * n + tid; W.rse = ib + 10 * n + tid; W.bf = ib + 11 * n + tid;
+        if (CX) W.ctx = ib + 12 * n + tid;
+        p += (CX ? 13 : 12) * n * sizeof(int);
         W.fl = p + tid;
         ws = TB;
     } else {                 // per-GPU SoA in lane-interleaved global scratch

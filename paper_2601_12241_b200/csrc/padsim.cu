@@ -1306,8 +1306,10 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
         size_t jb;
         const bool cx = model->decode_per_ctx_tok_s != 0.0;
         ctx->j_cx = cx;
-        if (NG == 8) jb = tbj == kThreads ? joint_smem_bytes<8, kThreads>() : joint_smem_bytes<8, 32>();
-        else jb = P.j_kglob ? 2 * 32 * sizeof(double) : joint_smem_bytes<64, 32>();
+        if (NG == 8)
+            jb = tbj == kThreads ? (cx ? joint_smem_bytes<8, kThreads, true>() : joint_smem_bytes<8, kThreads, false>())
+                                 : (cx ? joint_smem_bytes<8, 32, true>() : joint_smem_bytes<8, 32, false>());
+        else jb = P.j_kglob ? 2 * 32 * sizeof(double) : (cx ? joint_smem_bytes<64, 32, true>() : joint_smem_bytes<64, 32, false>());
         // next to a large stage C workload the joint replays run as one-warp CTAs
         // capped at 168 registers so they leave registers to stage C (cfg 4 536 →
         // 522 ms); when they are the bulk of the step (cfg 3) the 232-register
