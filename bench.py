@@ -6,11 +6,12 @@
 
 One *step* is one pass of the whole hot path (rows a1–a8 of SURVEY.md §8): every
 candidate allocation × every QPS point × every trace is replayed (static and
-dynamic kernels), reduced over traces and argmax-ed per QPS; with N > 1 ranks
-the per-rank Σmet are all-reduced over NCCL and the global argmax recomputed.
-Scaling is weak: rank r replays its own block of trace seeds (r·S … r·S+S−1),
-so per-GPU work is fixed as N grows; the units all ranks processed ÷ the max
-over ranks of the device time is ``value``.
+dynamic kernels), reduced over traces and argmax-ed per QPS.  With N > 1 ranks
+the fixed grid is sharded (strong scaling): QPS points striped
+q mod N when n_qps ≥ N, else blocks of candidates; seeds are never split.  The
+ranks' met / goodput blocks are all-gathered over NCCL and the global argmax
+taken on the gathered array; ``value`` is the whole grid ÷ the max over ranks
+of the device time.
 
 ``value`` times padsim_run with inputs resident in HBM (CUDA events on the
 launch stream, L2 flushed between steps by a 512 MiB write).  ``e2e`` times the
@@ -355,7 +356,7 @@ def main():
     if ev_a == 0:            # static replays ran in the joint kernel
         ev_dyn += ev_static
         ev_static = 0
-    wide = role.shape[1] > 8 and ev_a > 0     # N > 8: the wide-node factorized path
+    wide = ctx.static_path() == "warp"        # the warp-per-replay factorized stages
     # per-rank replay results of the timed configuration (for the parity sample)
     rep = ctx.fetch_replays()
 

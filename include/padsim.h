@@ -390,6 +390,13 @@ int padsim_set_tuning(padsim_ctx* ctx, const padsim_tuning* tuning);
 /* Kernel launches issued by the last padsim_run (for the bench's launch count). */
 int padsim_launch_count(padsim_ctx* ctx, int32_t* n);
 
+/* Which path the planner chose for the static candidates of the current plan
+ * (*path): 0 none, 1 thread-per-replay factorized stages (stageA_kernel /
+ * stageC_kernel, N ≤ 8), 2 warp-per-replay factorized stages (stageA_wide_kernel /
+ * stageC_wide_kernel: 8 < N ≤ 64, or N ≤ 8 with ≤ 8 static replays per SM),
+ * 3 the joint kernel.  PADSIM_EINVAL without a plan.                         */
+int padsim_static_path(padsim_ctx* ctx, int32_t* path);
+
 /* ---- a1 candidate enumeration (host) ----------------------------------------
  * All pool-uniform (x, p, d): x ∈ [1, N−1] prefill GPUs at p W, N−x decode
  * GPUs at d W, p,d ∈ {min_w + k·step_w} ∩ [min_w, max_w], x·p + (N−x)·d ≤ B

@@ -123,7 +123,7 @@ EXPORTS = ["padsim_create", "padsim_destroy", "padsim_last_error", "padsim_versi
            "padsim_evaluate_allocations", "padsim_plan", "padsim_run", "padsim_fetch",
            "padsim_get_device_results", "padsim_fetch_replays", "padsim_fetch_records",
            "padsim_argmax_device", "padsim_step_controller", "padsim_controller_decide_device",
-           "padsim_set_tuning", "padsim_launch_count", "padsim_enumerate_pool_uniform",
+           "padsim_set_tuning", "padsim_launch_count", "padsim_static_path", "padsim_enumerate_pool_uniform",
            "padsim_replay_kernel_ms", "padsim_kernel_times_ms", "padsim_set_slo_sweep",
            "padsim_fetch_extras", "padsim_fetch_decomposition", "padsim_fetch_percentiles",
            "padsim_replay_records"]
@@ -174,6 +174,7 @@ def load(path: str = LIB_PATH):
                                                   _P(WindowStats), C.c_double, _P(Action)]
     L.padsim_set_tuning.argtypes = [vp, _P(Tuning)]
     L.padsim_launch_count.argtypes = [vp, _P(C.c_int32)]
+    L.padsim_static_path.argtypes = [vp, _P(C.c_int32)]
     L.padsim_enumerate_pool_uniform.argtypes = [C.c_int32] * 6 + [_P(C.c_int32), C.c_int32,
                                                                   _P(C.c_int32)]
     _lib = L
@@ -295,6 +296,13 @@ class Context:
         """Launch-configuration overrides (padsim_set_tuning); results never depend on them."""
         t = dict(TUNING_AUTO, **(tuning or {}))
         self._check(self.L.padsim_set_tuning(self.ptr, C.byref(Tuning(**t))), "set_tuning")
+
+    def static_path(self) -> str:
+        """The planner's path for the static candidates: "none", "thread" (stageA_kernel /
+        stageC_kernel), "warp" (the wide stages) or "joint" (padsim_static_path)."""
+        n = C.c_int32(0)
+        self._check(self.L.padsim_static_path(self.ptr, C.byref(n)), "static_path")
+        return ("none", "thread", "warp", "joint")[n.value]
 
     def launch_count(self) -> int:
         n = C.c_int32(0)

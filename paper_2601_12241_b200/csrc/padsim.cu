@@ -1198,14 +1198,24 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
     CK(cudaGetLastError());
 
     // factorized static path (stage A prefill groups -> stage C decode) for N <= 8
-    ctx->fact = N <= 8 && !ctx->static_list.empty() && !(flags & PADSIM_JOINT) && Rmax < kRecMaxReq;
+    // Few static replays (≤ 8 per SM: cfg 1's 13, cfg 3's 160) leave the thread-per-replay
+    // stages latency-bound — one serial chain per thread, ~3 µs per request — and they
+    // take the warp-per-replay wide path instead (wide_path.cuh works for any N ≤ 64):
+    // measured cfg 1 1.40 → 0.83 ms, cfg 3 310 → 271 ms per step (its 160 static
+    // replays were a 258 ms stage A → C chain next to the joint replays), cfg 2 (122 k
+    // replays) 44 → 197 ms the other way.  padsim_tuning.wide_path = 1 forces it, 0 never.
+    const long long n_static_rep = (long long)ctx->static_list.size() * n_qps * n_traces;
+    const bool wide_small = N <= 8 && model->decode_per_ctx_tok_s == 0.0 && ctx->tune.wide_path != 0 &&
+                            (ctx->tune.wide_path == 1 || n_static_rep <= (long long)ctx->n_sm * 8);
+    ctx->fact = N <= 8 && !wide_small && !ctx->static_list.empty() && !(flags & PADSIM_JOINT) &&
+                Rmax < kRecMaxReq;
     if (ctx->fact) {
         int r_ = plan_factorized(ctx, model, slo, n_qps, n_traces, Rmax, tot, cands);
         if (r_) return r_;
     }
     // wide nodes: the warp-per-replay factorized path (no context term: with one the
     // static candidates stay on the joint kernel)
-    ctx->wide = N > 8 && N <= kWMax && !ctx->static_list.empty() && !(flags & PADSIM_JOINT) &&
+    ctx->wide = (N > 8 || wide_small) && N <= kWMax && !ctx->static_list.empty() && !(flags & PADSIM_JOINT) &&
                 Rmax < kRecMaxReq && model->decode_per_ctx_tok_s == 0.0 && ctx->tune.wide_path != 0;
     if (ctx->wide) {
         int r_ = plan_wide(ctx, model, slo, n_qps, n_traces, Rmax, cands);
@@ -1587,6 +1597,13 @@ int padsim_replay_records(padsim_ctx* ctx, const padsim_trace* trace, double qps
     rc = padsim_run(ctx, ctx->stream);
     if (rc) return rc;
     return padsim_fetch_records(ctx, ctx->stream, ttft, tpot, prefill_end, completion, nullptr, nullptr);
+}
+
+int padsim_static_path(padsim_ctx* ctx, int32_t* path) {
+    if (!ctx || !path) return PADSIM_EINVAL;
+    if (!ctx->planned) return fail(ctx, PADSIM_EINVAL, "no plan");
+    *path = ctx->static_list.empty() ? 0 : ctx->fact ? 1 : ctx->wide ? 2 : 3;
+    return PADSIM_OK;
 }
 
 int padsim_launch_count(padsim_ctx* ctx, int32_t* n) {

@@ -25,8 +25,17 @@ def gpu_records(traces, qps, model, role, cap, pols, slo, budget, tuning=None, c
 def compare_records(traces, qps, model, role, cap, pols, slo, budget, exact=True, tuning=None,
                     cand_budget=None):
     """Per-request, per-replay comparison; returns number of requests compared.
-    ``tuning``: launch-configuration overrides (padsim_set_tuning) to exercise."""
-    res, rep, rec = gpu_records(traces, qps, model, role, cap, pols, slo, budget, tuning, cand_budget)
+    ``tuning``: launch-configuration overrides (padsim_set_tuning) to exercise.
+
+    Static candidates of N ≤ 8 nodes have two planner paths — the thread-per-replay
+    stages (wide_path = 0) and, for small workloads like these, the warp-per-replay
+    wide path (the planner's auto choice, forced by wide_path = 1): unless the
+    tuning names one, both are run and compared."""
+    tuning = dict(tuning or {})
+    runs = [tuning]
+    if role.shape[1] <= 8 and "wide_path" not in tuning and any(p["kind"] == 0 for p in pols):
+        runs = [dict(tuning, wide_path=0), dict(tuning, wide_path=1)]
+    outs = [gpu_records(traces, qps, model, role, cap, pols, slo, budget, t, cand_budget) for t in runs]
     n = 0
     for c in range(role.shape[0]):
         for q, qv in enumerate(qps):
@@ -34,22 +43,24 @@ def compare_records(traces, qps, model, role, cap, pols, slo, budget, exact=True
                 bc = budget if cand_budget is None else int(cand_budget[c])
                 o = oracle.replay(model, role[c], cap[c], pols[c], bc, slo, tr, qv)
                 R = tr["s_unit"].size
-                for k in REC:
-                    g = rec[k][c, q, s, :R]
-                    if exact:
-                        bad = np.nonzero(g != o[k])[0]
-                    else:
-                        bad = np.nonzero(~np.isclose(g, o[k], rtol=RTOL, atol=0))[0]
-                    assert bad.size == 0, (k, c, q, s, bad[:5], g[bad[:5]], o[k][bad[:5]])
-                assert rep["met"][c, q, s] == o["met"], (c, q, s)
-                assert rep["near_boundary"][c, q, s] == o["near_boundary"]
-                assert rep["duration"][c, q, s] == o["duration"]
-                assert rep["goodput"][c, q, s] == o["goodput"]
+                for t, (_res, rep, rec) in zip(runs, outs):
+                    for k in REC:
+                        g = rec[k][c, q, s, :R]
+                        if exact:
+                            bad = np.nonzero(g != o[k])[0]
+                        else:
+                            bad = np.nonzero(~np.isclose(g, o[k], rtol=RTOL, atol=0))[0]
+                        assert bad.size == 0, (t, k, c, q, s, bad[:5], g[bad[:5]], o[k][bad[:5]])
+                    assert rep["met"][c, q, s] == o["met"], (t, c, q, s)
+                    assert rep["near_boundary"][c, q, s] == o["near_boundary"], t
+                    assert rep["duration"][c, q, s] == o["duration"], t
+                    assert rep["goodput"][c, q, s] == o["goodput"], t
                 n += R
     ev = oracle.evaluate(model, role, cap, pols, budget, slo, traces, qps, n_threads=8,
                          cand_budget_w=cand_budget)
-    assert np.array_equal(res["met"], ev["met"])
-    assert np.array_equal(res["argmax"], ev["argmax"])
-    assert np.array_equal(res["near_boundary"], ev["near_boundary"])
-    assert np.array_equal(res["goodput"], ev["goodput"])
+    for t, (res, _rep, _rec) in zip(runs, outs):
+        assert np.array_equal(res["met"], ev["met"]), t
+        assert np.array_equal(res["argmax"], ev["argmax"]), t
+        assert np.array_equal(res["near_boundary"], ev["near_boundary"]), t
+        assert np.array_equal(res["goodput"], ev["goodput"]), t
     return n

@@ -1,11 +1,13 @@
 """SLO-boundary decisions on the non-records path (GPU ↔ oracle, bit-exact).
 
-Stage C decides `tpot <= TPOT_SLO` and the 1e-9 near-boundary test without the
-FP64 division when the margin fixes the outcome (static_path.cuh,
-complete_leave); the records path always divides.  These SLOs are placed
-exactly on, and within 1e-12 … 3e-9 relative of, tpot values the oracle
-produced, so both branches of every decision are exercised; met / near counts
-and the SLO-sweep counts must equal the oracle's (north_star: bit-exact)."""
+Every path scores a completion as the oracle does: tpot = (t − pe) / (out − 1)
+in FP64, then the inclusive test `tpot <= TPOT_SLO` (A6) and the 1e-9-relative
+near-boundary test.  (A division-free variant that decided the tests from the
+margin was measured slower and not adopted.)  These SLOs are
+placed exactly on, and within 1e-12 … 3e-9 relative of, tpot values the oracle
+produced, so both outcomes of every decision are exercised on the non-records
+path; met / near counts and the SLO-sweep counts must equal the oracle's
+(north_star: bit-exact)."""
 import numpy as np
 import pytest
 
@@ -23,7 +25,8 @@ def pkg():
     return p
 
 
-def test_tpot_boundary_decisions_exact(pkg):
+@pytest.mark.parametrize("wide", [0, 1], ids=["thread-stages", "warp-stages"])
+def test_tpot_boundary_decisions_exact(pkg, wide):
     xpd = [(4, 600, 600), (4, 750, 450), (5, 650, 510), (6, 550, 700), (2, 700, 560), (7, 450, 750)]
     role, cap = static_candidates(8, xpd + [(4, 600, 600), (3, 600, 600)])
     pols = [policy("static")] * len(xpd) + [policy("dyn-both", cooldown_s=2.0), policy("dyn-power")]
@@ -37,7 +40,7 @@ def test_tpot_boundary_decisions_exact(pkg):
     f = [1 + 2e-10, 1 - 2e-10, 1 + 1e-9, 1 + 2.9e-9, 1 + 3.1e-9, 1 + 1e-12, 1 - 1e-12]
     sweep = [{"ttft": 2.0, "tpot": (T * x, T * x)} for x in f] + \
             [{"ttft": 2.0, "tpot": (np.nextafter(T, 1.0), np.nextafter(T, 0.0))}]
-    ctx = pkg.Context(0)
+    ctx = pkg.Context(0, tuning=dict(wide_path=wide))
     try:
         ctx.plan(traces, qps, DEFAULT_MODEL, role, cap, pols, slo, 4800)
         ctx.set_slo_sweep(sweep)

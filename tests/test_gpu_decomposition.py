@@ -24,8 +24,11 @@ def pkg():
     return p
 
 
-def _run(pkg, traces, qps, role, cap, pols, slo, budget, records=False, joint=False, pcts=None):
-    ctx = pkg.Context(0)
+def _run(pkg, traces, qps, role, cap, pols, slo, budget, records=False, joint=False, pcts=None,
+         wide=-1):
+    # wide: padsim_tuning.wide_path (-1 the planner's choice, 0 / 1 force the
+    # thread-per-replay / warp-per-replay static stages of N <= 8 nodes)
+    ctx = pkg.Context(0, tuning=dict(wide_path=wide))
     try:
         ctx.plan(traces, qps, DEFAULT_MODEL, role, cap, pols, slo, budget, records=records, joint=joint)
         ctx.run()
@@ -55,13 +58,13 @@ def _check_decomposition(dec, traces, qps, role, cap, pols, slo, budget):
 XPD = [(1, 750, 575), (3, 675, 525), (4, 600, 600), (6, 550, 700), (2, 450, 650)]
 
 
-@pytest.mark.parametrize("joint", [False, True])
-def test_decomposition_static(pkg, joint):
+@pytest.mark.parametrize("joint,wide", [(False, 0), (False, 1), (True, -1)])
+def test_decomposition_static(pkg, joint, wide):
     role, cap = static_candidates(8, XPD)
     pols = [policy("static")] * len(XPD)
     traces = [make_trace("lb", 70 + s, 400) for s in range(2)] + [make_trace("lb_bursty", 5, 300)]
     qps = [0.25, 1.5, 3.0, 5.0]
-    dec, _, _ = _run(pkg, traces, qps, role, cap, pols, DEFAULT_SLO, 4800, joint=joint)
+    dec, _, _ = _run(pkg, traces, qps, role, cap, pols, DEFAULT_SLO, 4800, joint=joint, wide=wide)
     _check_decomposition(dec, traces, qps, role, cap, pols, DEFAULT_SLO, 4800)
     # Fig. 6 backpressure shape: queueing grows with load for the 1P7D split
     assert dec["sum_queue"][0, -1] > dec["sum_queue"][0, 0]
@@ -103,14 +106,16 @@ def _check_percentiles(pc, rec, traces, qps, role, cap, pols, slo, budget):
                             assert got == np.sort(rec[m][c, q, s, :R])[(p * R + 99) // 100 - 1]
 
 
-def test_percentiles_exact(pkg):
+@pytest.mark.parametrize("wide", [0, 1])
+def test_percentiles_exact(pkg, wide):
     role, cap = static_candidates(8, XPD[:3])
     pols = [policy("static")] * 2 + [policy("dyn-both", cooldown_s=2.0)]
     traces = [make_trace("lb", 3, 500), make_trace("lb_bursty", 4, 37),
               {"s_unit": np.zeros(0), "in_tok": np.zeros(0, np.int32), "out_tok": np.zeros(0, np.int32),
                "phase": np.zeros(0, np.uint8)}]
     qps = [0.5, 2.5]
-    _, pc, rec = _run(pkg, traces, qps, role, cap, pols, DEFAULT_SLO, 4800, records=True, pcts=PCTS)
+    _, pc, rec = _run(pkg, traces, qps, role, cap, pols, DEFAULT_SLO, 4800, records=True, pcts=PCTS,
+                      wide=wide)
     _check_percentiles(pc, rec, traces, qps, role, cap, pols, DEFAULT_SLO, 4800)
 
 

@@ -348,7 +348,8 @@ def test_cfg4_shape_sampled(pkg):
         assert rep["goodput"][c, q, s] == o["goodput"]
 
 
-def test_slo_sweep_qps_per_watt_max80(pkg):
+@pytest.mark.parametrize("wide", [0, 1], ids=["thread-stages", "warp-stages"])
+def test_slo_sweep_qps_per_watt_max80(pkg, wide):
     # Fig. 8 SLO scaling (0.5x-2x), Fig. 5b TPOT 25 ms, QPS/W,
     # max QPS at >= 80 % attainment — static and dynamic candidates
     xpd = [(4, 600, 600), (4, 750, 450), (4, 675, 525), (5, 600, 600), (3, 700, 540)]
@@ -358,7 +359,7 @@ def test_slo_sweep_qps_per_watt_max80(pkg):
     qps = [0.5, 1.0, 1.5, 2.0]
     slos = [{"ttft": f * 1.0, "tpot": (f * 0.04, f * 0.04)} for f in (0.5, 2.0)] + \
            [{"ttft": 1.0, "tpot": (0.025, 0.025)}]
-    ctx = pkg.Context(0)
+    ctx = pkg.Context(0, tuning=dict(wide_path=wide))
     try:
         ctx.plan(traces, qps, DEFAULT_MODEL, role, cap, pols, DEFAULT_SLO, 4800)
         ctx.set_slo_sweep(slos)

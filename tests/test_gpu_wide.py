@@ -48,6 +48,18 @@ def test_wide_records_exact_other_sizes(pkg, N, B):
                     DEFAULT_SLO, B)
 
 
+@pytest.mark.parametrize("N,B", [(8, 4800), (4, 2400)])
+def test_wide_path_forced_small_nodes(pkg, N, B):
+    # padsim_tuning.wide_path = 1 sends N <= 8 static candidates down the wide path
+    # (the planner's choice for tiny workloads such as cfg 1): records = oracle
+    xpd = [(1, 700, 550), (N // 2, 600, 600), (N - 1, 600, 450), (N // 2, 400, 700)]
+    role, cap = static_candidates(N, xpd)
+    traces = [make_trace("lb", 13, 300), make_trace("phase", 14, 200)]
+    for w in (1, 0):
+        compare_records(traces, [0.5, 1.5, 4.0], DEFAULT_MODEL, role, cap, [policy("static")] * len(xpd),
+                        PHASE_SLO, B, tuning=dict(wide_path=w))
+
+
 def test_wide_non_uniform_caps_and_small_kv_buffer(pkg):
     # arbitrary per-GPU cap vectors and interleaved roles (the ABI takes full
     # vectors), a 4-slot KV buffer (waiting FIFO exercised), small batch limits
