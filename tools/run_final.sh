@@ -20,12 +20,8 @@ timeout 2400 python bench.py --config cfg5 --steps 1 --warmup 3 --e2e-steps 1 --
 # 30 s launch would take ~40 passes)
 timeout 2400 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__inst_issued.avg.pct_of_peak_sustained_active,smsp__thread_inst_executed_per_inst_executed.ratio,sm__warps_active.avg.pct_of_peak_sustained_active,smsp__inst_executed.sum --clock-control none -k regex:wide -o $D/wide_cfg5 python tools/prof_run.py --config cfg5 --runs 1 > $D/ncu_W5.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:stageC_wide -c 1 -o $D/cw_cfg5_sub python tools/prof_run.py --config cfg5 --traces 1 --cand-stride 16 --runs 1 > $D/ncu_cw.log 2>&1
-for v in jointg wide64 wide16; do
-  for tool in racecheck synccheck memcheck; do
-    timeout 600 compute-sanitizer --tool $tool python tools/sanitize_small.py $v > $D/san_${v}_${tool}.log 2>&1
-    echo "$v $tool rc=$? $(grep -c 'RACECHECK SUMMARY\|ERROR SUMMARY' $D/san_${v}_${tool}.log) $(grep 'SUMMARY' $D/san_${v}_${tool}.log | tail -1)" >> $D/san_summary.txt
-  done
-done
+# compute-sanitizer runs (tools/sanitize_small.py) are no longer allowed on this pool;
+# the round-2 logs are in profiles/r2_sanitize/ and profiles/r2_final/san_summary.txt
 # summaries on the box (the .ncu-rep files would exceed gpurun's 64 MiB copy-back)
 { python tools/ncu_summary.py full $D/stageC_cfg4.ncu-rep; python tools/ncu_hot.py $D/stageC_cfg4.ncu-rep 25; } > $D/sum_stageC_cfg4.txt 2>&1
 { python tools/ncu_summary.py full $D/stageA_cfg4.ncu-rep; python tools/ncu_hot.py $D/stageA_cfg4.ncu-rep 20; } > $D/sum_stageA_cfg4.txt 2>&1
