@@ -198,6 +198,7 @@ __host__ __device__ constexpr size_t j_work_bytes() {
 
 enum : unsigned char { JF_DRAIN = 1, JF_DIRTY = 2 };
 
+
 // dynamic shared memory of the joint kernel (same base as the kernel's smem[])
 extern __shared__ __align__(128) unsigned char joint_dyn_smem[];
 
@@ -787,7 +788,20 @@ struct JReplay {
         }
     }
 
+    // the replay in three parts (start / one instant / result) so that a lane can
+    // start its next replay inside the same event loop (lane refill, joint_kernel)
+    long long events;
+    int na;
+    double ta;
+    float win;
+
     __device__ ReplayResult run(int c, int q, long long rec) {
+        start(c, q, rec);
+        while (completed < R) instant();
+        return result();
+    }
+
+    __device__ void start(int c, int q, long long rec) {
         N = P.N;
         R = T.R;
         max_db = P.m.max_db;
@@ -845,14 +859,18 @@ struct JReplay {
             acc[0] = 0.0;
             acc[TB] = 0.0;
         }
-        long long events = 0;
-        int na = 0;
-        double ta = R > 0 ? arr(0) : PAD_INF;
+        events = 0;
+        na = 0;
+        ta = R > 0 ? arr(0) : PAD_INF;
         // keep the simulated clocks of a warp's lanes within sync_win mean
         // inter-arrival times (same trace → shared cache lines); scheduling only,
         // results are independent of it (see stageC_kernel)
-        const float win = P.sync_win > 0.f ? (float)((double)P.sync_win * inv_lam) : 0.f;
-        while (completed < R) {
+        win = P.sync_win > 0.f ? (float)((double)P.sync_win * inv_lam) : 0.f;
+    }
+
+    // one DES instant (all events at the next time t, then the dispatch pass)
+    __device__ __forceinline__ void instant() {
+        {
             double t = tab.tmin(ta < mte ? ta : mte);
             if (DYN) {
                 t = tick_t < t ? tick_t : t;
@@ -862,7 +880,7 @@ struct JReplay {
             if (win > 0.f) {
                 const float tf = (float)t;
                 const unsigned mn = __reduce_min_sync(__activemask(), __float_as_uint(tf));
-                if (tf > __uint_as_float(mn) + win) continue;
+                if (tf > __uint_as_float(mn) + win) return;
             }
             events++;
             touched = 0;
@@ -906,6 +924,9 @@ struct JReplay {
                 skip_ticks(tick_outcome, tab.tmin(ne));
             }
         }
+    }
+
+    __device__ ReplayResult result() {
         ReplayResult res;
         res.met = met;
         res.near = near;
@@ -923,6 +944,7 @@ struct JReplay {
 // 168-register variant that fits more warps next to stage C was not faster).
 template <bool DYN, int TB, int NG, bool CX, int MR = (TB == 32 ? 232 : 168)>
 __global__ void __launch_bounds__(TB) __maxnreg__(MR) joint_kernel(const __grid_constant__ Plan P) {
+    constexpr bool kRefill = TB == 32 && NG == 8 && MR == 168;
     extern __shared__ __align__(128) unsigned char smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     char* wbase = P.scratch + ((size_t)blockIdx.x * (TB / 32) + warp) * P.warp_bytes;
@@ -983,18 +1005,26 @@ __global__ void __launch_bounds__(TB) __maxnreg__(MR) joint_kernel(const __grid_
     T.s_unit = P.s_unit + off; T.kv = P.kv + off; T.in_tok = P.in_tok + off;
     T.out_tok = P.out_tok + off; T.phase = P.phase + off;
     const int QC = P.Q * P.n_clist;
-    for (;;) {
-        int item = 0;
-        if (lane == 0) item = (int)atomicAdd(P.work + s, 1u);
-        item = __shfl_sync(0xffffffffu, item, 0);
-        // an item is P.lpw replays: fewer than 32 lanes per warp when the whole
-        // workload has too few replays to give every SM several warps
-        if (item * P.lpw >= QC) break;
-        const int u = item * P.lpw + lane;
-        if (lane >= P.lpw || u >= QC) continue;
-        const int q = u / P.n_clist;
-        const int c = P.clist[u - q * P.n_clist];
-        const long long r = ((long long)c * P.Q + q) * P.S + s;
+    if constexpr (kRefill) {
+        // Lane refill (the 168-register one-warp variant, which runs next to a large
+        // stage C workload): the work counter counts replays; a warp's first lpw lanes
+        // start on consecutive replays (u = q·n_clist + c: one arrival stream), and a
+        // lane whose replay ends stores it and starts the next replay inside the same
+        // event loop instead of idling until the longest replay of its warp is done,
+        // so the warps — and the registers they hold next to stage C — are released
+        // sooner (cfg 4 461 → 452 ms/step; as the whole step, cfg 3, the lane clock
+        // window it has to give up is worth more: 270 → 324 ms).  Scheduling only:
+        // every replay is independent.
+        int u;
+        {
+            int first = 0;
+            if (lane == 0) first = (int)atomicAdd(P.work + s, (unsigned)P.lpw);
+            u = __shfl_sync(0xffffffffu, first, 0) + lane;
+        }
+        if (lane >= P.lpw || u >= QC) return;
+        int q = u / P.n_clist;
+        int c = P.clist[u - q * P.n_clist];
+        long long r = ((long long)c * P.Q + q) * P.S + s;
         JReplay<DYN, TB, NG, CX> rp(P, T, X, W);
         rp.ws = ws;
         rp.accoff = accoff;
@@ -1021,17 +1051,83 @@ __global__ void __launch_bounds__(TB) __maxnreg__(MR) joint_kernel(const __grid_
         rp.ring = (unsigned long long*)(wbase + P.off_ring) + (size_t)lane * NG * P.ring_slots;
         rp.wts = DYN ? (double*)(wbase + P.off_wts) + (size_t)lane * P.Rmax : nullptr;
         rp.wtf = DYN ? (unsigned char*)(wbase + P.off_wtf) + (size_t)lane * P.Rmax : nullptr;
-        const ReplayResult res = rp.run(c, q, P.rec_ttft ? r * P.Rmax : -1);
-        P.rep_met[r] = res.met;
-        P.rep_near[r] = res.near;
-        P.rep_dur[r] = res.duration;
-        P.rep_good[r] = res.goodput;
-        P.rep_events[r] = res.events;
-        P.sw.rep_watts[r] = res.watts;
-        {
-            const double* acc = (const double*)(smem + accoff) + tid;
-            P.sw.rep_sq[r] = acc[0];
-            P.sw.rep_se[r] = acc[TB];
+        rp.start(c, q, P.rec_ttft ? r * P.Rmax : -1);
+        for (;;) {
+            if (rp.completed >= rp.R) {
+                const ReplayResult res = rp.result();
+                P.rep_met[r] = res.met;
+                P.rep_near[r] = res.near;
+                P.rep_dur[r] = res.duration;
+                P.rep_good[r] = res.goodput;
+                P.rep_events[r] = res.events;
+                P.sw.rep_watts[r] = res.watts;
+                {
+                    const double* acc = (const double*)(smem + accoff) + tid;
+                    P.sw.rep_sq[r] = acc[0];
+                    P.sw.rep_se[r] = acc[TB];
+                }
+                u = (int)atomicAdd(P.work + s, 1u);
+                if (u >= QC) break;
+                q = u / P.n_clist;
+                c = P.clist[u - q * P.n_clist];
+                r = ((long long)c * P.Q + q) * P.S + s;
+                rp.metk = P.sw.rep_met + r * kMaxSloSweep;
+                rp.start(c, q, P.rec_ttft ? r * P.Rmax : -1);
+                continue;
+            }
+            rp.instant();
+        }
+    } else {
+        for (;;) {
+            int item = 0;
+            if (lane == 0) item = (int)atomicAdd(P.work + s, 1u);
+            item = __shfl_sync(0xffffffffu, item, 0);
+            // an item is P.lpw replays: fewer than 32 lanes per warp when the whole
+            // workload has too few replays to give every SM several warps
+            if (item * P.lpw >= QC) break;
+            const int u = item * P.lpw + lane;
+            if (lane >= P.lpw || u >= QC) continue;
+            const int q = u / P.n_clist;
+            const int c = P.clist[u - q * P.n_clist];
+            const long long r = ((long long)c * P.Q + q) * P.S + s;
+            JReplay<DYN, TB, NG, CX> rp(P, T, X, W);
+            rp.ws = ws;
+            rp.accoff = accoff;
+            if constexpr (NG == 64) {        // next-event / routing keys
+                if (P.j_kglob) {             // lane-interleaved global scratch (frees shared memory)
+                    rp.tab.tn = (double*)(wbase + P.off_keys) + lane;
+                    rp.tab.kp = (int*)(wbase + P.off_keys + (size_t)NG * 32 * sizeof(double)) + lane;
+                    rp.tab.kd = rp.tab.kp + NG * 32;
+                    rp.tab.st = 32;
+                } else {                     // shared memory
+                    rp.tab.tn = (double*)smem + tid;
+                    rp.tab.kp = (int*)(smem + (size_t)NG * TB * sizeof(double)) + tid;
+                    rp.tab.kd = rp.tab.kp + NG * TB;
+                    rp.tab.st = TB;
+                }
+            }
+            rp.metk = P.sw.rep_met + r * kMaxSloSweep;
+            rp.tte = tte;
+            rp.tti = tti;
+            rp.heads = (int*)(wbase + P.off_heads) + lane;
+            rp.bits = (unsigned*)(wbase + P.off_bits) + lane;
+            rp.RB = P.ring_slots;
+            rp.RBm = P.ring_slots - 1;
+            rp.ring = (unsigned long long*)(wbase + P.off_ring) + (size_t)lane * NG * P.ring_slots;
+            rp.wts = DYN ? (double*)(wbase + P.off_wts) + (size_t)lane * P.Rmax : nullptr;
+            rp.wtf = DYN ? (unsigned char*)(wbase + P.off_wtf) + (size_t)lane * P.Rmax : nullptr;
+            const ReplayResult res = rp.run(c, q, P.rec_ttft ? r * P.Rmax : -1);
+            P.rep_met[r] = res.met;
+            P.rep_near[r] = res.near;
+            P.rep_dur[r] = res.duration;
+            P.rep_good[r] = res.goodput;
+            P.rep_events[r] = res.events;
+            P.sw.rep_watts[r] = res.watts;
+            {
+                const double* acc = (const double*)(smem + accoff) + tid;
+                P.sw.rep_sq[r] = acc[0];
+                P.sw.rep_se[r] = acc[TB];
+            }
         }
     }
 }

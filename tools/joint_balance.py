@@ -24,9 +24,9 @@ a = ap.parse_args()
 import paper_2601_12241_b200 as pkg  # noqa: E402
 
 cfg = get_config(a.config)
-role, cap, pols, traces, qps = build_workload(cfg, 0, pkg.enumerate_pool_uniform)
+role, cap, pols, traces, qps, _cb = build_workload(cfg, 0, pkg.enumerate_pool_uniform)
 ctx = pkg.Context(0)
-ctx.plan(traces, qps, DEFAULT_MODEL, role, cap, pols, cfg["slo"], cfg["budget_w"])
+ctx.plan(traces, qps, DEFAULT_MODEL, role, cap, pols, cfg["slo"], cfg["budget_w"], cand_budget_w=_cb)
 ctx.run()
 ms = ctx.kernel_times_ms()
 ev = ctx.fetch_replays()["events"]          # [C, Q, S]

@@ -48,6 +48,9 @@ def rows(path):
             d[k] = v * SCALE.get(units[i], 1.0)
         name = vals[hdr.index("Kernel Name")]
         d["name"] = name.split("(")[0].split("<")[0].split("::")[-1].replace("void ", "").strip()
+        d["kw"] = None
+        if d["name"] == "stageC_kernel" and "<" in name:     # <CTX, IDX, KW, BL>: decode-pool class
+            d["kw"] = int(name.split("<")[1].split(">")[0].split(",")[2])
         yield d
 
 
@@ -64,8 +67,17 @@ def requests_per_kernel(wl):
     groups = {tuple(int(v) for v in cap[c][role[c] == 0]) for c in st}
     Q, C = len(qps), role.shape[0]
     if cfg["n_gpus"] <= 8:
+        # stage C launches one kernel per decode-pool class (padsim.cu plan_factorized:
+        # five classes KW = 1, 2, 4, 5, 7 for ≥ 400 k static replays, else KW = 2, 4, 7)
+        fine = len(st) * Q * len(traces) >= 400000
+        kw = {}
+        for c in st:
+            y = int((role[c] == 1).sum())
+            k = (1 if y <= 1 else 2 if y <= 2 else 4 if y <= 4 else 5 if y <= 5 else 7) if fine else \
+                (2 if y <= 2 else 4 if y <= 4 else 7)
+            kw[k] = kw.get(k, 0) + Q * r_sum
         return {"stageA_kernel": len(groups) * Q * r_sum, "stageC_kernel": len(st) * Q * r_sum,
-                "joint_kernel": (C - len(st)) * Q * r_sum}
+                "joint_kernel": (C - len(st)) * Q * r_sum, "_stageC_kw": kw}
     # N > 8: static candidates on the wide-node factorized path, dynamic ones on the joint kernel
     return {"stageA_wide_kernel": len(groups) * Q * r_sum, "stageC_wide_kernel": len(st) * Q * r_sum,
             "joint_kernel": (C - len(st)) * Q * r_sum}
@@ -83,6 +95,8 @@ def main():
                 continue
             a = agg[d["name"]]
             a["launches"] += 1
+            if d["kw"] is not None:
+                a["req"] += req.get("_stageC_kw", {}).get(d["kw"], 0)
             a["read"] += d["rd"] if d["rd"] == d["rd"] else 0.0
             a["write"] += d["wr"] if d["wr"] == d["wr"] else 0.0
             a["dur"] += d["dur"]
@@ -100,8 +114,9 @@ def main():
                 "issue_active": a["iss"] / a["dur"] / 100, "simt_threads": a["simt"] / a["dur"],
                 "warps_active": a["warps"] / a["dur"] / 100, "profile": tag,
                 "warp_instr": a["inst"],
-                "warp_instr_per_request": a["inst"] / req[n] if req.get(n) and a["inst"] else None,
-                "requests": req.get(n),
+                # per request of the launches collected (stage C: their decode-pool classes)
+                "warp_instr_per_request": (a["inst"] / (a["req"] or req[n])) if req.get(n) and a["inst"] else None,
+                "requests": a["req"] or req.get(n),
                 "launches_not_collected": missing.get(n, 0)}
     json.dump(data, open(OUT, "w"), indent=1)
     print(json.dumps(w, indent=1))
