@@ -1338,13 +1338,22 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
         int occj = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occj, fnj, tbj, jb));
         occj = std::max(occj, 1);
-        // replays per warp item: 32, or fewer when the joint workload would leave
-        // the SMs with fewer than ~4 latency-bound warps each (measured on cfg 3,
-        // 13.4k replays: 32 lanes 464 ms, 16 lanes 387 ms, 8 lanes 452 ms)
+        // replays per warp item: as few as still fit every warp in one wave of
+        // resident warps (fewer lanes per warp = less divergence on each latency-bound
+        // replay chain; a second wave doubles the step), at least 4, at most 32.
+        // Measured on cfg 3 (13.4 k replays, 8 resident one-warp CTAs per SM): 16
+        // lanes 267 ms, 12 lanes (1 120 warps, one wave) 245 ms, 10 lanes (1 344 warps,
+        // two waves) 342 ms.  The 168-register variant next to a large stage C workload
+        // (cfg 4) keeps 32: there the joint warps' registers are what stage C waits for
+        // (25 lanes: 455 -> 466 ms), and its lanes refill.
         {
-            const long long UJ2 = (long long)n_traces * n_qps * P.n_clist;
+            const int wpc0 = tbj / 32;
+            const long long per_trace_cap = ((long long)ctx->n_sm * occj) / n_traces;   // CTAs per trace, one wave
+            const long long qc = (long long)n_qps * P.n_clist;
             int lpw = 32;
-            while (lpw > 4 && UJ2 / lpw < (long long)ctx->n_sm * 4) lpw >>= 1;
+            if (per_trace_cap > 0 && !ctx->j_r168)
+                lpw = (int)std::min<long long>(32, std::max<long long>(4, (qc + per_trace_cap * wpc0 - 1) /
+                                                                              (per_trace_cap * wpc0)));
             if (ctx->tune.joint_lanes_per_warp > 0) lpw = std::min(32, ctx->tune.joint_lanes_per_warp);
             P.lpw = ctx->j_grp ? kGPW : lpw;
         }

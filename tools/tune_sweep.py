@@ -25,6 +25,8 @@ ap.add_argument("--cand-stride", type=int, default=1, help="every k-th candidate
 ap.add_argument("--qps-stride", type=int, default=1,
                 help="QPS points q with q mod k == offset (one rank's shard of the strong split)")
 ap.add_argument("--qps-offset", type=int, default=0)
+ap.add_argument("--flush", action="store_true",
+                help="as bench.py: a 512 MiB device write and a synchronize before the measured run")
 ap.add_argument("tunings", nargs="+")
 a = ap.parse_args()
 
@@ -51,6 +53,12 @@ for _ in range(a.runs):
         ctx = pkg.Context(0, tuning=json.loads(t))
         ctx.plan(traces, qps, DEFAULT_MODEL, role, cap, pols, cfg["slo"], cfg["budget_w"], cand_budget_w=cb)
         ctx.run()                                  # warm-up
+        if a.flush:
+            import torch
+            fl = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+            fl.fill_(1.0)
+            torch.cuda.synchronize()
+            del fl
         ctx.run()
         ms[j].append(ctx.replay_kernel_ms())
         kms[j] = [round(x, 2) for x in ctx.kernel_times_ms()]
