@@ -672,7 +672,7 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
     {
         size_t off = 0;
         auto take = [&](size_t b) { size_t o = off; off += (b + 255) & ~(size_t)255; return o; };
-        const bool idx16 = Rm <= 32767;
+        const bool idx16 = Rm <= 16383;          // 14-bit stream index + round + chain flags
         ctx->fC_idx16 = idx16;
         const size_t isz = idx16 ? 2 : 4;
         take(Rm * 32 * isz);
@@ -681,7 +681,7 @@ static int plan_factorized(padsim_ctx* ctx, const padsim_model* model, const pad
         int wheel = 32;
         while (wheel < maxo) wheel <<= 1;        // finish steps lie in (step, step + out − 1]
         F.wheel = wheel;
-        F.c_off_heads = take((size_t)32 * kNW * wheel * isz);
+        F.c_off_heads = take((size_t)32 * kNW * wheel * isz);   // per lane KW × (Wh, or Wh / 2 for KW = 4 / 5)
         F.c_off_bits = take((size_t)kNW * (wheel / 32) * 32 * sizeof(unsigned));
         int rb = 1;
         while (rb < model->max_decode_batch) rb <<= 1;

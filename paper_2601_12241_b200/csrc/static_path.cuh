@@ -497,12 +497,24 @@ __device__ __forceinline__ void hca_wait() { asm volatile("cp.async.wait_all;" :
 template <bool CTX, typename IDX, int KW, bool BL>
 __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) {
     constexpr unsigned kMulti = sizeof(IDX) == 2 ? 0x8000u : 0x80000000u;
+    // kHalf (the KW = 4 / 5 classes, whose wheel heads were most of stage C's DRAM
+    // traffic): the heads have Wh / 2 buckets (bucket = finish step mod Hb); a bucket
+    // holds members of at most two finish steps, f and f + Hb (live finish steps lie
+    // in (step, step + Wh)), told apart by bit lgH of the finish step, carried in
+    // each chain entry (kRound); the occupancy bitmap stays exact (Wh bits).  Halves
+    // the heads' footprint (cfg 4 stage C DRAM 221 → ~124 GB) at no cost in time for
+    // those classes; the KW = 1 / 2 classes lose time to the extra chain filtering
+    // (+20 %), so they keep one bucket per finish step.
+    constexpr bool kHalf = KW == 4 || KW == 5;
+    constexpr unsigned kRound = sizeof(IDX) == 2 ? 0x4000u : 0x40000000u;
+    constexpr unsigned kIdMask = ~(kMulti | kRound);
     extern __shared__ __align__(128) unsigned char smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     char* wb = P.scrC + ((size_t)blockIdx.x * kWarps + warp) * P.c_warp_bytes;
     IDX* link = (IDX*)wb + lane;                                       // [k*32]
-    const int Wh = P.wheel, Wm = P.wheel - 1, nwords = P.wheel >> 5;
-    IDX* heads = (IDX*)(wb + P.c_off_heads) + (size_t)lane * KW * Wh;    // per lane
+    const int Wm = P.wheel - 1, nwords = P.wheel >> 5;
+    const int Hb = kHalf ? P.wheel >> 1 : P.wheel, Hm = Hb - 1, lgH = __ffs(Hb) - 1;
+    IDX* heads = (IDX*)(wb + P.c_off_heads) + (size_t)lane * KW * Hb;    // per lane
     const int max_db = P.m.max_db;
     CWork W;
     unsigned* bits;
@@ -662,7 +674,7 @@ __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) 
                 if (tf > __uint_as_float(mn) + win) continue;
             }
             inst++;
-            unsigned bnd = 0, touched = 0, eag = 0;
+            unsigned bnd = 0, touched = 0, eag = 0, hcok = 0;
 #pragma unroll
             for (int w = 0; w < KW; w++) if (tnext[w] == t) bnd |= 1u << w;
             // kind 3: materialised step boundaries, worker order
@@ -721,22 +733,47 @@ __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) 
                         W.nact[o] = n0 - left;
                         if (left < n0) mf = (int)(e >> 32);
                     } else {
-                        const int b = sN & Wm;
+                        const int b = sN & Wm;            // bitmap bit of the finish step
+                        const int hb = sN & Hm;           // its head bucket
+                        const unsigned rr = (kHalf && ((sN >> lgH) & 1)) ? kRound : 0u;
                         unsigned cur;
                         if (hca) {
                             hca_wait();
                             const unsigned wd = hcs[w * kThreads];
-                            cur = sizeof(IDX) == 2 ? ((b & 1) ? (wd >> 16) : (wd & 0xffffu)) : wd;
+                            cur = sizeof(IDX) == 2 ? ((hb & 1) ? (wd >> 16) : (wd & 0xffffu)) : wd;
                         } else {
-                            cur = (unsigned)heads[(size_t)w * Wh + b];
+                            cur = (unsigned)heads[(size_t)w * Hb + hb];
                         }
-                        for (;;) {
-                            const int kk = (int)(cur & ~kMulti);
-                            leave_member(kk);
-                            left++;
-                            if (!(cur & kMulti)) break;
-                            cur = (unsigned)link[(size_t)kk * 32];   // IDX → unsigned keeps the flag bit
+                        // members of finish step sN leave; those of sN + Hb (other
+                        // round bit) are re-chained as the bucket's new list
+                        unsigned keep = 0u;
+                        bool kept = false;
+                        if constexpr (kHalf) {
+                            for (;;) {
+                                const int kk = (int)(cur & kIdMask);
+                                const bool more = (cur & kMulti) != 0u;
+                                const unsigned nx = more ? (unsigned)link[(size_t)kk * 32] : 0u;   // IDX → unsigned keeps the flags
+                                if ((cur & kRound) == rr) {
+                                    leave_member(kk);
+                                    left++;
+                                } else {
+                                    if (kept) link[(size_t)kk * 32] = (IDX)keep;
+                                    keep = (unsigned)kk | (cur & kRound) | (kept ? kMulti : 0u);
+                                    kept = true;
+                                }
+                                if (!more) break;
+                                cur = nx;
+                            }
+                        } else {             // one finish step per bucket: every member leaves
+                            for (;;) {
+                                const int kk = (int)(cur & ~kMulti);
+                                leave_member(kk);
+                                left++;
+                                if (!(cur & kMulti)) break;
+                                cur = (unsigned)link[(size_t)kk * 32];   // IDX → unsigned keeps the flag bit
+                            }
                         }
+                        if (kept) heads[(size_t)w * Hb + hb] = (IDX)keep;
                         unsigned* bw = bits + (size_t)w * nwords * bstride;
                         bw[(size_t)(b >> 5) * bstride] &= ~(1u << (b & 31));
                         const int n = W.nact[o] - left;
@@ -750,6 +787,13 @@ __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) 
                                 mword = bw[(size_t)wi * bstride];
                             }
                             mf = sN + ((((wi << 5) + __ffs(mword) - 1) - b) & Wm);
+                        }
+                        // the kept members finish next (mf = sN + Hb): their new list is the
+                        // head of the next bucket — cache it here (the dispatch would
+                        // otherwise copy back what this thread just stored)
+                        if (hca && kept && (mf & Hm) == hb) {
+                            hcs[w * kThreads] = (sizeof(IDX) == 2 && (hb & 1)) ? (keep << 16) : keep;
+                            hcok |= 1u << w;
                         }
                     }
                     W.mfin[o] = mf;
@@ -828,7 +872,7 @@ __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) 
                 const int step = eg ? W.nxs[o] : W.stm[o];
                 int mf = W.mfin[o];
                 int h = W.qh[o];
-                IDX* hw = heads + (size_t)w * Wh;
+                IDX* hw = heads + (size_t)w * Hb;
                 unsigned* bw = bits + (size_t)w * nwords * bstride;
                 while (n < max_db && qn > 0) {
                     const int kk = h;
@@ -845,20 +889,25 @@ __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) 
                     if constexpr (BL) {
                         bl_insert(w, n, fin, kk);
                     } else {
-                        const int b = fin & Wm;
+                        const int b = fin & Wm;              // bitmap bit of the finish step
+                        const int fb = fin & Hm;             // its head bucket
+                        const unsigned ent = (unsigned)kk | ((kHalf && ((fin >> lgH) & 1)) ? kRound : 0u);
                         unsigned* wp = bw + (size_t)(b >> 5) * bstride;
                         const unsigned bit = 1u << (b & 31);
+                        const int b2 = b ^ Hb;               // the bucket's other finish step
                         const unsigned old = *wp;
-                        if (old & bit) {                     // bucket occupied: chain
-                            link[(size_t)kk * 32] = hw[b];
-                            hw[b] = (IDX)((unsigned)kk | kMulti);
+                        const bool occ = (old & bit) ||
+                                         (kHalf && (bw[(size_t)(b2 >> 5) * bstride] & (1u << (b2 & 31))));
+                        if (occ) {                           // bucket occupied: chain
+                            link[(size_t)kk * 32] = hw[fb];
+                            hw[fb] = (IDX)(ent | kMulti);
                         } else {
-                            hw[b] = (IDX)kk;
-                            *wp = old | bit;
+                            hw[fb] = (IDX)ent;
                         }
-                        if (fin <= mf) {                     // head of the earliest bucket
-                            hv = (old & bit) ? ((unsigned)kk | kMulti) : (unsigned)kk;
-                            hb = b;
+                        *wp = old | bit;
+                        if (fin <= mf || (kHalf && fb == (mf & Hm))) {   // head of the earliest bucket (or of its bucket)
+                            hv = occ ? (ent | kMulti) : ent;
+                            hb = fb;
                             hset = true;
                         }
                     }
@@ -901,11 +950,11 @@ __global__ void __maxnreg__(168) stageC_kernel(const __grid_constant__ FPlan P) 
                         if (hset) {
                             hca_wait();
                             hcs[w * kThreads] = (sizeof(IDX) == 2 && (hb & 1)) ? (hv << 16) : hv;
-                        } else if ((touched >> (w + 16)) & 1u) {   // after a leave: copy it in
-                            hca_issue(hcs + w * kThreads, hw + (mf & Wm));
+                        } else if (((touched >> (w + 16)) & 1u) && !((hcok >> w) & 1u)) {   // after a leave: copy it in
+                            hca_issue(hcs + w * kThreads, hw + (mf & Hm));
                         }
                     } else {
-                        pf_head(hw + (mf & Wm));
+                        pf_head(hw + (mf & Hm));
                     }
                     set_tnext(w, seg_bnd(ts0, L, dL, mf - s0, gr));
                 } else {
