@@ -470,7 +470,7 @@ struct CWork {            // per-thread shared-memory SoA views (stride kThreads
 constexpr size_t kCWorkSlotBytes = 2 * sizeof(double) + 8 * sizeof(int);
 constexpr size_t kCWorkCtxSlotBytes = 2 * sizeof(long long) + sizeof(double);
 // IDX: stream-index type of link[] and the wheel heads — uint16_t when
-// n_req ≤ 32767 (halves the scratch footprint and its DRAM/L2 traffic),
+// n_req ≤ 16383 (halves the scratch footprint and its DRAM/L2 traffic),
 // else uint32_t; the top bit flags "more members chained through link[]".
 // KW: decode-worker slots (2, 4 or 7).  Candidates are launched in classes by
 // their decode pool size y ≤ KW, so replays with few decode GPUs run with
