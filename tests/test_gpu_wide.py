@@ -125,3 +125,35 @@ def test_wide_empty_and_single_request(pkg):
     one = make_trace("lb", 1, 1)
     compare_records([empty, one, make_trace("lb", 2, 40)], [0.5, 8.0], DEFAULT_MODEL, role, cap, pols,
                     DEFAULT_SLO, 9600)
+
+
+def test_planner_static_path_choice(pkg):
+    # padsim_static_path: thread-per-replay stages for large N <= 8 workloads, the
+    # warp-per-replay stages for small ones (<= 8 static replays per SM) and for
+    # N > 8, the joint kernel when asked (records-only joint flag)
+    role, cap = static_candidates(8, [(4, 600, 600), (3, 700, 540)])
+    pols = [policy("static")] * 2
+    small = [make_trace("lb", 1, 50)]
+    ctx = pkg.Context(0)
+    try:
+        ctx.plan(small, [1.0], DEFAULT_MODEL, role, cap, pols, DEFAULT_SLO, 4800)
+        assert ctx.static_path() == "warp"
+        big = [make_trace("lb", s, 20) for s in range(16)]
+        many = [0.1 * k for k in range(1, 81)]          # 2 x 80 x 16 = 2560 > 8 per SM
+        ctx.plan(big, many, DEFAULT_MODEL, role, cap, pols, DEFAULT_SLO, 4800)
+        assert ctx.static_path() == "thread"
+        ctx.plan(small, [1.0], DEFAULT_MODEL, role, cap, pols, DEFAULT_SLO, 4800, joint=True)
+        assert ctx.static_path() == "joint"
+        r64, c64 = static_candidates(64, [(32, 600, 600)])
+        ctx.plan(small, [1.0], DEFAULT_MODEL, r64, c64, [policy("static")], DEFAULT_SLO, 38400)
+        assert ctx.static_path() == "warp"
+        ctx.plan(small, [1.0], DEFAULT_MODEL, role, cap, [policy("dyn-both")] * 2, DEFAULT_SLO, 4800)
+        assert ctx.static_path() == "none"
+    finally:
+        ctx.close()
+    ctx = pkg.Context(0, tuning=dict(wide_path=0))
+    try:
+        ctx.plan(small, [1.0], DEFAULT_MODEL, role, cap, pols, DEFAULT_SLO, 4800)
+        assert ctx.static_path() == "thread"
+    finally:
+        ctx.close()
