@@ -143,6 +143,20 @@ def test_edge_cases(pkg):
         compare_records(traces, [0.5, 3.0], m, role, cap, pols, DEFAULT_SLO, 4800)
 
 
+@pytest.mark.parametrize("classes", [3, 5])
+def test_short_outputs_small_wheel(pkg, classes):
+    # every output ≤ 32 tokens: the decode timing wheel is its minimum (32 finish steps),
+    # so the half-size heads of the KW = 4 / 5 classes have 16 buckets and a bucket's two
+    # finish steps are 16 apart; heavy load keeps both in use
+    rng = np.random.default_rng(11)
+    R = 600
+    tr = _tr(np.cumsum(rng.exponential(1.0, R)), rng.integers(256, 4096, R), rng.integers(1, 33, R))
+    role, cap = static_candidates(8, XPD)
+    compare_records([tr], [1.0, 4.0, 8.0], DEFAULT_MODEL,
+                    role, cap, [policy("static")] * len(XPD), DEFAULT_SLO, 4800,
+                    tuning=dict(stage_c_classes=classes, wide_path=0))
+
+
 def test_empty_trace(pkg):
     role, cap = static_candidates(8, [(4, 600, 600)])
     empty = _tr([], [], [])
