@@ -1341,9 +1341,9 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
         // replays per warp item: as few as still fit every warp in one wave of
         // resident warps (fewer lanes per warp = less divergence on each latency-bound
         // replay chain; a second wave doubles the step), at least 4, at most 32.
-        // Measured on cfg 3 (13.4 k replays, 8 resident one-warp CTAs per SM): 16
-        // lanes 267 ms, 12 lanes (1 120 warps, one wave) 245 ms, 10 lanes (1 344 warps,
-        // two waves) 342 ms.  The 168-register variant next to a large stage C workload
+        // Measured on cfg 3 (13.4 k replays, 8 resident one-warp CTAs per SM), back-to-back
+        // runs: 16 lanes 270 ms, 12 lanes (1 120 warps, one wave) 245 ms, 10 lanes (1 344
+        // warps, two waves) 342 ms; with the bench's L2 flush before each run 267 -> 264 ms.  The 168-register variant next to a large stage C workload
         // (cfg 4) keeps 32: there the joint warps' registers are what stage C waits for
         // (25 lanes: 455 -> 466 ms), and its lanes refill.
         {
