@@ -1010,11 +1010,12 @@ __global__ void __launch_bounds__(TB) __maxnreg__(MR) joint_kernel(const __grid_
         // stage C workload): the work counter counts replays; a warp's first lpw lanes
         // start on consecutive replays (u = q·n_clist + c: one arrival stream), and a
         // lane whose replay ends stores it and starts the next replay inside the same
-        // event loop instead of idling until the longest replay of its warp is done,
-        // so the warps — and the registers they hold next to stage C — are released
-        // sooner (cfg 4 461 → 452 ms/step; as the whole step, cfg 3, the lane clock
-        // window it has to give up is worth more: 270 → 324 ms).  Scheduling only:
-        // every replay is independent.
+        // event loop instead of idling until the longest replay of its warp is done
+        // (for grids smaller than the replay count; at cfg 4's size every lane has
+        // exactly one replay).  This variant runs without the lane clock window: next to
+        // stage C that is what pays (cfg 4 461 → 452 ms/step), while the joint replays
+        // of cfg 3, the whole step there, keep it (270 vs 324 ms without).  Scheduling
+        // only: every replay is independent.
         int u;
         {
             int first = 0;

@@ -1332,7 +1332,9 @@ int padsim_plan(padsim_ctx* ctx, const padsim_trace* traces, int32_t n_traces,
             jb = 0;
             fnj = jointg_fn(dyn != 0, cx, tbj);
         }
-        if (ctx->j_r168) P.sync_win = 0.f;     // it refills lanes (dynamic_path.cuh): no lane clock window
+        // next to stage C the joint replays run without the lane clock window (cfg 4 461 ->
+        // 452 ms; refilled lanes could not keep it anyway), see dynamic_path.cuh
+        if (ctx->j_r168) P.sync_win = 0.f;
         P.smem_trace_bytes = jb;
         CK(cudaFuncSetAttribute(fnj, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jb));
         int occj = 0;
