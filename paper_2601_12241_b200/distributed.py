@@ -150,6 +150,8 @@ def evaluate_sharded(traces, qps, model, role, cap, policies, slo, budget_w, ctx
             cb = None if cand_budget_w is None else np.asarray(cand_budget_w)[sh.cand]
             out = evaluate_allocations(traces, [qps[q] for q in sh.qps], model, role[sh.cand], cap[sh.cand],
                                        [policies[c] for c in sh.cand], slo, budget_w, ctx=ctx, cand_budget_w=cb)
+            if world == 1:          # one process: the call's own results (no exchange to do)
+                return {"met": out["met"], "goodput": out["goodput"], "argmax": out["argmax"]}
             met_l = torch.as_tensor(out["met"]).to(dev)
             good_l = torch.as_tensor(out["goodput"]).to(dev)
         else:
